@@ -1,0 +1,324 @@
+"""Benchmark of the fused slice + 2D-LUT apply (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+
+Workload (BASELINE.json configs[1], "config 2"): per rank one 3x2160x3840
+float32 smooth-field image with its own SVD factors / grids / weights
+(synth.make_case(seed=rank)); d_t=33, n_s=8, d_s=17, K=6.  A step is the whole
+hot path on one batch: LUT reconstruction from U,S,Vt + table packing + fused
+slice/LUT apply, as CUDA kernels on the current stream.  Four input/output
+buffer sets rotate between steps (4 x 199 MB > 126 MB L2), so every step
+streams from HBM.  Multi-GPU: one process per GPU (torchrun), each rank its
+own image (per-image sharding, no data-path collective) -> "scaling": "weak";
+time = max over ranks of the CUDA-event time (NCCL all_reduce MAX).
+
+Reported besides the contract keys:
+  roofline      fused-kernel achieved GB/s (24 B/pixel algorithmic) vs the
+                measured HBM copy peak in MEASURED_PEAKS.json
+  cpu_baseline  the CPU oracle port (op-for-op restatement of the reference's
+                numba kernel, bit-identical output) on all host cores, rank 0
+  e2e           the same metric through the reference-facing host API
+                (svd.reconstruct_lut + transform.fused_enhance on pinned
+                numpy arrays): H2D + kernels + D2H inside the timed region
+  clocks        NVML SM clocks / throttle reasons sampled during the timed region
+"""
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "megapixels/sec fused slice+LUT apply at 4K fp32"
+UNIT = "MP/s"
+H, W = 2160, 3840
+BYTES_PER_PX = 24  # read 3 x f32 + write 3 x f32
+N_ROT = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["mine", "reference"], default="mine")
+    ap.add_argument("--variant", type=int, default=-1, help="fused kernel lane mapping (0/1)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def workload_config(world):
+    return {
+        "workload": "config2: 1x3x2160x3840 fp32 smooth field per rank, d_t=33 n_s=8 d_s=17 K=6; "
+                    "step = reconstruct(U,S,Vt) + pack tables + fused slice/LUT apply",
+        "global_batch": world, "height": H, "width": W, "parallelism": f"per-image dp{world}",
+        "l2": f"{N_ROT} rotating input/output sets ({N_ROT * 2 * 3 * H * W * 4 // 2**20} MiB) > L2",
+    }
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML SM clock + throttle reasons, sampled every ~5 ms in a thread."""
+
+    REASONS = {
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown", 0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown", 0x0000000000000001: "gpu_idle",
+        0x0000000000000002: "applications_clocks_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 - clocks are best effort
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def cpu_reference(case, reps):
+    """Time the oracle port (bit-identical restatement of the reference numba
+    kernel) on all host cores over full frames; returns (MP/s, threads, sample)."""
+    import oracle
+
+    planes = oracle.reconstruct(case.u, case.s, case.vt)
+    threads = len(os.sched_getaffinity(0))
+    args = (case.rgb, planes, case.lw, case.lb, case.grid_planes, case.gw, case.gb)
+    oracle.fused_fwd(*args, threads=threads)  # warm-up
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.reconstruct(case.u, case.s, case.vt)
+        oracle.fused_fwd(*args, threads=threads)
+        times.append(time.perf_counter() - t0)
+    med = float(np.median(times))
+    return H * W / med / 1e6, threads, med, times
+
+
+def run_reference_arm(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2508_16121_b200 import synth
+
+    case = synth.make_case(0)
+    k = max(1, a.steps)
+    mps, threads, med, times = cpu_reference(case, k + max(0, a.warmup))
+    times = times[max(0, a.warmup):] or times
+    total = sum(times)
+    value = H * W * len(times) / total / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": world, "steps": len(times), "warmup": a.warmup,
+        "ms_per_step": round(1e3 * total / len(times), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(1),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": "full 3x2160x3840 frame per step (reconstruct + fused apply), "
+                                   "oracle/svdlut_oracle.c on pthreads"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference_arm(a)
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    import __graft_entry__
+
+    __graft_entry__.build_library()
+    from paper_2508_16121_b200 import device, svd, synth, transform
+    from paper_2508_16121_b200.core_types import (GridSet, GridWeights, Image, LutWeights,
+                                                  SvdLut)
+
+    case = synth.make_case(rank)
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    p = {k: T(getattr(case, k)) for k in ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")}
+    base = T(case.rgb)[None]
+    ins = [base] + [torch.roll(base, shifts=17 * i, dims=3).contiguous() for i in range(1, N_ROT)]
+    outs = [torch.empty_like(base) for _ in range(N_ROT)]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        planes = device.reconstruct(p["u"], p["s"], p["vt"])
+        tables = device.pack_tables(planes, p["lw"], p["lb"], p["grid_planes"], p["gw"], p["gb"])
+        device.apply(ins[i % N_ROT], tables, out=outs[i % N_ROT], variant=a.variant)
+        return tables
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(max(3, a.warmup)):
+        step(i)
+    barrier()
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for i in range(a.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        # keep the clock sampler under load for >= 0.3 s (the timed region is short)
+        t_end = time.perf_counter() + 0.3
+        i = 0
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                step(i)
+                i += 1
+            torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / a.steps
+    ms = max_over_ranks(ms)
+    barrier()
+
+    # ---- roofline: the fused kernel alone, event-timed on its stream -------------
+    tables = step(0)
+    torch.cuda.synchronize(dev)
+    kreps = max(20, a.steps)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for i in range(kreps):
+        device.apply(ins[i % N_ROT], tables, out=outs[i % N_ROT], variant=a.variant)
+    k1.record(stream)
+    torch.cuda.synchronize(dev)
+    kms = k0.elapsed_time(k1) / kreps
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        peak = float(json.load(open(peaks_path))["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    achieved = BYTES_PER_PX * H * W / (kms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_fused_fwd.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "svdlut::fused_fwd_kernel", "kernel_ms": round(kms, 5),
+                "algorithmic_bytes_per_launch": BYTES_PER_PX * H * W, "peak_source": peak_src}
+
+    # ---- e2e through the reference-facing host API --------------------------------
+    e2e = None
+    if not a.no_e2e:
+        pin = torch.empty((3, H, W), dtype=torch.float32, pin_memory=True)
+        pin.copy_(torch.from_numpy(case.rgb))
+        img = Image(W, H, pin.numpy())
+        factors = SvdLut(case.u, case.s, case.vt)
+        lw = LutWeights(case.lw, case.lb)
+        grids, gw = GridSet(case.grid_planes), GridWeights(case.gw, case.gb)
+        for _ in range(2):
+            transform.fused_enhance(img, svd.reconstruct_lut(factors), lw, grids, gw)
+        barrier()
+        esteps = max(3, min(a.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(esteps):
+            y = transform.fused_enhance(img, svd.reconstruct_lut(factors), lw, grids, gw)
+        t1 = time.perf_counter()
+        ems = max_over_ranks(1e3 * (t1 - t0) / esteps)
+        table_h2d = 4 * (case.u.size + case.s.size + case.vt.size + 9 * 33 * 33 + 12
+                         + case.grid_planes.size + case.gw.size + case.gb.size)
+        e2e = {"value": round(world * H * W / (ems * 1e-3) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": int(case.rgb.nbytes + table_h2d),
+               "d2h_bytes_per_step": int(y.data.nbytes + 9 * 33 * 33 * 4),
+               "ms_per_step": round(ems, 4),
+               "api": "svd.reconstruct_lut + transform.fused_enhance (pinned host arrays)"}
+
+    cpu = None
+    if rank == 0 and not a.no_cpu:
+        mps, threads, med, _ = cpu_reference(case, 3)
+        cpu = {"value": round(mps, 3), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"full 3x2160x3840 frame, median of 3 ({med * 1e3:.1f} ms), "
+                         "oracle/svdlut_oracle.c on pthreads"}
+
+    if world > 1:
+        torch.distributed.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(world * H * W / (ms * 1e-3) / 1e6, 3), "unit": UNIT,
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded smooth field, SURVEY.md §8d recipe)",
+            "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": 4 * a.steps, "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

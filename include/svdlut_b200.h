@@ -1,0 +1,165 @@
+/*
+ * svdlut_b200.h — C ABI of the B200-native SVDLUT apply path (sm_100a).
+ *
+ * Drop-in boundary for the reference operator surface
+ * (/root/reference/pkg/src/svdlut):
+ *
+ *   svdlut_fused_fwd          replaces transform.fused_enhance / _fused_impl
+ *                             (transform.py:308-353, kernel transform.py:215-300)
+ *   svdlut_fused_fwd_exact    same, f64 op-for-op (bit-identical to the reference)
+ *   svdlut_reconstruct        replaces svd.reconstruct_lut (svd.py:210-220)
+ *   svdlut_pack_tables        the on-device table prologue the fused kernel reads
+ *   svdlut_fused_bwd /        backward of the apply and of the reconstruction
+ *   svdlut_reconstruct_bwd    (no reference counterpart)
+ *   svdlut_indices            per-pixel cell selection (interp.py:35-45,
+ *                             transform.py:144-149) for the bit-exact index test
+ *   svdlut_enhance_host       host-buffer entry (H2D + apply + D2H pipelined)
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no framework types.  `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - All device buffers are caller-owned (no allocation inside a call except
+ *     in svdlut_ctx_*, which owns its own staging buffers).
+ *   - Images are planar float32 (B, 3, H, W) C-contiguous; channel order r,g,b.
+ *   - LUT planes (B, 3, 3, d_t, d_t): [out channel][pair rg|rb|gb][a][b],
+ *     first plane axis = first named channel (core_types.py:119-125).
+ *   - Grid planes (B, K, 3, d_s, d_s): [grid][xy|xc|yc][a][b]; grid k reads
+ *     guide channel k%3 and adds into output channel k%3 (transform.py:269-297).
+ *   - (y0, h_total): the call covers rows y0..y0+H-1 of an image with h_total
+ *     rows; positions are normalised by the global h_total-1 (row strips).
+ *   - Return value is an svdlut_status; svdlut_last_error() gives the message
+ *     (thread-local).  Status codes map 1:1 onto the reference exception
+ *     classes (errors.py:4-31), see INTEGRATION.md.
+ *   - Stream-ordered and thread-safe across streams.
+ */
+#ifndef SVDLUT_B200_H
+#define SVDLUT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SVDLUT_OK = 0,
+  SVDLUT_ERR_DIMENSION_MISMATCH = 1, /* errors.DimensionMismatch */
+  SVDLUT_ERR_DEGENERATE_IMAGE = 2,   /* errors.DegenerateImage (W or H_total < 2) */
+  SVDLUT_ERR_BAD_GRID_COUNT = 3,     /* errors.BadGridCount (K % 3 != 0) */
+  SVDLUT_ERR_BAD_VERTEX_COUNT = 4,   /* errors.BadVertexCount (d < 2) */
+  SVDLUT_ERR_NON_FINITE = 5,         /* errors.NonFiniteValue */
+  SVDLUT_ERR_INVALID_ARGUMENT = 6,   /* NULL pointer, misaligned buffer, bad size */
+  SVDLUT_ERR_UNSUPPORTED = 7,        /* dims beyond the fast kernel (use _exact) */
+  SVDLUT_ERR_CUDA = 8                /* CUDA runtime error (message has details) */
+} svdlut_status;
+
+int svdlut_version(void);
+const char* svdlut_last_error(void);
+const char* svdlut_status_name(int status);
+
+/* ---- table prologue ---------------------------------------------------- */
+
+/* Bytes of one image's packed tables (LUT coefficient cells + merged grid
+ * cells), or 0 if (d_t, d_s) are invalid. */
+size_t svdlut_table_bytes(int d_t, int d_s);
+
+/* 1 if the fast fused kernel supports (d_t, d_s) (tables fit in shared
+ * memory), else 0. */
+int svdlut_fast_supported(int d_t, int d_s);
+
+/* Bytes of workspace svdlut_fused_fwd needs for a call of this shape. */
+size_t svdlut_workspace_bytes(int batch, int h, int w, int d_t, int d_s);
+
+/* svd.reconstruct_lut, batched: planes[b,c,p] = f32((f64 u * f64 s) @ f64 vt).
+ * u (B,3,3,d_t,n_s), s (B,3,3,n_s), vt (B,3,3,n_s,d_t) -> planes (B,3,3,d_t,d_t). */
+int svdlut_reconstruct(const float* u, const float* s, const float* vt, int batch, int d_t,
+                       int n_s, float* planes, void* stream);
+
+/* Fold weights into the LUT planes, merge the K grids per output channel and
+ * write each image's coefficient tables (svdlut_table_bytes each, 16 B
+ * aligned) into `tables`. */
+int svdlut_pack_tables(const float* lut_planes, const float* lw, const float* lb, int d_t,
+                       const float* grid_planes, const float* gw, const float* gb, int k,
+                       int d_s, int batch, void* tables, void* stream);
+
+/* ---- forward ------------------------------------------------------------ */
+
+/* Fused slice + 2D-LUT apply from packed tables (fast fp32 kernel, within
+ * 1e-5 of the reference; cell selection bit-exact).  `workspace` holds the
+ * spatial bracket tables: svdlut_workspace_bytes(...) - batch*table_bytes
+ * is enough; pass the tail of the fused workspace or a separate buffer. */
+int svdlut_fused_fwd_packed(const float* rgb, int batch, int h, int w, int y0, int h_total,
+                            const void* tables, int d_t, int d_s, float* out, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* As svdlut_fused_fwd_packed, plus: `nonfinite` (device int, may be NULL) is
+ * OR-ed with 1 if any output sample is NaN/Inf (the check core_types.py:55-59
+ * does on the host), and `variant` picks the lane->pixel mapping: 0 = four
+ * consecutive pixels per lane (128-bit I/O), 1 = interleaved lanes (a warp
+ * instruction covers 32 consecutive pixels), -1 = default. */
+int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0, int h_total,
+                               const void* tables, int d_t, int d_s, float* out, void* workspace,
+                               size_t workspace_bytes, int* nonfinite, int variant, void* stream);
+
+/* Reference-shaped entry: pack + apply.  `workspace` >= svdlut_workspace_bytes. */
+int svdlut_fused_fwd(const float* rgb, int batch, int h, int w, int y0, int h_total,
+                     const float* lut_planes, const float* lw, const float* lb, int d_t,
+                     const float* grid_planes, const float* gw, const float* gb, int k, int d_s,
+                     float* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* f64 op-for-op restatement of transform.py:215-300: output is bitwise equal
+ * to the reference fused_enhance.  Any d_t, d_s >= 2, any K % 3 == 0. */
+int svdlut_fused_fwd_exact(const float* rgb, int batch, int h, int w, int y0, int h_total,
+                           const float* lut_planes, const float* lw, const float* lb, int d_t,
+                           const float* grid_planes, const float* gw, const float* gb, int k,
+                           int d_s, float* out, void* stream);
+
+/* Cell selection exactly as the fast kernel computes it:
+ * idx (B, 8, H, W) int32 = ir, ig, ib (vs d_t), jr, jg, jb (vs d_s), jx, jy. */
+int svdlut_indices(const float* rgb, int batch, int h, int w, int y0, int h_total, int d_t,
+                   int d_s, int32_t* idx, void* stream);
+
+/* ---- backward ----------------------------------------------------------- */
+
+/* Bytes of scratch svdlut_fused_bwd needs. */
+size_t svdlut_bwd_workspace_bytes(int batch, int h, int w, int d_t, int d_s, int k);
+
+/* Gradients of the fused apply given gy (B,3,H,W).  Outputs are OVERWRITTEN:
+ * gx (B,3,H,W) (may be NULL), dlut_planes (B,3,3,d_t,d_t), dlw (B,3,3),
+ * dlb (B,3), dgrid_planes (B,K,3,d_s,d_s), dgw (B,K,3), dgb (B,K). */
+int svdlut_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w, int y0,
+                     int h_total, const float* lut_planes, const float* lw, int d_t,
+                     const float* grid_planes, const float* gw, int k, int d_s, float* gx,
+                     float* dlut_planes, float* dlw, float* dlb, float* dgrid_planes,
+                     float* dgw, float* dgb, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/* Backward of svdlut_reconstruct: du, ds, dvt (overwritten) from dplanes. */
+int svdlut_reconstruct_bwd(const float* u, const float* s, const float* vt,
+                           const float* dplanes, int batch, int d_t, int n_s, float* du,
+                           float* ds, float* dvt, void* stream);
+
+/* ---- host-buffer entry (end-to-end) ------------------------------------ */
+
+typedef struct svdlut_ctx svdlut_ctx;
+
+/* A context owns streams, device scratch and pinned staging on `device`. */
+svdlut_ctx* svdlut_ctx_create(int device);
+void svdlut_ctx_destroy(svdlut_ctx* ctx);
+
+/* One image from HOST memory to HOST memory: H2D of rgb + tables, pack,
+ * apply, D2H of out, pipelined over row strips on two streams.  Host buffers
+ * may be pinned (DMA directly) or pageable (staged).  Blocks until `out` is
+ * written.  exact != 0 selects the f64 kernel.  *nonfinite (optional) is set
+ * to 1 if any output sample is NaN/Inf. */
+int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
+                        const float* lut_planes, const float* lw, const float* lb, int d_t,
+                        const float* grid_planes, const float* gw, const float* gb, int k,
+                        int d_s, float* out, int exact, int* nonfinite);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SVDLUT_B200_H */

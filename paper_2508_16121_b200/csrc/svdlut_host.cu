@@ -1,0 +1,179 @@
+// svdlut_host.cu — host-buffer entry point (svdlut_enhance_host) and its
+// context: the end-to-end path a host caller (the reference's numpy Image)
+// goes through.  H2D of the image, table prologue, fused apply and D2H of the
+// result run as a pipeline over row strips on two streams, so the PCIe copies
+// in both directions overlap each other and the kernels (strips are
+// independent thanks to the (y0, h_total) contract).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/svdlut_b200.h"
+#include "svdlut_common.cuh"
+#include "svdlut_internal.h"
+
+using namespace svdlut;
+
+extern "C" int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0,
+                                          int h_total, const void* tables, int d_t, int d_s,
+                                          float* out, void* workspace, size_t workspace_bytes,
+                                          int* nonfinite, int variant, void* stream);
+
+struct svdlut_ctx {
+  int device = 0;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ev_tables = nullptr;
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  void* d_img = nullptr;  // input strips followed by output strips
+  size_t d_img_bytes = 0;
+  void* d_par = nullptr;  // parameters + packed tables + workspaces
+  size_t d_par_bytes = 0;
+  int* h_flag = nullptr;  // pinned flag readback
+  std::mutex mu;
+};
+
+namespace {
+
+cudaError_t ensure(void** buf, size_t* have, size_t need) {
+  if (*have >= need) return cudaSuccess;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(buf, need);
+  if (e == cudaSuccess) *have = need;
+  return e;
+}
+
+size_t rup(size_t v) { return (v + 255) / 256 * 256; }
+
+}  // namespace
+
+extern "C" {
+
+svdlut_ctx* svdlut_ctx_create(int device) {
+  svdlut_ctx* c = new svdlut_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete c;
+    return nullptr;
+  }
+  bool ok = true;
+  for (int i = 0; i < 2; ++i) {
+    ok &= cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) == cudaSuccess;
+    ok &= cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+  ok &= cudaEventCreateWithFlags(&c->ev_tables, cudaEventDisableTiming) == cudaSuccess;
+  ok &= cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault) == cudaSuccess;
+  if (!ok) {
+    svdlut_ctx_destroy(c);
+    return nullptr;
+  }
+  return c;
+}
+
+void svdlut_ctx_destroy(svdlut_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (int i = 0; i < 2; ++i) {
+    if (c->st[i]) cudaStreamSynchronize(c->st[i]);
+  }
+  if (c->d_img) cudaFree(c->d_img);
+  if (c->d_par) cudaFree(c->d_par);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
+  for (int i = 0; i < 2; ++i) {
+    if (c->st[i]) cudaStreamDestroy(c->st[i]);
+    if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+  }
+  if (c->ev_tables) cudaEventDestroy(c->ev_tables);
+  delete c;
+}
+
+int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
+                        const float* lut_planes, const float* lw, const float* lb, int d_t,
+                        const float* grid_planes, const float* gw, const float* gb, int k,
+                        int d_s, float* out, int exact, int* nonfinite) {
+  if (!ctx) return SVDLUT_ERR_INVALID_ARGUMENT;
+  if (!rgb || !out || !lut_planes || !lw || !lb || !grid_planes || !gw || !gb)
+    return SVDLUT_ERR_INVALID_ARGUMENT;
+  if (k % 3 != 0 || k < 1) return k < 1 ? SVDLUT_ERR_DIMENSION_MISMATCH : SVDLUT_ERR_BAD_GRID_COUNT;
+  if (w < 2 || h < 2) return SVDLUT_ERR_DEGENERATE_IMAGE;
+  if (d_t < 2 || d_s < 2) return SVDLUT_ERR_BAD_VERTEX_COUNT;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  const bool fast = !exact && svdlut_fast_supported(d_t, d_s);
+
+  // ---- device buffers -------------------------------------------------------
+  const size_t n_lut = 9ull * d_t * d_t, n_grid = (size_t)k * 3 * d_s * d_s;
+  const size_t par_floats = n_lut + 9 + 3 + n_grid + 3ull * k + k;
+  const size_t tb = fast ? svdlut_table_bytes(d_t, d_s) : 0;
+  const size_t ws = svdlut_workspace_bytes(1, h, w, d_t, d_s);
+  const size_t par_bytes = rup(par_floats * 4) + rup(tb) + 2 * rup(ws) + 256;
+  const size_t img_bytes = 2 * rup((size_t)3 * h * w * 4);
+  if (ensure(&ctx->d_img, &ctx->d_img_bytes, img_bytes) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (ensure(&ctx->d_par, &ctx->d_par_bytes, par_bytes) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  float* d_in = (float*)ctx->d_img;
+  float* d_out = (float*)((char*)ctx->d_img + rup((size_t)3 * h * w * 4));
+  float* d_lut = (float*)ctx->d_par;
+  float* d_lw = d_lut + n_lut;
+  float* d_lb = d_lw + 9;
+  float* d_grid = d_lb + 3;
+  float* d_gw = d_grid + n_grid;
+  float* d_gb = d_gw + 3ull * k;
+  char* d_tables = (char*)ctx->d_par + rup(par_floats * 4);
+  char* d_ws = d_tables + rup(tb);
+  int* d_flag = (int*)(d_ws + 2 * rup(ws));
+
+  cudaStream_t s0 = ctx->st[0];
+  // ---- parameters + table prologue on stream 0 -----------------------------
+  float* dst[6] = {d_lut, d_lw, d_lb, d_grid, d_gw, d_gb};
+  const float* src[6] = {lut_planes, lw, lb, grid_planes, gw, gb};
+  const size_t cnt[6] = {n_lut, 9, 3, n_grid, 3ull * k, (size_t)k};
+  for (int i = 0; i < 6; ++i)
+    if (cudaMemcpyAsync(dst[i], src[i], cnt[i] * 4, cudaMemcpyHostToDevice, s0) != cudaSuccess)
+      return SVDLUT_ERR_CUDA;
+  if (cudaMemsetAsync(d_flag, 0, sizeof(int), s0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (fast) {
+    int rc = svdlut_pack_tables(d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb, k, d_s, 1, d_tables, s0);
+    if (rc != SVDLUT_OK) return rc;
+  }
+  if (cudaEventRecord(ctx->ev_tables, s0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+
+  // ---- strip pipeline -------------------------------------------------------
+  const size_t plane = (size_t)h * w;
+  const int n_strips = h >= 64 ? (h >= 1024 ? 8 : 4) : 1;
+  for (int s = 0; s < n_strips; ++s) {
+    const int r0 = (int)((long long)h * s / n_strips), r1 = (int)((long long)h * (s + 1) / n_strips);
+    const int hs = r1 - r0;
+    if (hs == 0) continue;
+    cudaStream_t st = ctx->st[s & 1];
+    if (cudaStreamWaitEvent(st, ctx->ev_tables, 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+    float* din = d_in + (size_t)3 * r0 * w;    // strip-major device layout (3, hs, w)
+    float* dout = d_out + (size_t)3 * r0 * w;
+    // 3 channel rows of the strip: one 2D copy (pitch = plane)
+    if (cudaMemcpy2DAsync(din, (size_t)hs * w * 4, rgb + (size_t)r0 * w, plane * 4,
+                          (size_t)hs * w * 4, 3, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return SVDLUT_ERR_CUDA;
+    int rc;
+    if (fast) {
+      rc = svdlut_fused_fwd_packed_ex(din, 1, hs, w, r0, h, d_tables, d_t, d_s, dout,
+                                      d_ws + (s & 1) * rup(ws), ws, d_flag, -1, st);
+    } else {
+      rc = svdlut_fused_fwd_exact(din, 1, hs, w, r0, h, d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb,
+                                  k, d_s, dout, st);
+    }
+    if (rc != SVDLUT_OK) return rc;
+    if (cudaMemcpy2DAsync(out + (size_t)r0 * w, plane * 4, dout, (size_t)hs * w * 4,
+                          (size_t)hs * w * 4, 3, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return SVDLUT_ERR_CUDA;
+  }
+  cudaStream_t s1 = ctx->st[1];
+  if (cudaEventRecord(ctx->ev_done[1], s1) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (cudaStreamWaitEvent(s0, ctx->ev_done[1], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (cudaMemcpyAsync(ctx->h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s0) != cudaSuccess)
+    return SVDLUT_ERR_CUDA;
+  if (cudaStreamSynchronize(s0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (nonfinite) *nonfinite = fast ? *ctx->h_flag : 0;
+  return SVDLUT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,43 @@
+// svdlut_internal.h — launchers shared between the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include "svdlut_common.cuh"
+
+namespace svdlut {
+
+cudaError_t launch_reconstruct(const float* u, const float* s, const float* vt, int batch, int dt,
+                               int ns, float* planes, cudaStream_t st);
+cudaError_t launch_pack(const float* lp, const float* lw, const float* lb, const float* gp,
+                        const float* gw, const float* gb, int k, const TableLayout& L, int batch,
+                        float* tables, cudaStream_t st);
+cudaError_t launch_spatial(int w, int h, int y0, int h_total, int ds, SpatialBr* col,
+                           SpatialBr* row, cudaStream_t st);
+
+// Fast fused forward from packed tables.  `variant` selects the lane→pixel
+// mapping (see svdlut_fwd.cu); -1 = default.
+cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w,
+                             const float* tables, const TableLayout& L, const SpatialBr* col,
+                             const SpatialBr* row, int* nonfinite, int variant, cudaStream_t st);
+
+cudaError_t launch_fused_exact(const float* rgb, float* out, int batch, int h, int w, int y0,
+                               int h_total, const float* lp, const float* lw, const float* lb,
+                               int dt, const float* gp, const float* gw, const float* gb, int k,
+                               int ds, cudaStream_t st);
+
+cudaError_t launch_indices(const float* rgb, int batch, int h, int w, int y0, int h_total,
+                           int dt, int ds, int32_t* idx, cudaStream_t st);
+
+cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w, int y0,
+                             int h_total, const float* lp, const float* lw, int dt,
+                             const float* gp, const float* gw, int k, int ds, float* gx,
+                             float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
+                             float* dgb, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t bwd_workspace_bytes(int batch, int h, int w, int dt, int ds, int k);
+
+cudaError_t launch_reconstruct_bwd(const float* u, const float* s, const float* vt,
+                                   const float* dplanes, int batch, int dt, int ns, float* du,
+                                   float* ds, float* dvt, cudaStream_t st);
+
+int fwd_max_smem_bytes();
+
+}  // namespace svdlut

@@ -1,0 +1,191 @@
+// svdlut_prep.cu — table prologue kernels (K1): LUT reconstruction from SVD
+// factors, weight folding / grid merging into coefficient cells, and the
+// spatial bracket tables.  All tiny (≈60 KB of tables per image); launched
+// once per call on the caller's stream.
+#include "svdlut_common.cuh"
+#include "svdlut_internal.h"
+
+namespace svdlut {
+
+// svd.py:210-220: planes[c,p] = f32((f64(u) * f64(s)) @ f64(vt)).
+// One CTA per (plane, image); each thread owns output entries.  The f64
+// product u*s is exact; the n-term sum runs in index order without FMA.
+__global__ void reconstruct_kernel(const float* __restrict__ u, const float* __restrict__ s,
+                                   const float* __restrict__ vt, int dt, int ns,
+                                   float* __restrict__ planes) {
+  const int cp = blockIdx.x;  // 0..8
+  const long long b = blockIdx.y;
+  const float* U = u + (b * 9 + cp) * (long long)dt * ns;
+  const float* S = s + (b * 9 + cp) * (long long)ns;
+  const float* V = vt + (b * 9 + cp) * (long long)ns * dt;
+  float* P = planes + (b * 9 + cp) * (long long)dt * dt;
+  for (int e = threadIdx.x; e < dt * dt; e += blockDim.x) {
+    const int i = e / dt, j = e - i * dt;
+    double acc = 0.0;
+    for (int m = 0; m < ns; ++m) {
+      double us = __dmul_rn((double)U[i * ns + m], (double)S[m]);
+      acc = __dadd_rn(acc, __dmul_rn(us, (double)V[m * dt + j]));
+    }
+    P[e] = (float)acc;
+  }
+}
+
+// Coefficients of the bilinear form on one cell from its 4 corner values.
+struct Coef {
+  float a, b, c, d;
+};
+__device__ __forceinline__ Coef cell_coef(double p00, double p10, double p01, double p11) {
+  Coef k;
+  k.a = (float)p00;
+  k.b = (float)(p10 - p00);
+  k.c = (float)(p01 - p00);
+  k.d = (float)((p11 - p10) - (p01 - p00));
+  return k;
+}
+
+// Packs one image's tables (layout in svdlut_common.cuh).  grid.y = image.
+__global__ void pack_kernel(const float* __restrict__ lp, const float* __restrict__ lw,
+                            const float* __restrict__ lb, const float* __restrict__ gp,
+                            const float* __restrict__ gw, const float* __restrict__ gb, int k,
+                            TableLayout L, float* __restrict__ tables) {
+  const long long b = blockIdx.y;
+  const int dt = L.dt, ds = L.ds;
+  const float* P = lp + b * 9LL * dt * dt;
+  const float* W = lw + b * 9;
+  const float* Bl = lb + b * 3;
+  const float* G = gp + b * (long long)k * 3 * ds * ds;
+  const float* GW = gw + b * (long long)k * 3;
+  const float* GB = gb + b * (long long)k;
+  float* T = tables + b * (long long)L.total_floats;
+
+  const int n_lut = 3 * (dt - 1) * L.cst;     // cells incl. padding
+  const int n_xy = (ds - 1) * L.css;
+  const int n_xc = 3 * (ds - 1) * L.css;
+  const int n_yc = n_xc;
+  const int total = n_lut + n_xy + n_xc + n_yc + (L.total_floats - (L.yc_off + 12 * (ds - 1) * L.css));
+  const int tid0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = gridDim.x * blockDim.x;
+
+  for (int e = tid0; e < total; e += stride) {
+    if (e < n_lut) {
+      const int p = e / ((dt - 1) * L.cst);
+      const int rem = e - p * (dt - 1) * L.cst;
+      const int i = rem / L.cst, j = rem - i * L.cst;
+      float v[12];
+      for (int c = 0; c < 3; ++c) {
+        Coef q = {0.f, 0.f, 0.f, 0.f};
+        if (j < dt - 1) {
+          const float* pl = P + (c * 3 + p) * dt * dt;
+          const double w = (double)W[c * 3 + p];
+          q = cell_coef(w * pl[i * dt + j], w * pl[(i + 1) * dt + j], w * pl[i * dt + j + 1],
+                        w * pl[(i + 1) * dt + j + 1]);
+        }
+        v[c] = q.a;
+        v[3 + c] = q.b;
+        v[6 + c] = q.c;
+        v[9 + c] = q.d;
+      }
+      float* dst = T + L.lut_off + e * 12;
+      for (int t = 0; t < 12; ++t) dst[t] = v[t];
+      continue;
+    }
+    int r = e - n_lut;
+    if (r < n_xy) {
+      const int jx = r / L.css, jy = r - jx * L.css;
+      float v[12];
+      for (int c = 0; c < 3; ++c) {
+        Coef q = {0.f, 0.f, 0.f, 0.f};
+        if (jy < ds - 1) {
+          double p00 = 0, p10 = 0, p01 = 0, p11 = 0;
+          for (int kk = c; kk < k; kk += 3) {
+            const float* pl = G + (kk * 3 + 0) * ds * ds;
+            const double w = (double)GW[kk * 3 + 0];
+            p00 += w * pl[jx * ds + jy];
+            p10 += w * pl[(jx + 1) * ds + jy];
+            p01 += w * pl[jx * ds + jy + 1];
+            p11 += w * pl[(jx + 1) * ds + jy + 1];
+          }
+          q = cell_coef(p00, p10, p01, p11);
+        }
+        v[c] = q.a;
+        v[3 + c] = q.b;
+        v[6 + c] = q.c;
+        v[9 + c] = q.d;
+      }
+      float* dst = T + L.xy_off + r * 12;
+      for (int t = 0; t < 12; ++t) dst[t] = v[t];
+      continue;
+    }
+    r -= n_xy;
+    if (r < n_xc + n_yc) {
+      const int plane = r < n_xc ? 1 : 2;  // xc or yc
+      if (r >= n_xc) r -= n_xc;
+      const int c = r / ((ds - 1) * L.css);
+      const int rem = r - c * (ds - 1) * L.css;
+      const int ja = rem / L.css, jc = rem - ja * L.css;
+      Coef q = {0.f, 0.f, 0.f, 0.f};
+      if (jc < ds - 1) {
+        double p00 = 0, p10 = 0, p01 = 0, p11 = 0;
+        for (int kk = c; kk < k; kk += 3) {
+          const float* pl = G + (kk * 3 + plane) * ds * ds;
+          const double w = (double)GW[kk * 3 + plane];
+          p00 += w * pl[ja * ds + jc];
+          p10 += w * pl[(ja + 1) * ds + jc];
+          p01 += w * pl[ja * ds + jc + 1];
+          p11 += w * pl[(ja + 1) * ds + jc + 1];
+        }
+        if (plane == 2) {
+          // fold the channel's total bias lb[c] + sum gb[k] into the constant term
+          double bias = (double)Bl[c];
+          for (int kk = c; kk < k; kk += 3) bias += (double)GB[kk];
+          p00 += bias;
+          p10 += bias;
+          p01 += bias;
+          p11 += bias;
+        }
+        q = cell_coef(p00, p10, p01, p11);
+      }
+      float* dst = T + (plane == 1 ? L.xc_off : L.yc_off) + r * 4;
+      dst[0] = q.a;
+      dst[1] = q.b;
+      dst[2] = q.c;
+      dst[3] = q.d;
+      continue;
+    }
+    r -= n_xc + n_yc;
+    T[L.yc_off + 12 * (ds - 1) * L.css + r] = 0.f;  // tail padding
+  }
+}
+
+// Column brackets for x in [0, w) and row brackets for rows y0..y0+h-1 of h_total.
+__global__ void spatial_kernel(int w, int h, int y0, int h_total, int ds, SpatialBr* __restrict__ col,
+                               SpatialBr* __restrict__ row) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < w) col[t] = spatial_bracket(t, w, ds);
+  if (t < h) row[t] = spatial_bracket(y0 + t, h_total, ds);
+}
+
+cudaError_t launch_reconstruct(const float* u, const float* s, const float* vt, int batch, int dt,
+                               int ns, float* planes, cudaStream_t st) {
+  dim3 grid(9, batch);
+  reconstruct_kernel<<<grid, 256, 0, st>>>(u, s, vt, dt, ns, planes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const float* lp, const float* lw, const float* lb, const float* gp,
+                        const float* gw, const float* gb, int k, const TableLayout& L, int batch,
+                        float* tables, cudaStream_t st) {
+  const int items = 3 * (L.dt - 1) * L.cst + 7 * (L.ds - 1) * L.css + 32;
+  dim3 grid((items + 255) / 256, batch);
+  pack_kernel<<<grid, 256, 0, st>>>(lp, lw, lb, gp, gw, gb, k, L, tables);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spatial(int w, int h, int y0, int h_total, int ds, SpatialBr* col, SpatialBr* row,
+                           cudaStream_t st) {
+  const int n = w > h ? w : h;
+  spatial_kernel<<<(n + 255) / 256, 256, 0, st>>>(w, h, y0, h_total, ds, col, row);
+  return cudaGetLastError();
+}
+
+}  // namespace svdlut

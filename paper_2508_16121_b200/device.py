@@ -1,0 +1,220 @@
+"""Device-tensor API over the C ABI (torch is the allocator and stream source).
+
+Everything here takes CUDA float32 tensors that are already resident in HBM
+and launches on ``torch.cuda.current_stream()``; nothing copies to the host.
+Shapes (B = batch of independent images, each with its own tables):
+
+    rgb / out      (B, 3, H, W)          planar, C-contiguous
+    lut_planes     (B, 3, 3, d_t, d_t)   [out channel][rg|rb|gb][a][b]
+    lw, lb         (B, 3, 3), (B, 3)
+    grid_planes    (B, K, 3, d_s, d_s)   [grid][xy|xc|yc][a][b]
+    gw, gb         (B, K, 3), (B, K)
+    u, s, vt       (B, 3, 3, d_t, n), (B, 3, 3, n), (B, 3, 3, n, d_t)
+
+Unbatched inputs (no leading B) are accepted and promoted to B = 1.
+(y0, h_total) evaluate a row strip of a taller image (global normalisation).
+"""
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import DimensionMismatch
+
+__all__ = [
+    "table_bytes", "fast_supported", "PackedTables", "reconstruct", "pack_tables", "apply",
+    "apply_exact", "fused_forward", "indices", "fused_backward", "reconstruct_backward",
+]
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(t):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _f32(t, name, ndim):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != torch.float32:
+        raise DimensionMismatch(f"{name} must be float32, got {t.dtype}")
+    if not t.is_cuda:
+        raise DimensionMismatch(f"{name} must be a CUDA tensor")
+    if t.dim() == ndim - 1:
+        t = t.unsqueeze(0)
+    if t.dim() != ndim:
+        raise DimensionMismatch(f"{name} must have {ndim} dims (batched), got {tuple(t.shape)}")
+    return t.contiguous()
+
+
+def table_bytes(d_t, d_s):
+    return int(_lib.load().svdlut_table_bytes(d_t, d_s))
+
+
+def fast_supported(d_t, d_s):
+    return bool(_lib.load().svdlut_fast_supported(d_t, d_s))
+
+
+class PackedTables:
+    """Per-image coefficient tables produced by the on-device prologue."""
+
+    def __init__(self, buf, batch, d_t, d_s):
+        self.buf, self.batch, self.d_t, self.d_s = buf, batch, d_t, d_s
+
+    @property
+    def device(self):
+        return self.buf.device
+
+
+def reconstruct(u, s, vt):
+    """svd.reconstruct_lut on device: planes = f32((f64 u * f64 s) @ f64 vt)."""
+    u, s, vt = _f32(u, "u", 5), _f32(s, "s", 4), _f32(vt, "vt", 5)
+    b, _, _, d, n = u.shape
+    if tuple(s.shape) != (b, 3, 3, n) or tuple(vt.shape) != (b, 3, 3, n, d):
+        raise DimensionMismatch(f"inconsistent factor shapes {tuple(u.shape)} {tuple(s.shape)} "
+                                f"{tuple(vt.shape)}")
+    planes = torch.empty((b, 3, 3, d, d), dtype=torch.float32, device=u.device)
+    _lib.call("svdlut_reconstruct", _p(u), _p(s), _p(vt), b, d, n, _p(planes), _stream(u))
+    return planes
+
+
+def _check_tables(lut_planes, lw, lb, grid_planes, gw, gb):
+    lp = _f32(lut_planes, "lut_planes", 5)
+    lw, lb = _f32(lw, "lw", 3), _f32(lb, "lb", 2)
+    gp = _f32(grid_planes, "grid_planes", 5)
+    gw, gb = _f32(gw, "gw", 3), _f32(gb, "gb", 2)
+    b, d_t = lp.shape[0], lp.shape[3]
+    k, d_s = gp.shape[1], gp.shape[3]
+    if tuple(lp.shape[1:3]) != (3, 3) or lp.shape[3] != lp.shape[4]:
+        raise DimensionMismatch(f"lut_planes must be (B,3,3,d,d), got {tuple(lp.shape)}")
+    if gp.shape[2] != 3 or gp.shape[3] != gp.shape[4]:
+        raise DimensionMismatch(f"grid_planes must be (B,K,3,d,d), got {tuple(gp.shape)}")
+    if tuple(lw.shape) != (b, 3, 3) or tuple(lb.shape) != (b, 3):
+        raise DimensionMismatch("LUT weights must be (B,3,3) and (B,3)")
+    if gw.shape[0] != b or gw.shape[2] != 3 or gb.shape[0] != b or gp.shape[0] != b:
+        raise DimensionMismatch("grid tensors disagree on the batch size")
+    if gw.shape[1] != k or gb.shape[1] != k:
+        raise DimensionMismatch(f"{k} grids but {gw.shape[1]} weight rows")
+    return lp, lw, lb, gp, gw, gb, b, d_t, k, d_s
+
+
+def pack_tables(lut_planes, lw, lb, grid_planes, gw, gb):
+    """Fold weights, merge grids per channel, write coefficient cells."""
+    lp, lw, lb, gp, gw, gb, b, d_t, k, d_s = _check_tables(lut_planes, lw, lb, grid_planes, gw, gb)
+    nbytes = table_bytes(d_t, d_s)
+    buf = torch.empty(b * nbytes // 4, dtype=torch.float32, device=lp.device)
+    _lib.call("svdlut_pack_tables", _p(lp), _p(lw), _p(lb), d_t, _p(gp), _p(gw), _p(gb), k, d_s,
+              b, _p(buf), _stream(lp))
+    return PackedTables(buf, b, d_t, d_s)
+
+
+def _image(rgb, batch):
+    rgb = _f32(rgb, "rgb", 4)
+    if rgb.shape[1] != 3:
+        raise DimensionMismatch(f"rgb must be (B,3,H,W), got {tuple(rgb.shape)}")
+    if batch is not None and rgb.shape[0] != batch:
+        raise DimensionMismatch(f"{rgb.shape[0]} images but tables for {batch}")
+    return rgb
+
+
+def apply(rgb, tables, out=None, y0=0, h_total=None, variant=-1, nonfinite=None):
+    """Fused slice + LUT apply (fast fp32 kernel) from packed tables.
+
+    ``nonfinite``: optional int32 CUDA tensor (1 element) OR-ed with 1 if any
+    output is NaN/Inf.  ``variant``: 0 = 128-bit lanes, 1 = interleaved lanes.
+    """
+    rgb = _image(rgb, tables.batch)
+    b, _, h, w = rgb.shape
+    h_total = h if h_total is None else h_total
+    if out is None:
+        out = torch.empty_like(rgb)
+    elif out.shape != rgb.shape or not out.is_contiguous() or out.dtype != torch.float32:
+        raise DimensionMismatch("out must be a contiguous float32 tensor shaped like rgb")
+    L = _lib.load()
+    ws_bytes = int(L.svdlut_workspace_bytes(0, h, w, tables.d_t, tables.d_s))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=rgb.device)
+    _lib.call("svdlut_fused_fwd_packed_ex", _p(rgb), b, h, w, y0, h_total, _p(tables.buf),
+              tables.d_t, tables.d_s, _p(out), _p(ws), ws_bytes, _p(nonfinite), variant,
+              _stream(rgb))
+    return out
+
+
+def apply_exact(rgb, lut_planes, lw, lb, grid_planes, gw, gb, out=None, y0=0, h_total=None):
+    """f64 op-for-op kernel: bitwise equal to the reference fused_enhance."""
+    lp, lw, lb, gp, gw, gb, bt, d_t, k, d_s = _check_tables(lut_planes, lw, lb, grid_planes, gw, gb)
+    rgb = _image(rgb, bt)
+    b, _, h, w = rgb.shape
+    h_total = h if h_total is None else h_total
+    if out is None:
+        out = torch.empty_like(rgb)
+    _lib.call("svdlut_fused_fwd_exact", _p(rgb), b, h, w, y0, h_total, _p(lp), _p(lw), _p(lb), d_t,
+              _p(gp), _p(gw), _p(gb), k, d_s, _p(out), _stream(rgb))
+    return out
+
+
+def fused_forward(rgb, lut_planes, lw, lb, grid_planes, gw, gb, out=None, y0=0, h_total=None,
+                  exact=False):
+    """Pack + apply; dimensions beyond the shared-memory kernel use the exact kernel."""
+    if exact or not fast_supported(lut_planes.shape[-1], grid_planes.shape[-1]):
+        return apply_exact(rgb, lut_planes, lw, lb, grid_planes, gw, gb, out, y0, h_total)
+    tables = pack_tables(lut_planes, lw, lb, grid_planes, gw, gb)
+    return apply(rgb, tables, out=out, y0=y0, h_total=h_total)
+
+
+def indices(rgb, d_t, d_s, y0=0, h_total=None):
+    """(B, 8, H, W) int32 cell selection as the fast kernel computes it."""
+    rgb = _image(rgb, None)
+    b, _, h, w = rgb.shape
+    h_total = h if h_total is None else h_total
+    idx = torch.empty((b, 8, h, w), dtype=torch.int32, device=rgb.device)
+    _lib.call("svdlut_indices", _p(rgb), b, h, w, y0, h_total, d_t, d_s, _p(idx), _stream(rgb))
+    return idx
+
+
+def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None, need_gx=True):
+    """Gradients of the fused apply w.r.t. the input and every table.
+
+    Returns dict(gx, dlut_planes, dlw, dlb, dgrid_planes, dgw, dgb).
+    """
+    lp = _f32(lut_planes, "lut_planes", 5)
+    lw = _f32(lw, "lw", 3)
+    gp = _f32(grid_planes, "grid_planes", 5)
+    gw = _f32(gw, "gw", 3)
+    b, d_t = lp.shape[0], lp.shape[3]
+    k, d_s = gp.shape[1], gp.shape[3]
+    rgb = _image(rgb, b)
+    gy = _image(gy, b)
+    if gy.shape != rgb.shape:
+        raise DimensionMismatch("gy must be shaped like rgb")
+    _, _, h, w = rgb.shape
+    h_total = h if h_total is None else h_total
+    dev = rgb.device
+    g = dict(
+        gx=torch.empty_like(rgb) if need_gx else None,
+        dlut_planes=torch.empty_like(lp),
+        dlw=torch.empty((b, 3, 3), dtype=torch.float32, device=dev),
+        dlb=torch.empty((b, 3), dtype=torch.float32, device=dev),
+        dgrid_planes=torch.empty_like(gp),
+        dgw=torch.empty((b, k, 3), dtype=torch.float32, device=dev),
+        dgb=torch.empty((b, k), dtype=torch.float32, device=dev),
+    )
+    ws_bytes = int(_lib.load().svdlut_bwd_workspace_bytes(b, h, w, d_t, d_s, k))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    _lib.call("svdlut_fused_bwd", _p(rgb), _p(gy), b, h, w, y0, h_total, _p(lp), _p(lw), d_t,
+              _p(gp), _p(gw), k, d_s, _p(g["gx"]), _p(g["dlut_planes"]), _p(g["dlw"]),
+              _p(g["dlb"]), _p(g["dgrid_planes"]), _p(g["dgw"]), _p(g["dgb"]), _p(ws), ws_bytes,
+              _stream(rgb))
+    return g
+
+
+def reconstruct_backward(u, s, vt, dplanes):
+    u, s, vt = _f32(u, "u", 5), _f32(s, "s", 4), _f32(vt, "vt", 5)
+    dplanes = _f32(dplanes, "dplanes", 5)
+    b, _, _, d, n = u.shape
+    du, ds, dvt = torch.empty_like(u), torch.empty_like(s), torch.empty_like(vt)
+    _lib.call("svdlut_reconstruct_bwd", _p(u), _p(s), _p(vt), _p(dplanes), b, d, n, _p(du),
+              _p(ds), _p(dvt), _stream(u))
+    return du, ds, dvt

@@ -1,0 +1,125 @@
+"""Reference-facing operator: ``fused_enhance`` on host (numpy) values.
+
+Mirrors ``svdlut.transform.fused_enhance`` (reference transform.py:308-353):
+same signature, same validation order and exception classes, exactly one
+output raster allocated through ``_alloc_raster`` (observable through
+``_raster_hook``, reference transform.py:50-58), and a new ``Image`` returned.
+
+The work runs on the GPU through ``svdlut_enhance_host`` (C ABI): the image
+and tables are copied host→device, the tables are packed on device, the fused
+sm_100a kernel runs, and the result is copied back — pipelined over row
+strips on two streams.  ``threads`` is accepted for signature compatibility
+and ignored.  The output raster is page-locked so the device→host copy is a
+direct DMA.  There is no CPU path: without the built library or a GPU this
+raises.
+"""
+
+import atexit
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib
+from .core_types import Image as _Image
+from .errors import BadGridCount, CudaError, DegenerateImage, DimensionMismatch, NonFiniteValue
+
+__all__ = ["fused_enhance", "_alloc_raster"]
+
+# Test instrumentation: called with the shape of every raster this module
+# allocates (the reference's contract; transform.py:50-58).
+_raster_hook = None
+
+
+def _alloc_raster(shape):
+    if _raster_hook is not None:
+        _raster_hook(shape)
+    return _pinned_empty(shape)
+
+
+def _pinned_empty(shape):
+    import torch
+
+    if torch.cuda.is_available():
+        return torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
+    return np.empty(shape, dtype=np.float32)
+
+
+_ctx_lock = threading.Lock()
+_ctxs = {}
+
+
+def _host_ctx(device):
+    with _ctx_lock:
+        ctx = _ctxs.get(device)
+        if ctx is None:
+            ctx = _lib.load().svdlut_ctx_create(device)
+            if not ctx:
+                raise CudaError(f"could not create a CUDA context on device {device}")
+            _ctxs[device] = ctx
+        return ctx
+
+
+@atexit.register
+def _release():
+    if _lib._lib is None:
+        return
+    for ctx in _ctxs.values():
+        _lib._lib.svdlut_ctx_destroy(ctx)
+    _ctxs.clear()
+
+
+def _current_device():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise CudaError("no CUDA device: the apply path has no CPU fallback")
+    return torch.cuda.current_device()
+
+
+def _image_type(img):
+    """Return an Image class compatible with the caller's (reference or ours)."""
+    return type(img)
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _c32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def fused_enhance(img, luts, lut_weights, grids, grid_weights, threads: int = 1,
+                  exact: bool = False):
+    """Single-pass LUT transform plus grid slicing on the GPU.
+
+    ``exact=True`` selects the f64 kernel whose output is bitwise equal to the
+    reference; the default fp32 kernel agrees within 1e-5 with identical cell
+    selection.
+    """
+    del threads  # the GPU decides its own parallelism
+    if grids.k % 3 != 0:
+        raise BadGridCount(f"grid count {grids.k} is not a multiple of 3")
+    if grid_weights.k != grids.k:
+        raise DimensionMismatch(f"{grids.k} grids but {grid_weights.k} weight rows")
+    if img.width < 2 or img.height < 2:
+        raise DegenerateImage("slicing needs at least 2 px in each direction")
+    h, w = img.height, img.width
+    out = _alloc_raster((3, h, w))
+    rgb = _c32(img.data)
+    planes = _c32(luts.planes)
+    lw, lb = _c32(lut_weights.w), _c32(lut_weights.b)
+    gp = _c32(grids.planes)
+    gw, gb = _c32(grid_weights.w), _c32(grid_weights.b)
+    flag = ctypes.c_int(0)
+    ctx = _host_ctx(_current_device())
+    _lib.call("svdlut_enhance_host", ctx, _ptr(rgb), h, w, _ptr(planes), _ptr(lw), _ptr(lb),
+              planes.shape[2], _ptr(gp), _ptr(gw), _ptr(gb), gp.shape[0], gp.shape[2], _ptr(out),
+              int(bool(exact)), ctypes.byref(flag))
+    cls = _image_type(img)
+    if not exact and issubclass(cls, _Image):
+        if flag.value:
+            raise NonFiniteValue("image data contains a NaN or infinite entry")
+        return cls._trusted(w, h, out)
+    return cls(w, h, out)  # exact mode / foreign Image type: the constructor validates

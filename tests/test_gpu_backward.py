@@ -1,0 +1,103 @@
+"""GPU parity of the backward kernels against the f64 oracle (SURVEY.md
+Appendix B; the reference itself has no backward — "parity unpinned" by the
+reference, pinned by autograd + finite differences in test_oracle.py).
+Tolerance (BASELINE.json north_star): 1e-4 relative, per tensor
+max|g - g_ref| <= 1e-4 * max|g_ref|; touched-vertex pattern must match."""
+
+import numpy as np
+import pytest
+
+from conftest import make_inputs
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+
+    import __graft_entry__
+
+    __graft_entry__.build_library()
+    assert torch.cuda.is_available()
+    return torch.device("cuda", 0)
+
+
+def T(a, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def close(got, want, what):
+    scale = max(float(np.abs(want).max()), 1e-30)
+    err = float(np.abs(got - want).max())
+    assert err <= RTOL * scale, f"{what}: err {err} vs scale {scale}"
+
+
+@pytest.mark.parametrize("w,h,d_t,d_s,k,low,high", [
+    (37, 21, 9, 5, 6, 0.0, 1.0),
+    (64, 33, 33, 17, 6, -0.2, 1.2),
+    (19, 40, 17, 8, 9, 0.0, 1.0),
+    (5, 3, 2, 2, 3, -1.0, 2.0),
+])
+def test_fused_backward_vs_oracle(dev, oracle_mod, w, h, d_t, d_s, k, low, high):
+    from paper_2508_16121_b200 import device
+
+    c = make_inputs(w, h, d_t=d_t, d_s=d_s, k=k, seed=w + h, low=low, high=high)
+    gy = np.random.default_rng(7).normal(size=(3, h, w)).astype(np.float32)
+    g = device.fused_backward(T(c["rgb"], dev), T(gy, dev), T(c["lp"], dev), T(c["lw"], dev),
+                              T(c["gp"], dev), T(c["gw"], dev))
+    ref = oracle_mod.fused_bwd(c["rgb"], gy, c["lp"], c["lw"], c["gp"], c["gw"])
+    names = dict(gx="gx", dlut_planes="dlp", dlw="dlw", dlb="dlb", dgrid_planes="dgp", dgw="dgw",
+                 dgb="dgb")
+    for mine, theirs in names.items():
+        got = g[mine][0].cpu().numpy()
+        close(got, ref[theirs], mine)
+    for mine, theirs in (("dlut_planes", "dlp"), ("dgrid_planes", "dgp")):
+        got = g[mine][0].cpu().numpy()
+        assert np.array_equal(got != 0, ref[theirs] != 0), mine
+
+
+def test_fused_backward_smooth_1080p_batch(dev, oracle_mod):
+    """Config-5 shaped (smaller batch): smooth 1080p images, gY = 2(Y-T)/N."""
+    import torch
+
+    from paper_2508_16121_b200 import device, synth
+
+    case = synth.make_batch([5, 6], h=1080, w=1920)
+    t = {k: T(getattr(case, k), dev) for k in ("rgb", "u", "s", "vt", "lw", "lb", "grid_planes",
+                                              "gw", "gb")}
+    planes = device.reconstruct(t["u"], t["s"], t["vt"])
+    y = device.fused_forward(t["rgb"], planes, t["lw"], t["lb"], t["grid_planes"], t["gw"], t["gb"])
+    target = t["rgb"].clamp_min(0) ** 0.8
+    gy = 2.0 * (y - target) / y.numel()
+    g = device.fused_backward(t["rgb"], gy, planes, t["lw"], t["grid_planes"], t["gw"])
+    for b in range(2):
+        ref = oracle_mod.fused_bwd(case.rgb[b], gy[b].cpu().numpy(), planes[b].cpu().numpy(),
+                                   case.lw[b], case.grid_planes[b], case.gw[b])
+        close(g["gx"][b].cpu().numpy(), ref["gx"], "gx")
+        close(g["dlut_planes"][b].cpu().numpy(), ref["dlp"], "dlut")
+        close(g["dgrid_planes"][b].cpu().numpy(), ref["dgp"], "dgrid")
+        close(g["dlw"][b].cpu().numpy(), ref["dlw"], "dlw")
+        close(g["dgw"][b].cpu().numpy(), ref["dgw"], "dgw")
+        close(g["dlb"][b].cpu().numpy(), ref["dlb"], "dlb")
+        close(g["dgb"][b].cpu().numpy(), ref["dgb"], "dgb")
+    torch.cuda.synchronize()
+
+
+def test_reconstruct_backward_vs_oracle(dev, oracle_mod):
+    from paper_2508_16121_b200 import device
+
+    rng = np.random.default_rng(3)
+    for d, n in ((33, 8), (9, 9), (2, 1)):
+        u = rng.normal(0, 0.1, (3, 3, d, n)).astype(np.float32)
+        s = rng.normal(0, 0.1, (3, 3, n)).astype(np.float32)
+        vt = rng.normal(0, 0.1, (3, 3, n, d)).astype(np.float32)
+        dT = rng.normal(size=(3, 3, d, d)).astype(np.float32)
+        du, ds, dvt = device.reconstruct_backward(T(u, dev), T(s, dev), T(vt, dev), T(dT, dev))
+        rdu, rds, rdvt = oracle_mod.reconstruct_bwd(u, s, vt, dT)
+        close(du[0].cpu().numpy(), rdu, "du")
+        close(ds[0].cpu().numpy(), rds, "ds")
+        close(dvt[0].cpu().numpy(), rdvt, "dvt")
