@@ -68,7 +68,7 @@ size_t svdlut_table_bytes(int d_t, int d_s);
  * memory), else 0. */
 int svdlut_fast_supported(int d_t, int d_s);
 
-/* Bytes of workspace svdlut_fused_fwd needs for a call of this shape. */
+/* Bytes of workspace svdlut_fused_fwd needs (the packed tables of the batch). */
 size_t svdlut_workspace_bytes(int batch, int h, int w, int d_t, int d_s);
 
 /* svd.reconstruct_lut, batched: planes[b,c,p] = f32((f64 u * f64 s) @ f64 vt).
@@ -86,18 +86,16 @@ int svdlut_pack_tables(const float* lut_planes, const float* lw, const float* lb
 /* ---- forward ------------------------------------------------------------ */
 
 /* Fused slice + 2D-LUT apply from packed tables (fast fp32 kernel, within
- * 1e-5 of the reference; cell selection bit-exact).  `workspace` holds the
- * spatial bracket tables: svdlut_workspace_bytes(...) - batch*table_bytes
- * is enough; pass the tail of the fused workspace or a separate buffer. */
+ * 1e-5 of the reference; cell selection bit-exact).  Spatial brackets are
+ * computed in the kernel; `workspace` is unused (may be NULL) and kept for
+ * ABI stability. */
 int svdlut_fused_fwd_packed(const float* rgb, int batch, int h, int w, int y0, int h_total,
                             const void* tables, int d_t, int d_s, float* out, void* workspace,
                             size_t workspace_bytes, void* stream);
 
 /* As svdlut_fused_fwd_packed, plus: `nonfinite` (device int, may be NULL) is
  * OR-ed with 1 if any output sample is NaN/Inf (the check core_types.py:55-59
- * does on the host), and `variant` picks the lane->pixel mapping: 0 = four
- * consecutive pixels per lane (128-bit I/O), 1 = interleaved lanes (a warp
- * instruction covers 32 consecutive pixels), -1 = default. */
+ * does on the host).  `variant` is reserved (pass -1). */
 int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0, int h_total,
                                const void* tables, int d_t, int d_s, float* out, void* workspace,
                                size_t workspace_bytes, int* nonfinite, int variant, void* stream);

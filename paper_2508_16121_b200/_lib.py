@@ -11,7 +11,7 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsvdlut_b200.so")
+LIB_PATH = os.environ.get("SVDLUT_LIB") or os.path.join(_HERE, "_lib", "libsvdlut_b200.so")
 
 _lib = None
 

@@ -66,10 +66,6 @@ int check_k(int k) {
 
 size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// spatial bracket tables live after the packed tables in the workspace
-size_t spatial_bytes(int h, int w) {
-  return round_up((size_t)w * sizeof(SpatialBr), 256) + round_up((size_t)h * sizeof(SpatialBr), 256) + 256;
-}
 
 }  // namespace
 
@@ -101,13 +97,14 @@ size_t svdlut_table_bytes(int d_t, int d_s) {
 
 int svdlut_fast_supported(int d_t, int d_s) {
   if (d_t < 2 || d_s < 2) return 0;
-  return TableLayout::make(d_t, d_s).bytes() <= (size_t)fwd_max_smem_bytes() ? 1 : 0;
+  return fwd_smem_bytes(d_t, d_s) <= (size_t)fwd_max_smem_bytes() ? 1 : 0;
 }
 
 size_t svdlut_workspace_bytes(int batch, int h, int w, int d_t, int d_s) {
-  if (batch < 0 || h < 0 || w < 0) return 0;
-  const size_t tb = svdlut_table_bytes(d_t, d_s);
-  return (size_t)batch * tb + spatial_bytes(h, w) + 256;
+  (void)h;
+  (void)w;
+  if (batch < 0) return 0;
+  return (size_t)batch * svdlut_table_bytes(d_t, d_s) + 256;  // packed tables only
 }
 
 int svdlut_reconstruct(const float* u, const float* s, const float* vt, int batch, int d_t,
@@ -142,6 +139,9 @@ int svdlut_pack_tables(const float* lut_planes, const float* lw, const float* lb
 static int fused_fwd_packed_impl(const float* rgb, int batch, int h, int w, int y0, int h_total,
                                  const void* tables, int d_t, int d_s, float* out, void* ws,
                                  size_t ws_bytes, int* nonfinite, int variant, cudaStream_t st) {
+  (void)ws;
+  (void)ws_bytes;
+  (void)variant;
   int rc;
   if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
   if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
@@ -149,22 +149,10 @@ static int fused_fwd_packed_impl(const float* rgb, int batch, int h, int w, int 
     return fail(SVDLUT_ERR_UNSUPPORTED,
                 "tables for d_t=%d d_s=%d exceed shared memory; use svdlut_fused_fwd_exact", d_t, d_s);
   if ((long long)batch * h * w == 0) return SVDLUT_OK;
-  if (!rgb || !tables || !out || !ws) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
-  if (!aligned16(tables) || !aligned16(ws))
-    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables/workspace must be 16-byte aligned");
-  if (ws_bytes < spatial_bytes(h, w))
-    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes,
-                spatial_bytes(h, w));
+  if (!rgb || !tables || !out) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
   const TableLayout L = TableLayout::make(d_t, d_s);
-  char* p = (char*)ws;
-  SpatialBr* col = (SpatialBr*)p;
-  SpatialBr* row = (SpatialBr*)(p + round_up((size_t)w * sizeof(SpatialBr), 256));
-  CUDA_TRY(launch_spatial(w, h, y0, h_total, d_s, col, row, st), "spatial brackets");
-  // 128-bit path needs 16 B aligned planes; otherwise use the scalar mapping
-  if (variant < 0) variant = 0;
-  if (variant == 0 && (!aligned16(rgb) || !aligned16(out) || (w % 4) != 0)) variant = 1;
-  CUDA_TRY(launch_fused_fwd(rgb, out, batch, h, w, (const float*)tables, L, col, row, nonfinite,
-                            variant, st),
+  CUDA_TRY(launch_fused_fwd(rgb, out, batch, h, w, y0, h_total, (const float*)tables, L, nonfinite, st),
            "fused forward");
   return SVDLUT_OK;
 }
@@ -204,8 +192,8 @@ int svdlut_fused_fwd(const float* rgb, int batch, int h, int w, int y0, int h_to
   if ((rc = svdlut_pack_tables(lut_planes, lw, lb, d_t, grid_planes, gw, gb, k, d_s, batch,
                                workspace, stream)) != SVDLUT_OK)
     return rc;
-  return fused_fwd_packed_impl(rgb, batch, h, w, y0, h_total, workspace, d_t, d_s, out,
-                               (char*)workspace + round_up(tb, 256), workspace_bytes - round_up(tb, 256),
+  (void)tb;
+  return fused_fwd_packed_impl(rgb, batch, h, w, y0, h_total, workspace, d_t, d_s, out, nullptr, 0,
                                nullptr, -1, (cudaStream_t)stream);
 }
 

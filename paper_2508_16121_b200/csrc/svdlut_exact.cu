@@ -125,9 +125,11 @@ __global__ void fused_exact_kernel(const float* __restrict__ rgb, float* __restr
   }
 }
 
-// Cell selection as the fast kernel computes it (svdlut_common.cuh helpers).
+// Cell selection as the fast kernel computes it (svdlut_common.cuh helpers:
+// color_bracket and the table-free col_bracket / row_bracket).
 __global__ void indices_kernel(const float* __restrict__ rgb, int batch, int h, int w, int y0,
-                               int h_total, int dt, int ds, int32_t* __restrict__ idx) {
+                               int h_total, int dt, int ds, double rcp_w, double rcp_h,
+                               int32_t* __restrict__ idx) {
   const long long plane = (long long)h * w;
   const long long total = (long long)batch * plane;
   const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
@@ -149,8 +151,9 @@ __global__ void indices_kernel(const float* __restrict__ rgb, int batch, int h, 
       color_bracket(q, sdm1, sdm2, i, d);
       I[(3 + c) * plane + o] = i;
     }
-    I[6 * plane + o] = spatial_bracket(x, w, ds).i;
-    I[7 * plane + o] = spatial_bracket(y0 + y, h_total, ds).i;
+    float ex, ey;
+    I[6 * plane + o] = (int32_t)(col_bracket(x, rcp_w, sdm1, sdm2, ex) - 0x4B000000u);
+    I[7 * plane + o] = (int32_t)(row_bracket(y0 + y, rcp_h, sdm1, sdm2, ey) - 0x4B000000u);
   }
 }
 
@@ -177,7 +180,8 @@ cudaError_t launch_indices(const float* rgb, int batch, int h, int w, int y0, in
   const long long total = (long long)batch * h * w;
   if (total == 0) return cudaSuccess;
   indices_kernel<<<grid_for(total, 256), 256, 0, st>>>(rgb, batch, h, w, y0, h_total, dt, ds,
-                                                       idx);
+                                                       1.0 / (double)(w - 1),
+                                                       1.0 / (double)(h_total - 1), idx);
   return cudaGetLastError();
 }
 

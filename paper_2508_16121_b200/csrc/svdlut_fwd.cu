@@ -3,40 +3,60 @@
 // Replaces transform._fused_impl (reference transform.py:215-300).
 //
 // Design:
-//   * One persistent CTA per SM (the packed tables of one image, ≈187 KB at
-//     d_t=33 / d_s=17, live in shared memory; staged by a TMA bulk copy
-//     `cp.async.bulk` completing on an mbarrier).
-//   * Work = 128-pixel row chunks over (image, row, chunk), split into one
-//     contiguous range per CTA; a CTA re-stages tables only when its range
-//     crosses into the next image.  Warps take chunks round-robin and
-//     software-pipeline the next chunk's global loads under the current
-//     chunk's math.
-//   * Per pixel: 6 brackets, 9 LUT terms as 3 channel-packed coefficient
-//     cells (3×LDS.128 each), 1 channel-packed xy cell (3×LDS.128) and one
-//     xc + one yc cell per output channel (LDS.128 each); every term is
-//     v = A + B·a + C·b + D·a·b with weights folded in by the prologue.
+//   * One persistent CTA per SM; the packed tables of one image (≈182 KB at
+//     d_t=33 / d_s=17) live in shared memory, staged by TMA bulk copies
+//     (`cp.async.bulk`, completion on an mbarrier).  A CTA owns a contiguous
+//     range of 128-pixel row chunks over (image, row, chunk) and re-stages
+//     only when the range crosses an image boundary.
+//   * Inside an image phase every warp owns a contiguous sub-range of chunks
+//     and software-pipelines the next chunk's global loads under the current
+//     chunk's math.  Lane l handles pixels x0 + l + 32u (u < 4), so one warp
+//     instruction covers 32 consecutive pixels: neighbouring pixels of a
+//     smooth image hit the same or adjacent LUT cells, which the shared-memory
+//     pipe serves with few wavefronts.
+//   * Grid terms: the y-direction is interpolated once per row, per warp, into
+//     warp-private 1-D tables (yc: over the guide, xy: over x), so per pixel and
+//     channel the grids cost one xc coefficient cell (LDS.128) + one yc knot
+//     pair (LDS.64); xy is one channel-packed LDS.128 + LDS.64 per pixel.
+//   * LUT: 3 channel-packed coefficient cells (3×LDS.128 each) with weights
+//     folded in; every term is v = A + B·a + C·b + D·a·b.
+//   * Integer work stays on 32-bit shared addresses; the colour floor is an
+//     add of 2^23 (svdlut_common.cuh), so the index bits feed IMADs directly.
 //   * Streaming I/O: 24 B/pixel of HBM traffic (3 f32 in, 3 f32 out).
 #include <cstdint>
+#include <mutex>
+#include <vector>
+
 #include "svdlut_common.cuh"
 #include "svdlut_internal.h"
 
 namespace svdlut {
 
-constexpr int kFwdWarps = 16;
-constexpr int kPx = 4;              // pixels per lane per chunk
-constexpr int kChunk = 32 * kPx;    // pixels per warp chunk
+// Kernel shape (pixels per lane PX, warps per CTA NW) is a template choice;
+// the default below is what launch_fused_fwd uses (FWD_PX / FWD_NW override
+// it at build time for experiments).
+#ifndef FWD_PX
+#define FWD_PX 4
+#endif
+#ifndef FWD_NW
+#define FWD_NW 15  // 15 x 128 px = 1920: divides 1080p / 4K / 8K rows exactly
+#endif
+constexpr int kPx = FWD_PX;
+constexpr int kFwdWarps = FWD_NW;
+constexpr int kChunk = 32 * kPx;
+constexpr uint32_t kMagicBits = 0x4B000000u;  // bits of 2^23
 
 struct FwdParams {
   const float* rgb;
   float* out;
-  int h, w;
+  int batch, h, w;
+  int y0;                   // first row of this strip in an image of h_total rows
   const float* tables;
   TableLayout L;
-  const SpatialBr* col;
-  const SpatialBr* row;
-  int cpr;             // chunks per row
-  long long per_img;   // h * cpr
-  long long total;     // batch * h * cpr
+  cudaTextureObject_t tex;  // float4 texels over the packed tables (pair gb reads)
+  int tex_base;             // texel index of image 0's table start
+  double rcp_w;             // RN64(1 / (W - 1)) for the exact column brackets
+  double rcp_h;             // RN64(1 / (h_total - 1)) for the row brackets
   int* nonfinite;
 };
 
@@ -69,292 +89,522 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-
-// v += A + B*a + C*b + D*a*b for 3 packed channels: cell = {A0 A1 A2 B0|B1 B2 C0 C1|C2 D0 D1 D2}
-__device__ __forceinline__ void cell3(const float* cellp, float a, float b, float& o0, float& o1,
-                                      float& o2) {
-  const float4* q = reinterpret_cast<const float4*>(cellp);
-  const float4 c0 = q[0], c1 = q[1], c2 = q[2];
-  o0 += __fmaf_rn(b, __fmaf_rn(c2.y, a, c1.z), __fmaf_rn(c0.w, a, c0.x));
-  o1 += __fmaf_rn(b, __fmaf_rn(c2.z, a, c1.w), __fmaf_rn(c1.x, a, c0.y));
-  o2 += __fmaf_rn(b, __fmaf_rn(c2.w, a, c2.x), __fmaf_rn(c1.y, a, c0.z));
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
 }
-// v = A + B*a + C*b + D*a*b for one channel cell {A,B,C,D}
-__device__ __forceinline__ float cell1(const float* cellp, float a, float b) {
-  const float4 c = *reinterpret_cast<const float4*>(cellp);
-  return __fmaf_rn(b, __fmaf_rn(c.w, a, c.z), __fmaf_rn(c.y, a, c.x));
+__device__ __forceinline__ float2 lds2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
 }
 
-struct PixCtx {
-  const float* lut0;  // pair rg base
-  const float* lut1;  // pair rb base
-  const float* lut2;  // pair gb base
-  const float* xy;
-  const float* xc;    // channel 0 base; channel c at + c*xcs
-  const float* yc;
-  int cst, css, xcs;
-  float tdm1, tdm2, sdm1, sdm2;
-};
-
-__device__ __forceinline__ void apply_pixel(const PixCtx& C, float r, float g, float bl, int jx,
-                                            float ex, int jy, float ey, float& o0, float& o1,
-                                            float& o2) {
-  const float qr = clamp01(r), qg = clamp01(g), qb = clamp01(bl);
-  int ir, ig, ib;
-  float dr, dg, db;
-  color_bracket(qr, C.tdm1, C.tdm2, ir, dr);
-  color_bracket(qg, C.tdm1, C.tdm2, ig, dg);
-  color_bracket(qb, C.tdm1, C.tdm2, ib, db);
-  o0 = 0.f;
-  o1 = 0.f;
-  o2 = 0.f;
-  cell3(C.lut0 + (ir * C.cst + ig) * 12, dr, dg, o0, o1, o2);
-  cell3(C.lut1 + (ir * C.cst + ib) * 12, dr, db, o0, o1, o2);
-  cell3(C.lut2 + (ig * C.cst + ib) * 12, dg, db, o0, o1, o2);
-  cell3(C.xy + (jx * C.css + jy) * 12, ex, ey, o0, o1, o2);
-  int jr, jg, jb;
-  float er, eg, eb;
-  color_bracket(qr, C.sdm1, C.sdm2, jr, er);
-  color_bracket(qg, C.sdm1, C.sdm2, jg, eg);
-  color_bracket(qb, C.sdm1, C.sdm2, jb, eb);
-  o0 += cell1(C.xc + (jx * C.css + jr) * 4, ex, er);
-  o1 += cell1(C.xc + C.xcs + (jx * C.css + jg) * 4, ex, eg);
-  o2 += cell1(C.xc + 2 * C.xcs + (jx * C.css + jb) * 4, ex, eb);
-  o0 += cell1(C.yc + (jy * C.css + jr) * 4, ey, er);
-  o1 += cell1(C.yc + C.xcs + (jy * C.css + jg) * 4, ey, eg);
-  o2 += cell1(C.yc + 2 * C.xcs + (jy * C.css + jb) * 4, ey, eb);
+// Streaming 128-bit load that does not allocate in L1 (keeps L1 for the
+// texture-path LUT pair).
+__device__ __forceinline__ float4 ldg_stream4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ldg_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
 }
 
-// Inputs of one 128-pixel chunk for one lane.
+// Colour bracket returning the 2^23-biased index bits (see svdlut_common.cuh).
+__device__ __forceinline__ uint32_t cbracket(float q, float dm1, float dm2, float& delta) {
+  const float t = fminf(__fmul_rz(q, dm1), dm2);
+  const float m = __fadd_rz(t, 8388608.0f);
+  delta = __fmaf_rn(q, dm1, -(m - 8388608.0f));
+  return __float_as_uint(m);
+}
+
+// o_c (+)= A_c + B_c*a + C_c*b + D_c*a*b; cell = {A0 A1 A2 B0|B1 B2 C0 C1|C2 D0 D1 D2}
+template <bool FIRST>
+__device__ __forceinline__ void lut_term(uint32_t a, float da, float db, float& o0, float& o1,
+                                         float& o2) {
+  const float4 c0 = lds4(a), c1 = lds4(a + 16), c2 = lds4(a + 32);
+  const float v0 = __fmaf_rn(db, __fmaf_rn(c2.y, da, c1.z), __fmaf_rn(c0.w, da, c0.x));
+  const float v1 = __fmaf_rn(db, __fmaf_rn(c2.z, da, c1.w), __fmaf_rn(c1.x, da, c0.y));
+  const float v2 = __fmaf_rn(db, __fmaf_rn(c2.w, da, c2.x), __fmaf_rn(c1.y, da, c0.z));
+  if (FIRST) {
+    o0 = v0;
+    o1 = v1;
+    o2 = v2;
+  } else {
+    o0 += v0;
+    o1 += v1;
+    o2 += v2;
+  }
+}
+
+// Same term with the cell read through the texture path (texel index t).
+__device__ __forceinline__ void lut_term_tex(cudaTextureObject_t tex, int t, float da, float db,
+                                             float& o0, float& o1, float& o2) {
+  const float4 c0 = tex1Dfetch<float4>(tex, t);
+  const float4 c1 = tex1Dfetch<float4>(tex, t + 1);
+  const float4 c2 = tex1Dfetch<float4>(tex, t + 2);
+  o0 += __fmaf_rn(db, __fmaf_rn(c2.y, da, c1.z), __fmaf_rn(c0.w, da, c0.x));
+  o1 += __fmaf_rn(db, __fmaf_rn(c2.z, da, c1.w), __fmaf_rn(c1.x, da, c0.y));
+  o2 += __fmaf_rn(db, __fmaf_rn(c2.w, da, c2.x), __fmaf_rn(c1.y, da, c0.z));
+}
+
+template <int PX>
 struct ChunkIn {
-  float r[kPx], g[kPx], b[kPx];
-  int jx[kPx];
-  float ex[kPx];
+  float r[PX], g[PX], b[PX];  // PX consecutive pixels per lane
 };
 
-// INTERLEAVE=false: lane owns 4 consecutive pixels (128-bit loads/stores).
-// INTERLEAVE=true : lane owns pixels lane + 32u (32-bit loads, a warp
-//                   instruction covers 32 consecutive pixels — better
-//                   shared-memory locality on smooth images).
-template <bool INTERLEAVE>
-__device__ __forceinline__ void load_chunk(const FwdParams& p, const float* plane0, long long rowoff,
-                                           int x0, int lane, bool vec_ok, ChunkIn& in) {
-  const long long pl = (long long)p.h * p.w;
-  if (!INTERLEAVE) {
-    const int x = x0 + lane * kPx;
-    if (vec_ok && x + kPx <= p.w) {
-      const float4 r4 = __ldcs(reinterpret_cast<const float4*>(plane0 + rowoff + x));
-      const float4 g4 = __ldcs(reinterpret_cast<const float4*>(plane0 + pl + rowoff + x));
-      const float4 b4 = __ldcs(reinterpret_cast<const float4*>(plane0 + 2 * pl + rowoff + x));
-      in.r[0] = r4.x; in.r[1] = r4.y; in.r[2] = r4.z; in.r[3] = r4.w;
-      in.g[0] = g4.x; in.g[1] = g4.y; in.g[2] = g4.z; in.g[3] = g4.w;
-      in.b[0] = b4.x; in.b[1] = b4.y; in.b[2] = b4.z; in.b[3] = b4.w;
-      const int4 c01 = __ldg(reinterpret_cast<const int4*>(p.col + x));
-      const int4 c23 = __ldg(reinterpret_cast<const int4*>(p.col + x + 2));
-      in.jx[0] = c01.x; in.ex[0] = __int_as_float(c01.y);
-      in.jx[1] = c01.z; in.ex[1] = __int_as_float(c01.w);
-      in.jx[2] = c23.x; in.ex[2] = __int_as_float(c23.y);
-      in.jx[3] = c23.z; in.ex[3] = __int_as_float(c23.w);
-    } else {
-#pragma unroll
-      for (int u = 0; u < kPx; ++u) {
-        const int xx = min(x + u, p.w - 1);
-        in.r[u] = __ldcs(plane0 + rowoff + xx);
-        in.g[u] = __ldcs(plane0 + pl + rowoff + xx);
-        in.b[u] = __ldcs(plane0 + 2 * pl + rowoff + xx);
-        const SpatialBr c = p.col[xx];
-        in.jx[u] = c.i;
-        in.ex[u] = c.d;
-      }
-    }
+template <int PX>
+__device__ __forceinline__ void ldg_stream_vec(const float* p, float* v) {
+  if (PX == 4) {
+    const float4 t = ldg_stream4(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else if (PX == 2) {
+    float2 t;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(t.x), "=f"(t.y) : "l"(p));
+    v[0] = t.x; v[1] = t.y;
+  } else {
+    v[0] = ldg_stream(p);
+  }
+}
+
+template <int PX>
+__device__ __forceinline__ void stg_stream_vec(float* p, const float* v) {
+  if (PX == 4) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+  } else if (PX == 2) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
+  } else {
+    __stcs(p, v[0]);
+  }
+}
+
+// Lane owns pixels x0 + PX*lane + u (u < PX): vector loads when the row is
+// aligned, clamped scalar loads otherwise (and at the right edge).
+template <int PX>
+__device__ __forceinline__ void load_chunk(const float* plane0, long long pl, int y, int x0, int w,
+                                           int lane, bool vec_ok, ChunkIn<PX>& in) {
+  const long long rowoff = (long long)y * w;
+  const int x = x0 + PX * lane;
+  if (vec_ok && x + PX <= w) {
+    ldg_stream_vec<PX>(plane0 + rowoff + x, in.r);
+    ldg_stream_vec<PX>(plane0 + pl + rowoff + x, in.g);
+    ldg_stream_vec<PX>(plane0 + 2 * pl + rowoff + x, in.b);
   } else {
 #pragma unroll
-    for (int u = 0; u < kPx; ++u) {
-      const int xx = min(x0 + lane + 32 * u, p.w - 1);
-      in.r[u] = __ldcs(plane0 + rowoff + xx);
-      in.g[u] = __ldcs(plane0 + pl + rowoff + xx);
-      in.b[u] = __ldcs(plane0 + 2 * pl + rowoff + xx);
-      const SpatialBr c = p.col[xx];
-      in.jx[u] = c.i;
-      in.ex[u] = c.d;
+    for (int u = 0; u < PX; ++u) {
+      const int xx = min(x + u, w - 1);
+      in.r[u] = ldg_stream(plane0 + rowoff + xx);
+      in.g[u] = ldg_stream(plane0 + pl + rowoff + xx);
+      in.b[u] = ldg_stream(plane0 + 2 * pl + rowoff + xx);
     }
   }
 }
 
-template <bool INTERLEAVE, bool CHECK>
-__global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams p) {
+// Grid part of one image's tables (shared memory copy; slot builds / wide path).
+struct GridG {
+  const float4* xc;   // [c][jx][jc] {A,B,C,D}
+  const float* gxy;   // [a][b][3]
+  const float* gyc;   // [c][a][b]
+};
+
+// Merged grid coefficients of channel c at (row bracket jy/ey, x-cell jx, guide cell jc):
+//   {M, N, M', N'} with term = M + N*ex + (M' + N'*ex)*ec  (biases included)
+__device__ __forceinline__ float4 grid_entry(const GridG& G, int ds, int c, int jx, int jc, int jy,
+                                             float ey) {
+  const float4 x = G.xc[(c * (ds - 1) + jx) * (ds - 1) + jc];
+  const float* Y = G.gyc + c * ds * ds;
+  const float y00 = Y[jy * ds + jc], y01 = Y[jy * ds + jc + 1];
+  const float y10 = Y[(jy + 1) * ds + jc], y11 = Y[(jy + 1) * ds + jc + 1];
+  const float q0 = __fmaf_rn(ey, y10 - y00, y00), q1 = __fmaf_rn(ey, y11 - y01, y01);
+  const float* X = G.gxy;
+  const float v00 = X[(jx * ds + jy) * 3 + c], v01 = X[(jx * ds + jy + 1) * 3 + c];
+  const float v10 = X[((jx + 1) * ds + jy) * 3 + c];
+  const float v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
+  const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
+  return make_float4(x.x + q0 + r0, x.y + (r1 - r0), x.z + (q1 - q0), x.w);
+}
+
+template <int DT, int DS, bool CHECK, int PX, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
+  constexpr int CH = 32 * PX;  // pixels per warp chunk
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar_storage;
+  const int dt = DT ? DT : p.L.dt;
+  const int ds = DS ? DS : p.L.ds;
+  const TableLayout L = TableLayout::make(dt, ds);
   const uint32_t bar = smem_addr(&bar_storage);
+  const uint32_t sbase = smem_addr(smem);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const TableLayout& L = p.L;
 
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  const uint32_t table_bytes = (uint32_t)L.staged_bytes();  // smem prefix (all but lut2)
+  const int nent = (ds - 1) * 3 * (ds - 1);                  // slot entries per row
+  float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
 
-  PixCtx C;
-  C.lut0 = smem + L.lut_off;
-  C.lut1 = C.lut0 + (L.dt - 1) * L.cst * 12;
-  C.lut2 = C.lut1 + (L.dt - 1) * L.cst * 12;
-  C.xy = smem + L.xy_off;
-  C.xc = smem + L.xc_off;
-  C.yc = smem + L.yc_off;
-  C.cst = L.cst;
-  C.css = L.css;
-  C.xcs = (L.ds - 1) * L.css * 4;
-  C.tdm1 = (float)(L.dt - 1);
-  C.tdm2 = (float)(L.dt - 2);
-  C.sdm1 = (float)(L.ds - 1);
-  C.sdm2 = (float)(L.ds - 2);
+  GridG G;
+  G.xc = reinterpret_cast<const float4*>(smem + L.xc_off);
+  G.gxy = smem + L.gxy_off;
+  G.gyc = smem + L.gyc_off;
 
-  const long long c_begin = (long long)blockIdx.x * p.total / gridDim.x;
-  const long long c_end = (long long)(blockIdx.x + 1) * p.total / gridDim.x;
-  const bool vec_ok = (p.w % kPx) == 0;
-  const uint32_t table_bytes = (uint32_t)L.bytes();
+  const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
+  const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
+  const uint32_t cst48 = (uint32_t)L.cst * 48u;
+  const uint32_t pair_bytes = (uint32_t)(dt - 1) * cst48;
+  const uint32_t cst3 = (uint32_t)L.cst * 3u;
+  // address = base + bits_a*cst48 + bits_b*48 with the 2^23 bias folded in
+  const uint32_t lutK = sbase + (uint32_t)L.lut_off * 4u - kMagicBits * (cst48 + 48u);
+  const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;  // one channel of a slot row
+  const uint32_t jx_bytes = 3u * chan_bytes;             // one x-cell of a slot row
+  const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
+  const uint32_t slotK0 = smem_addr(slots) - kMagicBits * 16u;
+
+  // contiguous range of global rows (image b, row y) for this CTA
+  const long long rows_total = (long long)p.batch * p.h;
+  const long long r_begin = (long long)blockIdx.x * rows_total / gridDim.x;
+  const long long r_end = (long long)(blockIdx.x + 1) * rows_total / gridDim.x;
+  const long long pl = (long long)p.h * p.w;
+  const bool vec_ok = ((p.w & 3) == 0) &&
+                      ((reinterpret_cast<uintptr_t>(p.rgb) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0;
   uint32_t phase = 0;
   bool bad = false;
 
-  long long c = c_begin;
-  while (c < c_end) {
-    const int b = (int)(c / p.per_img);
-    const long long phase_end = min(c_end, (long long)(b + 1) * p.per_img);
+  long long r = r_begin;
+  while (r < r_end) {
+    const int b = (int)(r / p.h);
+    const int y_first = (int)(r - (long long)b * p.h);
+    const int y_last = (int)(min(r_end, (long long)(b + 1) * p.h) - 1 - (long long)b * p.h);
+    const float* tb = p.tables + (long long)b * L.total_floats;
     // ---- stage image b's tables into shared memory (TMA bulk copy) ----
     __syncthreads();  // every warp is done reading the previous image's tables
     if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive_expect_tx(bar, table_bytes);
-      const char* src = reinterpret_cast<const char*>(p.tables + (long long)b * L.total_floats);
-      const uint32_t dst = smem_addr(smem);
+      const char* src = reinterpret_cast<const char*>(tb);
       for (uint32_t off = 0; off < table_bytes; off += 32768u) {
         const uint32_t n = min(32768u, table_bytes - off);
-        bulk_g2s(dst + off, src + off, n, bar);
+        bulk_g2s(sbase + off, src + off, n, bar);
       }
     }
-    const float* plane0 = p.rgb + (long long)b * 3 * p.h * p.w;
-    float* oplane0 = p.out + (long long)b * 3 * p.h * p.w;
-    const long long pl = (long long)p.h * p.w;
+    const float* plane0 = p.rgb + (long long)b * 3 * pl;
+    float* oplane0 = p.out + (long long)b * 3 * pl;
+    // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
+    const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
+                          (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
 
-    // first chunk's loads overlap the table copy
-    long long t = c + warp;
-    ChunkIn cur;
-    int cur_y = 0, cur_x0 = 0;
-    if (t < phase_end) {
-      const long long rem = t - (long long)b * p.per_img;
-      cur_y = (int)(rem / p.cpr);
-      cur_x0 = (int)(rem - (long long)cur_y * p.cpr) * kChunk;
-      load_chunk<INTERLEAVE>(p, plane0, (long long)cur_y * p.w, cur_x0, lane, vec_ok, cur);
-    }
+    // the first chunk's loads overlap the table copy
+    const int cpr = (p.w + CH - 1) / CH;
+    ChunkIn<PX> cur;
+    int cur_y = y_first, cur_k = warp;
+    if (cur_k < cpr) load_chunk<PX>(plane0, pl, cur_y, cur_k * CH, p.w, lane, vec_ok, cur);
     mbar_wait(bar, phase);
     phase ^= 1u;
+    // slots of the first row (buffer 0)
+    {
+      float ey;
+      const int jy = (int)(row_bracket(p.y0 + y_first, p.rcp_h, sdm1, sdm2, ey) - kMagicBits);
+      for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
+        const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
+        slots[e] = grid_entry(G, ds, ch, jx, jc, jy, ey);
+      }
+    }
+    __syncthreads();
 
-    for (; t < phase_end; t += kFwdWarps) {
-      // prefetch the next chunk of this warp
-      const long long tn = t + kFwdWarps;
-      ChunkIn nxt;
-      int nxt_y = 0, nxt_x0 = 0;
-      if (tn < phase_end) {
-        const long long rem = tn - (long long)b * p.per_img;
-        nxt_y = (int)(rem / p.cpr);
-        nxt_x0 = (int)(rem - (long long)nxt_y * p.cpr) * kChunk;
-        load_chunk<INTERLEAVE>(p, plane0, (long long)nxt_y * p.w, nxt_x0, lane, vec_ok, nxt);
-      }
-      const SpatialBr rb = p.row[cur_y];
-      float o0[kPx], o1[kPx], o2[kPx];
+    for (int y = y_first; y <= y_last; ++y) {
+      const int buf = (y - y_first) & 1;
+      float ey;
+      (void)row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey);
+      const uint32_t slotK = slotK0 + (uint32_t)buf * slot_row_bytes;
+      // ---- this warp's chunks of row y: k = warp, warp + W, ... ----
+      for (; cur_y == y && cur_k < cpr;) {
+        ChunkIn<PX> nxt;
+        int nxt_y = cur_y, nxt_k = cur_k + NW;
+        if (nxt_k >= cpr) {
+          nxt_k = warp;
+          ++nxt_y;
+        }
+        if (nxt_y <= y_last && nxt_k < cpr)
+          load_chunk<PX>(plane0, pl, nxt_y, nxt_k * CH, p.w, lane, vec_ok, nxt);
+
+        const int xl = cur_k * CH + PX * lane;
+        int jxs[PX];
+        float exs[PX];
 #pragma unroll
-      for (int u = 0; u < kPx; ++u) {
-        apply_pixel(C, cur.r[u], cur.g[u], cur.b[u], cur.jx[u], cur.ex[u], rb.i, rb.d, o0[u],
-                    o1[u], o2[u]);
-        if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
-      }
-      const long long rowoff = (long long)cur_y * p.w;
-      if (!INTERLEAVE) {
-        const int x = cur_x0 + lane * kPx;
-        if (vec_ok && x + kPx <= p.w) {
-          __stcs(reinterpret_cast<float4*>(oplane0 + rowoff + x), make_float4(o0[0], o0[1], o0[2], o0[3]));
-          __stcs(reinterpret_cast<float4*>(oplane0 + pl + rowoff + x), make_float4(o1[0], o1[1], o1[2], o1[3]));
-          __stcs(reinterpret_cast<float4*>(oplane0 + 2 * pl + rowoff + x), make_float4(o2[0], o2[1], o2[2], o2[3]));
+        for (int u = 0; u < PX; ++u)
+          jxs[u] = (int)(col_bracket(min(xl + u, p.w - 1), p.rcp_w, sdm1, sdm2, exs[u]) - kMagicBits);
+
+        // Pair gb is gathered through the texture path one pixel ahead of its
+        // use (software pipeline depth 1), hiding the texture latency behind
+        // the shared-memory work of the previous pixel.
+        float o0[PX], o1[PX], o2[PX];
+        float4 tx0, tx1, tx2;  // in-flight texture cells of the next pixel
+        float tdg, tdb;        // its deltas
+        {
+          const float qg = __saturatef(cur.g[0]), qb = __saturatef(cur.b[0]);
+          const uint32_t bg = cbracket(qg, tdm1, tdm2, tdg);
+          const uint32_t bb = cbracket(qb, tdm1, tdm2, tdb);
+          const int ti = (int)(bg * cst3 + bb * 3u + texK);
+          tx0 = tex1Dfetch<float4>(p.tex, ti);
+          tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
+          tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
+        }
+#pragma unroll
+        for (int u = 0; u < PX; ++u) {
+          const float4 c0 = tx0, c1 = tx1, c2 = tx2;
+          const float dg = tdg, db = tdb;
+          if (u + 1 < PX) {
+            const float qg1 = __saturatef(cur.g[u + 1]), qb1 = __saturatef(cur.b[u + 1]);
+            const uint32_t bg1 = cbracket(qg1, tdm1, tdm2, tdg);
+            const uint32_t bb1 = cbracket(qb1, tdm1, tdm2, tdb);
+            const int ti = (int)(bg1 * cst3 + bb1 * 3u + texK);
+            tx0 = tex1Dfetch<float4>(p.tex, ti);
+            tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
+            tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
+          }
+          const float qr = __saturatef(cur.r[u]), qg = __saturatef(cur.g[u]),
+                      qb = __saturatef(cur.b[u]);
+          float dr, dg_, db_;
+          const uint32_t br = cbracket(qr, tdm1, tdm2, dr);
+          const uint32_t bg = cbracket(qg, tdm1, tdm2, dg_);
+          const uint32_t bb = cbracket(qb, tdm1, tdm2, db_);
+          const uint32_t ur = br * cst48 + lutK;
+          float a0, a1, a2;
+          lut_term<true>(ur + bg * 48u, dr, dg_, a0, a1, a2);
+          lut_term<false>(ur + bb * 48u + pair_bytes, dr, db_, a0, a1, a2);
+          a0 += __fmaf_rn(db, __fmaf_rn(c2.y, dg, c1.z), __fmaf_rn(c0.w, dg, c0.x));
+          a1 += __fmaf_rn(db, __fmaf_rn(c2.z, dg, c1.w), __fmaf_rn(c1.x, dg, c0.y));
+          a2 += __fmaf_rn(db, __fmaf_rn(c2.w, dg, c2.x), __fmaf_rn(c1.y, dg, c0.z));
+          // grids: one merged (xy + xc + yc) coefficient cell per channel
+          float er, eg, eb;
+          const uint32_t sr = cbracket(qr, sdm1, sdm2, er);
+          const uint32_t sg = cbracket(qg, sdm1, sdm2, eg);
+          const uint32_t sb = cbracket(qb, sdm1, sdm2, eb);
+          const float ex = exs[u];
+          const uint32_t sa = slotK + (uint32_t)jxs[u] * jx_bytes;
+          const float4 g0 = lds4(sa + sr * 16u);
+          const float4 g1 = lds4(sa + chan_bytes + sg * 16u);
+          const float4 g2 = lds4(sa + 2u * chan_bytes + sb * 16u);
+          o0[u] = a0 + __fmaf_rn(er, __fmaf_rn(g0.w, ex, g0.z), __fmaf_rn(g0.y, ex, g0.x));
+          o1[u] = a1 + __fmaf_rn(eg, __fmaf_rn(g1.w, ex, g1.z), __fmaf_rn(g1.y, ex, g1.x));
+          o2[u] = a2 + __fmaf_rn(eb, __fmaf_rn(g2.w, ex, g2.z), __fmaf_rn(g2.y, ex, g2.x));
+          if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
+        }
+        const long long rowoff = (long long)cur_y * p.w;
+        if (vec_ok && xl + PX <= p.w) {
+          stg_stream_vec<PX>(oplane0 + rowoff + xl, o0);
+          stg_stream_vec<PX>(oplane0 + pl + rowoff + xl, o1);
+          stg_stream_vec<PX>(oplane0 + 2 * pl + rowoff + xl, o2);
         } else {
 #pragma unroll
-          for (int u = 0; u < kPx; ++u) {
-            if (x + u < p.w) {
-              __stcs(oplane0 + rowoff + x + u, o0[u]);
-              __stcs(oplane0 + pl + rowoff + x + u, o1[u]);
-              __stcs(oplane0 + 2 * pl + rowoff + x + u, o2[u]);
+          for (int u = 0; u < PX; ++u) {
+            if (xl + u < p.w) {
+              __stcs(oplane0 + rowoff + xl + u, o0[u]);
+              __stcs(oplane0 + pl + rowoff + xl + u, o1[u]);
+              __stcs(oplane0 + 2 * pl + rowoff + xl + u, o2[u]);
             }
           }
         }
-      } else {
-#pragma unroll
-        for (int u = 0; u < kPx; ++u) {
-          const int xx = cur_x0 + lane + 32 * u;
-          if (xx < p.w) {
-            __stcs(oplane0 + rowoff + xx, o0[u]);
-            __stcs(oplane0 + pl + rowoff + xx, o1[u]);
-            __stcs(oplane0 + 2 * pl + rowoff + xx, o2[u]);
-          }
+        cur = nxt;
+        cur_y = nxt_y;
+        cur_k = nxt_k;
+      }
+      // ---- slots of row y+1 into the other buffer (free since the last barrier) ----
+      if (y < y_last) {
+        float ey1;
+        const int jy1 = (int)(row_bracket(p.y0 + y + 1, p.rcp_h, sdm1, sdm2, ey1) - kMagicBits);
+        float4* S = slots + (buf ^ 1) * nent;
+        for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+          const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
+          const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
+          S[e] = grid_entry(G, ds, ch, jx, jc, jy1, ey1);
         }
       }
-      cur = nxt;
-      cur_y = nxt_y;
-      cur_x0 = nxt_x0;
+      __syncthreads();
     }
-    c = phase_end;
+    r += y_last - y_first + 1;
   }
   if (CHECK) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.nonfinite, 1);
   }
 }
 
-static int g_num_sms = 0;
+size_t fwd_smem_bytes(int dt, int ds) {
+  const TableLayout L = TableLayout::make(dt, ds);
+  // staged tables + double-buffered per-row grid slots [jx][c][jc] (float4)
+  return (size_t)L.staged_bytes() + 2 * (size_t)(ds - 1) * 3 * (ds - 1) * 16;
+}
 
 int fwd_max_smem_bytes() { return kMaxSmemBytes - kSmemReserve; }
 
-template <bool IL, bool CHK>
-static cudaError_t launch_variant(const FwdParams& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = fused_fwd_kernel<IL, CHK>;
+static int g_num_sms = 0;
+
+// ---- texture objects over packed-table buffers --------------------------------
+// One linear float4 texture per (device, buffer, size), cached; evicted
+// objects are destroyed only after an event recorded behind their last use
+// has completed, so kernels still in flight never lose their texture.
+namespace {
+struct TexEntry {
+  int dev;
+  const void* base;
+  size_t bytes;
+  cudaTextureObject_t tex;
+  cudaEvent_t last_use;
+  unsigned long long stamp;
+  bool pinned;  // referenced by a captured CUDA graph: never retired
+};
+struct TexRetired {
+  cudaTextureObject_t tex;
+  cudaEvent_t ev;
+};
+std::mutex g_tex_mu;
+std::vector<TexEntry> g_tex;
+std::vector<TexRetired> g_tex_retired;
+unsigned long long g_tex_clock = 0;
+constexpr size_t kTexCache = 32;
+
+void reap_retired() {
+  for (size_t i = 0; i < g_tex_retired.size();) {
+    if (cudaEventQuery(g_tex_retired[i].ev) == cudaSuccess) {
+      cudaDestroyTextureObject(g_tex_retired[i].tex);
+      cudaEventDestroy(g_tex_retired[i].ev);
+      g_tex_retired[i] = g_tex_retired.back();
+      g_tex_retired.pop_back();
+    } else {
+      cudaGetLastError();  // clear cudaErrorNotReady
+      ++i;
+    }
+  }
+}
+
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+// Texture over [base, base + bytes); base must be textureAlignment-aligned.
+// During stream capture no events are queried or recorded and the entry is
+// pinned, since the graph keeps using the texture object on every replay.
+cudaError_t tex_for(int dev, const void* base, size_t bytes, cudaStream_t st, cudaTextureObject_t* out) {
+  std::lock_guard<std::mutex> lock(g_tex_mu);
+  const bool cap = capturing(st);
+  if (!cap) reap_retired();
+  TexEntry* hit = nullptr;
+  for (auto& e : g_tex)
+    if (e.dev == dev && e.base == base && e.bytes == bytes) hit = &e;
+  if (!hit) {
+    if (g_tex.size() >= kTexCache) {  // retire the least recently used unpinned entry
+      long lru = -1;
+      for (size_t i = 0; i < g_tex.size(); ++i)
+        if (!g_tex[i].pinned && (lru < 0 || g_tex[i].stamp < g_tex[lru].stamp)) lru = (long)i;
+      if (lru >= 0) {
+        g_tex_retired.push_back({g_tex[lru].tex, g_tex[lru].last_use});
+        g_tex[lru] = g_tex.back();
+        g_tex.pop_back();
+      }
+    }
+    cudaResourceDesc rd = {};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = const_cast<void*>(base);
+    rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+    rd.res.linear.sizeInBytes = bytes;
+    cudaTextureDesc td = {};
+    td.readMode = cudaReadModeElementType;
+    TexEntry e{dev, base, bytes, 0, nullptr, 0, false};
+    cudaError_t err = cudaCreateTextureObject(&e.tex, &rd, &td, nullptr);
+    if (err != cudaSuccess) return err;
+    err = cudaEventCreateWithFlags(&e.last_use, cudaEventDisableTiming);
+    if (err != cudaSuccess) return err;
+    g_tex.push_back(e);
+    hit = &g_tex.back();
+  }
+  hit->stamp = ++g_tex_clock;
+  hit->pinned |= cap;
+  *out = hit->tex;
+  return cudaSuccess;
+}
+
+// Marks the texture's last use after the launch just issued on `st`.
+cudaError_t tex_mark_used(cudaTextureObject_t tex, cudaStream_t st) {
+  if (capturing(st)) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(g_tex_mu);
+  for (auto& t : g_tex)
+    if (t.tex == tex) return cudaEventRecord(t.last_use, st);
+  return cudaSuccess;
+}
+}  // namespace
+
+template <int DT, int DS>
+static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t smem,
+                               cudaStream_t st) {
+  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps>
+                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // smallest shared-memory carve-out that fits: the rest of the 256 KB stays L1
+  // for the texture-path LUT pair
+  const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
   if (e != cudaSuccess) return e;
   kern<<<grid, kFwdWarps * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w,
-                             const float* tables, const TableLayout& L, const SpatialBr* col,
-                             const SpatialBr* row, int* nonfinite, int variant, cudaStream_t st) {
+cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,
+                             int h_total, const float* tables, const TableLayout& L,
+                             int* nonfinite, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
   if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   FwdParams p;
   p.rgb = rgb;
   p.out = out;
+  p.batch = batch;
   p.h = h;
   p.w = w;
+  p.y0 = y0;
   p.tables = tables;
   p.L = L;
-  p.col = col;
-  p.row = row;
-  p.cpr = (w + kChunk - 1) / kChunk;
-  p.per_img = (long long)h * p.cpr;
-  p.total = (long long)batch * p.per_img;
+  p.rcp_w = 1.0 / (double)(w - 1);
+  p.rcp_h = 1.0 / (double)(h_total - 1);
   p.nonfinite = nonfinite;
-  if (p.total == 0) return cudaSuccess;
+  const long long rows = (long long)batch * h;
+  if (rows == 0 || w == 0) return cudaSuccess;
+  // texture over the whole batch of tables, base aligned down to textureAlignment
+  int talign = 512;
+  cudaDeviceGetAttribute(&talign, cudaDevAttrTextureAlignment, dev);
+  const uintptr_t tb = reinterpret_cast<uintptr_t>(tables);
+  const uintptr_t base = tb / (uintptr_t)talign * (uintptr_t)talign;
+  const size_t bytes = (size_t)(tb - base) + (size_t)batch * L.bytes();
+  p.tex_base = (int)((tb - base) / 16);
+  cudaError_t e = tex_for(dev, reinterpret_cast<const void*>(base), bytes, st, &p.tex);
+  if (e != cudaSuccess) return e;
   long long grid = g_num_sms;
-  if (grid > p.total) grid = p.total;
-  const size_t smem = L.bytes();
-  const bool il = variant == 1;
-  if (nonfinite) {
-    return il ? launch_variant<true, true>(p, (int)grid, smem, st)
-              : launch_variant<false, true>(p, (int)grid, smem, st);
-  }
-  return il ? launch_variant<true, false>(p, (int)grid, smem, st)
-            : launch_variant<false, false>(p, (int)grid, smem, st);
+  if (grid > rows) grid = rows;
+  const size_t smem = fwd_smem_bytes(L.dt, L.ds);
+  const bool chk = nonfinite != nullptr;
+  if (L.dt == 33 && L.ds == 17) e = launch_dims<33, 17>(p, chk, (int)grid, smem, st);
+  else if (L.dt == 17 && L.ds == 8) e = launch_dims<17, 8>(p, chk, (int)grid, smem, st);
+  else e = launch_dims<0, 0>(p, chk, (int)grid, smem, st);
+  if (e != cudaSuccess) return e;
+  return tex_mark_used(p.tex, st);
 }
 
 }  // namespace svdlut

@@ -106,8 +106,7 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   const size_t n_lut = 9ull * d_t * d_t, n_grid = (size_t)k * 3 * d_s * d_s;
   const size_t par_floats = n_lut + 9 + 3 + n_grid + 3ull * k + k;
   const size_t tb = fast ? svdlut_table_bytes(d_t, d_s) : 0;
-  const size_t ws = svdlut_workspace_bytes(1, h, w, d_t, d_s);
-  const size_t par_bytes = rup(par_floats * 4) + rup(tb) + 2 * rup(ws) + 256;
+  const size_t par_bytes = rup(par_floats * 4) + rup(tb) + 256;
   const size_t img_bytes = 2 * rup((size_t)3 * h * w * 4);
   if (ensure(&ctx->d_img, &ctx->d_img_bytes, img_bytes) != cudaSuccess) return SVDLUT_ERR_CUDA;
   if (ensure(&ctx->d_par, &ctx->d_par_bytes, par_bytes) != cudaSuccess) return SVDLUT_ERR_CUDA;
@@ -120,8 +119,7 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   float* d_gw = d_grid + n_grid;
   float* d_gb = d_gw + 3ull * k;
   char* d_tables = (char*)ctx->d_par + rup(par_floats * 4);
-  char* d_ws = d_tables + rup(tb);
-  int* d_flag = (int*)(d_ws + 2 * rup(ws));
+  int* d_flag = (int*)(d_tables + rup(tb));
 
   cudaStream_t s0 = ctx->st[0];
   // ---- parameters + table prologue on stream 0 -----------------------------
@@ -155,8 +153,8 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
       return SVDLUT_ERR_CUDA;
     int rc;
     if (fast) {
-      rc = svdlut_fused_fwd_packed_ex(din, 1, hs, w, r0, h, d_tables, d_t, d_s, dout,
-                                      d_ws + (s & 1) * rup(ws), ws, d_flag, -1, st);
+      rc = svdlut_fused_fwd_packed_ex(din, 1, hs, w, r0, h, d_tables, d_t, d_s, dout, nullptr, 0,
+                                      d_flag, -1, st);
     } else {
       rc = svdlut_fused_fwd_exact(din, 1, hs, w, r0, h, d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb,
                                   k, d_s, dout, st);

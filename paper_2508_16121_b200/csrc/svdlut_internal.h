@@ -13,11 +13,11 @@ cudaError_t launch_pack(const float* lp, const float* lw, const float* lb, const
 cudaError_t launch_spatial(int w, int h, int y0, int h_total, int ds, SpatialBr* col,
                            SpatialBr* row, cudaStream_t st);
 
-// Fast fused forward from packed tables.  `variant` selects the lane→pixel
-// mapping (see svdlut_fwd.cu); -1 = default.
-cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w,
-                             const float* tables, const TableLayout& L, const SpatialBr* col,
-                             const SpatialBr* row, int* nonfinite, int variant, cudaStream_t st);
+// Fast fused forward from packed tables; spatial brackets are computed in the
+// kernel (rows of a strip y0.. of an image with h_total rows).
+cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,
+                             int h_total, const float* tables, const TableLayout& L,
+                             int* nonfinite, cudaStream_t st);
 
 cudaError_t launch_fused_exact(const float* rgb, float* out, int batch, int h, int w, int y0,
                                int h_total, const float* lp, const float* lw, const float* lb,
@@ -39,5 +39,7 @@ cudaError_t launch_reconstruct_bwd(const float* u, const float* s, const float* 
                                    float* ds, float* dvt, cudaStream_t st);
 
 int fwd_max_smem_bytes();
+// dynamic shared memory the fast kernel needs for (d_t, d_s): tables + per-warp row tables
+size_t fwd_smem_bytes(int dt, int ds);
 
 }  // namespace svdlut

@@ -58,15 +58,15 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
   const float* GB = gb + b * (long long)k;
   float* T = tables + b * (long long)L.total_floats;
 
-  const int n_lut = 3 * (dt - 1) * L.cst;     // cells incl. padding
-  const int n_xy = (ds - 1) * L.css;
-  const int n_xc = 3 * (ds - 1) * L.css;
-  const int n_yc = n_xc;
-  const int total = n_lut + n_xy + n_xc + n_yc + (L.total_floats - (L.yc_off + 12 * (ds - 1) * L.css));
-  const int tid0 = blockIdx.x * blockDim.x + threadIdx.x;
-  const int stride = gridDim.x * blockDim.x;
+  const int n_lut = 3 * (dt - 1) * L.cst;  // cells incl. padding
+  const int n_xc = 3 * (ds - 1) * (ds - 1);
+  const int n_gxy = ds * ds;  // vertices (3 floats each)
+  const int n_gyc = 3 * ds * ds;
+  const int n_pad = L.lut2_off - (L.gyc_off + n_gyc);
+  const int n_tail = L.total_floats - (L.lut2_off + L.pair_floats);
+  const int total = n_lut + n_xc + n_gxy + n_gyc + n_pad + n_tail;
 
-  for (int e = tid0; e < total; e += stride) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     if (e < n_lut) {
       const int p = e / ((dt - 1) * L.cst);
       const int rem = e - p * (dt - 1) * L.cst;
@@ -85,75 +85,60 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
         v[6 + c] = q.c;
         v[9 + c] = q.d;
       }
-      float* dst = T + L.lut_off + e * 12;
+      float* dst = T + L.pair_off(p) + rem * 12;
       for (int t = 0; t < 12; ++t) dst[t] = v[t];
       continue;
     }
     int r = e - n_lut;
-    if (r < n_xy) {
-      const int jx = r / L.css, jy = r - jx * L.css;
-      float v[12];
-      for (int c = 0; c < 3; ++c) {
-        Coef q = {0.f, 0.f, 0.f, 0.f};
-        if (jy < ds - 1) {
-          double p00 = 0, p10 = 0, p01 = 0, p11 = 0;
-          for (int kk = c; kk < k; kk += 3) {
-            const float* pl = G + (kk * 3 + 0) * ds * ds;
-            const double w = (double)GW[kk * 3 + 0];
-            p00 += w * pl[jx * ds + jy];
-            p10 += w * pl[(jx + 1) * ds + jy];
-            p01 += w * pl[jx * ds + jy + 1];
-            p11 += w * pl[(jx + 1) * ds + jy + 1];
-          }
-          q = cell_coef(p00, p10, p01, p11);
-        }
-        v[c] = q.a;
-        v[3 + c] = q.b;
-        v[6 + c] = q.c;
-        v[9 + c] = q.d;
+    if (r < n_xc) {  // merged xc cell (c, jx, jc)
+      const int c = r / ((ds - 1) * (ds - 1));
+      const int rem = r - c * (ds - 1) * (ds - 1);
+      const int ja = rem / (ds - 1), jc = rem - ja * (ds - 1);
+      double p00 = 0, p10 = 0, p01 = 0, p11 = 0;
+      for (int kk = c; kk < k; kk += 3) {
+        const float* pl = G + (kk * 3 + 1) * ds * ds;
+        const double w = (double)GW[kk * 3 + 1];
+        p00 += w * pl[ja * ds + jc];
+        p10 += w * pl[(ja + 1) * ds + jc];
+        p01 += w * pl[ja * ds + jc + 1];
+        p11 += w * pl[(ja + 1) * ds + jc + 1];
       }
-      float* dst = T + L.xy_off + r * 12;
-      for (int t = 0; t < 12; ++t) dst[t] = v[t];
-      continue;
-    }
-    r -= n_xy;
-    if (r < n_xc + n_yc) {
-      const int plane = r < n_xc ? 1 : 2;  // xc or yc
-      if (r >= n_xc) r -= n_xc;
-      const int c = r / ((ds - 1) * L.css);
-      const int rem = r - c * (ds - 1) * L.css;
-      const int ja = rem / L.css, jc = rem - ja * L.css;
-      Coef q = {0.f, 0.f, 0.f, 0.f};
-      if (jc < ds - 1) {
-        double p00 = 0, p10 = 0, p01 = 0, p11 = 0;
-        for (int kk = c; kk < k; kk += 3) {
-          const float* pl = G + (kk * 3 + plane) * ds * ds;
-          const double w = (double)GW[kk * 3 + plane];
-          p00 += w * pl[ja * ds + jc];
-          p10 += w * pl[(ja + 1) * ds + jc];
-          p01 += w * pl[ja * ds + jc + 1];
-          p11 += w * pl[(ja + 1) * ds + jc + 1];
-        }
-        if (plane == 2) {
-          // fold the channel's total bias lb[c] + sum gb[k] into the constant term
-          double bias = (double)Bl[c];
-          for (int kk = c; kk < k; kk += 3) bias += (double)GB[kk];
-          p00 += bias;
-          p10 += bias;
-          p01 += bias;
-          p11 += bias;
-        }
-        q = cell_coef(p00, p10, p01, p11);
-      }
-      float* dst = T + (plane == 1 ? L.xc_off : L.yc_off) + r * 4;
+      const Coef q = cell_coef(p00, p10, p01, p11);
+      float* dst = T + L.xc_off + r * 4;
       dst[0] = q.a;
       dst[1] = q.b;
       dst[2] = q.c;
       dst[3] = q.d;
       continue;
     }
-    r -= n_xc + n_yc;
-    T[L.yc_off + 12 * (ds - 1) * L.css + r] = 0.f;  // tail padding
+    r -= n_xc;
+    if (r < n_gxy) {  // merged xy vertex (a, b), channels packed
+      double acc[3] = {0.0, 0.0, 0.0};
+      for (int kk = 0; kk < k; ++kk) acc[kk % 3] += (double)GW[kk * 3 + 0] * G[(kk * 3 + 0) * ds * ds + r];
+      float* dst = T + L.gxy_off + r * 3;
+      dst[0] = (float)acc[0];
+      dst[1] = (float)acc[1];
+      dst[2] = (float)acc[2];
+      if (r == n_gxy - 1)  // alignment padding up to gyc_off
+        for (int t = L.gxy_off + n_gxy * 3; t < L.gyc_off; ++t) T[t] = 0.f;
+      continue;
+    }
+    r -= n_gxy;
+    if (r < n_gyc) {  // merged yc vertex (c, a, b) + channel bias
+      const int c = r / (ds * ds), ab = r - c * ds * ds;
+      double acc = (double)Bl[c];
+      for (int kk = c; kk < k; kk += 3) acc += (double)GB[kk];
+      for (int kk = c; kk < k; kk += 3) acc += (double)GW[kk * 3 + 2] * G[(kk * 3 + 2) * ds * ds + ab];
+      T[L.gyc_off + r] = (float)acc;
+      continue;
+    }
+    r -= n_gyc;
+    if (r < n_pad) {
+      T[L.gyc_off + n_gyc + r] = 0.f;  // padding before lut2
+      continue;
+    }
+    r -= n_pad;
+    T[L.lut2_off + L.pair_floats + r] = 0.f;  // tail padding
   }
 }
 
@@ -175,7 +160,7 @@ cudaError_t launch_reconstruct(const float* u, const float* s, const float* vt, 
 cudaError_t launch_pack(const float* lp, const float* lw, const float* lb, const float* gp,
                         const float* gw, const float* gb, int k, const TableLayout& L, int batch,
                         float* tables, cudaStream_t st) {
-  const int items = 3 * (L.dt - 1) * L.cst + 7 * (L.ds - 1) * L.css + 32;
+  const int items = L.total_floats / 4;
   dim3 grid((items + 255) / 256, batch);
   pack_kernel<<<grid, 256, 0, st>>>(lp, lw, lb, gp, gw, gb, k, L, tables);
   return cudaGetLastError();

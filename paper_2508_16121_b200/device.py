@@ -124,7 +124,7 @@ def apply(rgb, tables, out=None, y0=0, h_total=None, variant=-1, nonfinite=None)
     """Fused slice + LUT apply (fast fp32 kernel) from packed tables.
 
     ``nonfinite``: optional int32 CUDA tensor (1 element) OR-ed with 1 if any
-    output is NaN/Inf.  ``variant``: 0 = 128-bit lanes, 1 = interleaved lanes.
+    output is NaN/Inf.  ``variant`` is reserved.  One kernel launch.
     """
     rgb = _image(rgb, tables.batch)
     b, _, h, w = rgb.shape
@@ -133,11 +133,8 @@ def apply(rgb, tables, out=None, y0=0, h_total=None, variant=-1, nonfinite=None)
         out = torch.empty_like(rgb)
     elif out.shape != rgb.shape or not out.is_contiguous() or out.dtype != torch.float32:
         raise DimensionMismatch("out must be a contiguous float32 tensor shaped like rgb")
-    L = _lib.load()
-    ws_bytes = int(L.svdlut_workspace_bytes(0, h, w, tables.d_t, tables.d_s))
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=rgb.device)
     _lib.call("svdlut_fused_fwd_packed_ex", _p(rgb), b, h, w, y0, h_total, _p(tables.buf),
-              tables.d_t, tables.d_s, _p(out), _p(ws), ws_bytes, _p(nonfinite), variant,
+              tables.d_t, tables.d_s, _p(out), _p(None), 0, _p(nonfinite), variant,
               _stream(rgb))
     return out
 

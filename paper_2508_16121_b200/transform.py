@@ -91,12 +91,13 @@ def _c32(a):
 
 
 def fused_enhance(img, luts, lut_weights, grids, grid_weights, threads: int = 1,
-                  exact: bool = False):
+                  exact: bool = False, alloc=None):
     """Single-pass LUT transform plus grid slicing on the GPU.
 
     ``exact=True`` selects the f64 kernel whose output is bitwise equal to the
     reference; the default fp32 kernel agrees within 1e-5 with identical cell
-    selection.
+    selection.  ``alloc`` overrides the raster allocator (the plugin passes
+    the reference module's ``_alloc_raster`` so its ``_raster_hook`` fires).
     """
     del threads  # the GPU decides its own parallelism
     if grids.k % 3 != 0:
@@ -106,7 +107,9 @@ def fused_enhance(img, luts, lut_weights, grids, grid_weights, threads: int = 1,
     if img.width < 2 or img.height < 2:
         raise DegenerateImage("slicing needs at least 2 px in each direction")
     h, w = img.height, img.width
-    out = _alloc_raster((3, h, w))
+    out = (alloc or _alloc_raster)((3, h, w))
+    if not (out.flags.c_contiguous and out.dtype == np.float32 and out.flags.writeable):
+        raise DimensionMismatch("raster allocator must return a writable float32 C-contiguous array")
     rgb = _c32(img.data)
     planes = _c32(luts.planes)
     lw, lb = _c32(lut_weights.w), _c32(lut_weights.b)

@@ -46,10 +46,24 @@ def test_version_and_status_names(lib):
                          "BadVertexCount", "NonFiniteValue"]
 
 
+def layout_bytes(dt, ds):
+    """Python mirror of TableLayout (svdlut_common.cuh)."""
+    cst = (dt - 1) + ((3 - (dt - 1)) & 7)
+    pair = (dt - 1) * cst * 12
+    xc = 2 * pair
+    gxy = xc + 3 * (ds - 1) * (ds - 1) * 4
+    gyc = gxy + ((ds * ds * 3 + 3) & ~3)
+    lut2 = (gyc + 3 * ds * ds + 31) & ~31
+    return ((lut2 + pair + 31) & ~31) * 4
+
+
 def test_table_sizes(lib):
-    # d_t=33, d_s=17: 3*32*33*48 + 16*17*48 + 2*3*16*17*16 bytes, 128 B rounded
-    want = 3 * 32 * 33 * 48 + 16 * 17 * 48 + 2 * 3 * 16 * 17 * 16
-    assert lib.svdlut_table_bytes(33, 17) == (want + 127) // 128 * 128
+    # d_t=33, d_s=17: LUT row stride 35 (= 3 mod 8) -> 3 pairs of 32*35 cells x 48 B
+    assert 35 % 8 == 3
+    assert lib.svdlut_table_bytes(33, 17) == layout_bytes(33, 17)
+    assert layout_bytes(33, 17) >= 3 * 32 * 35 * 48 + 3 * 16 * 16 * 16 + 17 * 17 * 12 + 3 * 17 * 17 * 4
+    for dt, ds in ((2, 2), (7, 8), (17, 8), (65, 33)):
+        assert lib.svdlut_table_bytes(dt, ds) == layout_bytes(dt, ds)
     assert lib.svdlut_table_bytes(1, 17) == 0
     assert lib.svdlut_fast_supported(33, 17) == 1
     assert lib.svdlut_fast_supported(17, 8) == 1
