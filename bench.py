@@ -65,7 +65,7 @@ def dist_env():
 def workload_config(world):
     return {
         "workload": "config2: 1x3x2160x3840 fp32 smooth field per rank, d_t=33 n_s=8 d_s=17 K=6; "
-                    "step = reconstruct(U,S,Vt) + pack tables + fused slice/LUT apply",
+                    "step = tables from (U,S,Vt) on device + fused slice/LUT apply",
         "global_batch": world, "height": H, "width": W, "parallelism": f"per-image dp{world}",
         "l2": f"{N_ROT} rotating input/output sets ({N_ROT * 2 * 3 * H * W * 4 // 2**20} MiB) > L2",
     }
@@ -204,13 +204,14 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def eager_step(i):
-        planes = device.reconstruct(p["u"], p["s"], p["vt"])
-        tables = device.pack_tables(planes, p["lw"], p["lb"], p["grid_planes"], p["gw"], p["gb"])
+        # reconstruct(U,S,Vt) fused into the table packing, then the apply
+        tables = device.pack_tables_factors(p["u"], p["s"], p["vt"], p["lw"], p["lb"],
+                                            p["grid_planes"], p["gw"], p["gb"])
         device.apply(ins[i % N_ROT], tables, out=outs[i % N_ROT], variant=a.variant)
         return tables
 
     # One CUDA graph per rotating buffer set: a step is a single graph launch
-    # (reconstruct + pack + brackets + fused apply = 4 kernels), so host launch
+    # (factors->tables prologue + fused apply = 2 kernels), so host launch
     # latency never gates the device.
     graphs, apply_graphs = [], []
     tables0 = eager_step(0)
@@ -220,11 +221,11 @@ def main():
         torch.cuda.synchronize(dev)
         for i in range(N_ROT):
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, capture_error_mode="relaxed"):
                 eager_step(i)
             graphs.append(g)
             g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g2):
+            with torch.cuda.graph(g2, capture_error_mode="relaxed"):
                 device.apply(ins[i], tables0, out=outs[i], variant=a.variant)
             apply_graphs.append(g2)
 
@@ -344,7 +345,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded smooth field, SURVEY.md §8d recipe)",
             "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": 4 * a.steps, "clocks": sampler.summary(),
+            "e2e": e2e, "gpu_launches": 2 * a.steps, "clocks": sampler.summary(),
             "launch": "cuda graph per step" if graphs else "eager",
         }
         print(json.dumps(line), flush=True)

@@ -83,6 +83,15 @@ int svdlut_pack_tables(const float* lut_planes, const float* lw, const float* lb
                        const float* grid_planes, const float* gw, const float* gb, int k,
                        int d_s, int batch, void* tables, void* stream);
 
+/* Same tables straight from the SVD factors (svdlut_reconstruct fused into
+ * the packing; the planes are never materialised).  u (B,3,3,d_t,n_s),
+ * s (B,3,3,n_s), vt (B,3,3,n_s,d_t); LUT entries are bit-identical to
+ * svdlut_reconstruct's. */
+int svdlut_pack_tables_factors(const float* u, const float* s, const float* vt, int n_s,
+                               const float* lw, const float* lb, int d_t,
+                               const float* grid_planes, const float* gw, const float* gb, int k,
+                               int d_s, int batch, void* tables, void* stream);
+
 /* ---- forward ------------------------------------------------------------ */
 
 /* Fused slice + 2D-LUT apply from packed tables (fast fp32 kernel, within

@@ -29,6 +29,8 @@ _SIGS = {
     "svdlut_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
     "svdlut_reconstruct": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp]),
     "svdlut_pack_tables": (_i, [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i, _vp, _vp]),
+    "svdlut_pack_tables_factors": (_i, [_vp, _vp, _vp, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _i,
+                                        _vp, _vp]),
     "svdlut_fused_fwd_packed": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp, _sz, _vp]),
     "svdlut_fused_fwd_packed_ex": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp, _sz, _vp,
                                         _i, _vp]),

@@ -130,9 +130,28 @@ int svdlut_pack_tables(const float* lut_planes, const float* lw, const float* lb
     return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
   const TableLayout L = TableLayout::make(d_t, d_s);
-  CUDA_TRY(launch_pack(lut_planes, lw, lb, grid_planes, gw, gb, k, L, batch, (float*)tables,
-                       (cudaStream_t)stream),
+  CUDA_TRY(launch_pack(lut_planes, nullptr, nullptr, nullptr, 0, lw, lb, grid_planes, gw, gb, k, L,
+                       batch, (float*)tables, (cudaStream_t)stream),
            "svdlut_pack_tables");
+  return SVDLUT_OK;
+}
+
+int svdlut_pack_tables_factors(const float* u, const float* s, const float* vt, int n_s,
+                               const float* lw, const float* lb, int d_t,
+                               const float* grid_planes, const float* gw, const float* gb, int k,
+                               int d_s, int batch, void* tables, void* stream) {
+  int rc;
+  if ((rc = check_k(k)) != SVDLUT_OK) return rc;
+  if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
+  if (n_s < 1 || n_s > d_t) return fail(SVDLUT_ERR_DIMENSION_MISMATCH, "rank %d outside 1..%d", n_s, d_t);
+  if (batch == 0) return SVDLUT_OK;
+  if (!u || !s || !vt || !lw || !lb || !grid_planes || !gw || !gb || !tables)
+    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
+  const TableLayout L = TableLayout::make(d_t, d_s);
+  CUDA_TRY(launch_pack(nullptr, u, s, vt, n_s, lw, lb, grid_planes, gw, gb, k, L, batch,
+                       (float*)tables, (cudaStream_t)stream),
+           "svdlut_pack_tables_factors");
   return SVDLUT_OK;
 }
 

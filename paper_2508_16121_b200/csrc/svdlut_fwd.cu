@@ -58,6 +58,7 @@ struct FwdParams {
   double rcp_w;             // RN64(1 / (W - 1)) for the exact column brackets
   double rcp_h;             // RN64(1 / (h_total - 1)) for the row brackets
   int* nonfinite;
+  int col_smem;             // 1: column brackets come from a per-CTA smem table of t values
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -251,6 +252,16 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const uint32_t table_bytes = (uint32_t)L.staged_bytes();  // smem prefix (all but lut2)
   const int nent = (ds - 1) * 3 * (ds - 1);                  // slot entries per row
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
+  // column table: t(x) = RN32(RN32(x/(W-1)) * (d_s-1)) for every column, built once
+  float* col_t = reinterpret_cast<float*>(slots + 2 * nent);
+  const uint32_t col_addr = smem_addr(col_t);
+  if (p.col_smem) {
+    const int wpad = (p.w + 3) & ~3;
+    for (int x = threadIdx.x; x < wpad; x += blockDim.x) {
+      const int xc = min(x, p.w - 1);
+      col_t[x] = __fmul_rn(__double2float_rn(__dmul_rn((double)xc, p.rcp_w)), (float)(ds - 1));
+    }
+  }
 
   GridG G;
   G.xc = reinterpret_cast<const float4*>(smem + L.xc_off);
@@ -340,9 +351,29 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         const int xl = cur_k * CH + PX * lane;
         int jxs[PX];
         float exs[PX];
+        if (p.col_smem) {
+          float ts[PX];
+          if (PX == 4) {
+            // lanes past the row end read the last (in-bounds) group; their
+            // pixels are never stored
+            const int xt = min(xl, ((p.w + 3) & ~3) - 4);
+            const float4 t4 = lds4(col_addr + (uint32_t)xt * 4u);
+            ts[0] = t4.x; ts[PX > 1 ? 1 : 0] = t4.y; ts[PX > 2 ? 2 : 0] = t4.z; ts[PX > 3 ? 3 : 0] = t4.w;
+          } else {
 #pragma unroll
-        for (int u = 0; u < PX; ++u)
-          jxs[u] = (int)(col_bracket(min(xl + u, p.w - 1), p.rcp_w, sdm1, sdm2, exs[u]) - kMagicBits);
+            for (int u = 0; u < PX; ++u) ts[u] = col_t[min(xl + u, p.w - 1)];
+          }
+#pragma unroll
+          for (int u = 0; u < PX; ++u) {
+            const float m = __fadd_rz(fminf(ts[u], sdm2), 8388608.0f);
+            exs[u] = ts[u] - (m - 8388608.0f);
+            jxs[u] = (int)(__float_as_uint(m) - kMagicBits);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < PX; ++u)
+            jxs[u] = (int)(col_bracket(min(xl + u, p.w - 1), p.rcp_w, sdm1, sdm2, exs[u]) - kMagicBits);
+        }
 
         // Pair gb is gathered through the texture path one pixel ahead of its
         // use (software pipeline depth 1), hiding the texture latency behind
@@ -444,6 +475,11 @@ size_t fwd_smem_bytes(int dt, int ds) {
   // staged tables + double-buffered per-row grid slots [jx][c][jc] (float4)
   return (size_t)L.staged_bytes() + 2 * (size_t)(ds - 1) * 3 * (ds - 1) * 16;
 }
+
+// Keep at least this much of the 256 KB L1/shared array as L1 so the
+// texture-path LUT pair stays resident; the column table is added only if it
+// fits under the limit.
+constexpr size_t kSmemForL1Tex = 196 * 1024 - 2048;
 
 int fwd_max_smem_bytes() { return kMaxSmemBytes - kSmemReserve; }
 
@@ -553,13 +589,20 @@ static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t 
                                cudaStream_t st) {
   auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps>
                     : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  // smallest shared-memory carve-out that fits: the rest of the 256 KB stays L1
-  // for the texture-path LUT pair
-  const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
-  if (e != cudaSuccess) return e;
+  // function attributes are set once per (instantiation, smem size); setting
+  // them is not a stream operation, so graph capture does not see it
+  static size_t configured[2] = {0, 0};
+  cudaError_t e = cudaSuccess;
+  if (configured[check] != smem) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // smallest shared-memory carve-out that fits: the rest of the 256 KB stays
+    // L1 for the texture-path LUT pair
+    const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+    if (e != cudaSuccess) return e;
+    configured[check] = smem;
+  }
   kern<<<grid, kFwdWarps * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -598,7 +641,10 @@ cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int
   if (e != cudaSuccess) return e;
   long long grid = g_num_sms;
   if (grid > rows) grid = rows;
-  const size_t smem = fwd_smem_bytes(L.dt, L.ds);
+  size_t smem = fwd_smem_bytes(L.dt, L.ds);
+  const size_t col_bytes = (size_t)((w + 3) & ~3) * 4;
+  p.col_smem = smem + col_bytes <= kSmemForL1Tex ? 1 : 0;
+  if (p.col_smem) smem += col_bytes;
   const bool chk = nonfinite != nullptr;
   if (L.dt == 33 && L.ds == 17) e = launch_dims<33, 17>(p, chk, (int)grid, smem, st);
   else if (L.dt == 17 && L.ds == 8) e = launch_dims<17, 8>(p, chk, (int)grid, smem, st);

@@ -7,9 +7,11 @@ namespace svdlut {
 
 cudaError_t launch_reconstruct(const float* u, const float* s, const float* vt, int batch, int dt,
                                int ns, float* planes, cudaStream_t st);
-cudaError_t launch_pack(const float* lp, const float* lw, const float* lb, const float* gp,
-                        const float* gw, const float* gb, int k, const TableLayout& L, int batch,
-                        float* tables, cudaStream_t st);
+// LUT planes from `lp`, or (lp == NULL) reconstructed on the fly from (fu, fs, fvt, ns).
+cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const float* fvt, int ns,
+                        const float* lw, const float* lb, const float* gp, const float* gw,
+                        const float* gb, int k, const TableLayout& L, int batch, float* tables,
+                        cudaStream_t st);
 cudaError_t launch_spatial(int w, int h, int y0, int h_total, int ds, SpatialBr* col,
                            SpatialBr* row, cudaStream_t st);
 

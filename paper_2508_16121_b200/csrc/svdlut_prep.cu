@@ -43,14 +43,30 @@ __device__ __forceinline__ Coef cell_coef(double p00, double p10, double p01, do
   return k;
 }
 
+// One reconstructed LUT entry, identical to reconstruct_kernel's output:
+// f32(sum_m (f64 U[i,m] * f64 S[m]) * f64 Vt[m,j]) in index order, no FMA.
+__device__ __forceinline__ float lut_entry(const float* __restrict__ U, const float* __restrict__ S,
+                                           const float* __restrict__ V, int dt, int ns, int i,
+                                           int j) {
+  double acc = 0.0;
+  for (int m = 0; m < ns; ++m)
+    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn((double)U[i * ns + m], (double)S[m]), (double)V[m * dt + j]));
+  return (float)acc;
+}
+
 // Packs one image's tables (layout in svdlut_common.cuh).  grid.y = image.
-__global__ void pack_kernel(const float* __restrict__ lp, const float* __restrict__ lw,
+// The LUT planes come either from `lp` (B,3,3,d_t,d_t) or, when lp == NULL,
+// straight from the SVD factors (u, s, vt, n_s) — the fused prologue that
+// skips materialising the planes.
+__global__ void pack_kernel(const float* __restrict__ lp, const float* __restrict__ fu,
+                            const float* __restrict__ fs, const float* __restrict__ fvt, int ns,
+                            const float* __restrict__ lw,
                             const float* __restrict__ lb, const float* __restrict__ gp,
                             const float* __restrict__ gw, const float* __restrict__ gb, int k,
                             TableLayout L, float* __restrict__ tables) {
   const long long b = blockIdx.y;
   const int dt = L.dt, ds = L.ds;
-  const float* P = lp + b * 9LL * dt * dt;
+  const float* P = lp ? lp + b * 9LL * dt * dt : nullptr;
   const float* W = lw + b * 9;
   const float* Bl = lb + b * 3;
   const float* G = gp + b * (long long)k * 3 * ds * ds;
@@ -75,10 +91,25 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
       for (int c = 0; c < 3; ++c) {
         Coef q = {0.f, 0.f, 0.f, 0.f};
         if (j < dt - 1) {
-          const float* pl = P + (c * 3 + p) * dt * dt;
           const double w = (double)W[c * 3 + p];
-          q = cell_coef(w * pl[i * dt + j], w * pl[(i + 1) * dt + j], w * pl[i * dt + j + 1],
-                        w * pl[(i + 1) * dt + j + 1]);
+          float t00, t10, t01, t11;
+          if (P) {
+            const float* pl = P + (c * 3 + p) * dt * dt;
+            t00 = pl[i * dt + j];
+            t10 = pl[(i + 1) * dt + j];
+            t01 = pl[i * dt + j + 1];
+            t11 = pl[(i + 1) * dt + j + 1];
+          } else {
+            const long long cp = b * 9 + c * 3 + p;
+            const float* U = fu + cp * dt * ns;
+            const float* S = fs + cp * ns;
+            const float* V = fvt + cp * ns * dt;
+            t00 = lut_entry(U, S, V, dt, ns, i, j);
+            t10 = lut_entry(U, S, V, dt, ns, i + 1, j);
+            t01 = lut_entry(U, S, V, dt, ns, i, j + 1);
+            t11 = lut_entry(U, S, V, dt, ns, i + 1, j + 1);
+          }
+          q = cell_coef(w * t00, w * t10, w * t01, w * t11);
         }
         v[c] = q.a;
         v[3 + c] = q.b;
@@ -157,12 +188,15 @@ cudaError_t launch_reconstruct(const float* u, const float* s, const float* vt, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack(const float* lp, const float* lw, const float* lb, const float* gp,
-                        const float* gw, const float* gb, int k, const TableLayout& L, int batch,
-                        float* tables, cudaStream_t st) {
-  const int items = L.total_floats / 4;
-  dim3 grid((items + 255) / 256, batch);
-  pack_kernel<<<grid, 256, 0, st>>>(lp, lw, lb, gp, gw, gb, k, L, tables);
+cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const float* fvt, int ns,
+                        const float* lw, const float* lb, const float* gp, const float* gw,
+                        const float* gb, int k, const TableLayout& L, int batch, float* tables,
+                        cudaStream_t st) {
+  // one thread per LUT cell / grid entry; small blocks spread the latency-bound
+  // f64 work over many SMs
+  const int items = 3 * (L.dt - 1) * L.cst + 3 * (L.ds - 1) * (L.ds - 1) + 4 * L.ds * L.ds + 64;
+  dim3 grid((items + 63) / 64, batch);
+  pack_kernel<<<grid, 64, 0, st>>>(lp, fu, fs, fvt, ns, lw, lb, gp, gw, gb, k, L, tables);
   return cudaGetLastError();
 }
 

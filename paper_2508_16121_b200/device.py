@@ -23,7 +23,8 @@ from . import _lib
 from .errors import DimensionMismatch
 
 __all__ = [
-    "table_bytes", "fast_supported", "PackedTables", "reconstruct", "pack_tables", "apply",
+    "table_bytes", "fast_supported", "PackedTables", "reconstruct", "pack_tables",
+    "pack_tables_factors", "apply",
     "apply_exact", "fused_forward", "indices", "fused_backward", "reconstruct_backward",
 ]
 
@@ -109,6 +110,28 @@ def pack_tables(lut_planes, lw, lb, grid_planes, gw, gb):
     _lib.call("svdlut_pack_tables", _p(lp), _p(lw), _p(lb), d_t, _p(gp), _p(gw), _p(gb), k, d_s,
               b, _p(buf), _stream(lp))
     return PackedTables(buf, b, d_t, d_s)
+
+
+def pack_tables_factors(u, s, vt, lw, lb, grid_planes, gw, gb):
+    """Tables straight from the SVD factors (reconstruct fused into packing)."""
+    u, s, vt = _f32(u, "u", 5), _f32(s, "s", 4), _f32(vt, "vt", 5)
+    b, _, _, d, n = u.shape
+    if tuple(s.shape) != (b, 3, 3, n) or tuple(vt.shape) != (b, 3, 3, n, d):
+        raise DimensionMismatch(f"inconsistent factor shapes {tuple(u.shape)} {tuple(s.shape)} "
+                                f"{tuple(vt.shape)}")
+    lw, lb = _f32(lw, "lw", 3), _f32(lb, "lb", 2)
+    gp = _f32(grid_planes, "grid_planes", 5)
+    gw, gb = _f32(gw, "gw", 3), _f32(gb, "gb", 2)
+    k, d_s = gp.shape[1], gp.shape[3]
+    if tuple(lw.shape) != (b, 3, 3) or tuple(lb.shape) != (b, 3) or gp.shape[0] != b:
+        raise DimensionMismatch("weights / grids disagree with the factors' batch")
+    if tuple(gw.shape) != (b, k, 3) or tuple(gb.shape) != (b, k):
+        raise DimensionMismatch(f"{k} grids but weights shaped {tuple(gw.shape)} {tuple(gb.shape)}")
+    nbytes = table_bytes(d, d_s)
+    buf = torch.empty(b * nbytes // 4, dtype=torch.float32, device=u.device)
+    _lib.call("svdlut_pack_tables_factors", _p(u), _p(s), _p(vt), n, _p(lw), _p(lb), d, _p(gp),
+              _p(gw), _p(gb), k, d_s, b, _p(buf), _stream(u))
+    return PackedTables(buf, b, d, d_s)
 
 
 def _image(rgb, batch):

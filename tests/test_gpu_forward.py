@@ -242,3 +242,24 @@ def test_drop_in_nonfinite_raises(dev):
         transform.fused_enhance(Image(16, 8, c["rgb"]), Lut2DSet(c["lp"]),
                                 LutWeights(np.full((3, 3), 3e38, np.float32), c["lb"]),
                                 GridSet(np.abs(c["gp"]) + 1), GridWeights(np.full((6, 3), 3e38), c["gb"]))
+
+
+def test_pack_from_factors_equals_reconstruct_then_pack(dev):
+    import torch
+
+    from paper_2508_16121_b200 import device, synth
+
+    case = synth.make_batch([11, 12], h=64, w=96)
+    t = {k: T(getattr(case, k), dev) for k in ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")}
+    planes = device.reconstruct(t["u"], t["s"], t["vt"])
+    a = device.pack_tables(planes, t["lw"], t["lb"], t["grid_planes"], t["gw"], t["gb"])
+    b = device.pack_tables_factors(t["u"], t["s"], t["vt"], t["lw"], t["lb"], t["grid_planes"],
+                                   t["gw"], t["gb"])
+    assert torch.equal(a.buf, b.buf)
+
+
+def test_column_table_and_inline_brackets_agree(dev, oracle_mod):
+    """Very wide rows fall back to in-kernel column brackets (no smem table)."""
+    c = make_inputs(20000, 3, d_t=17, d_s=8, seed=21)
+    want = oracle_out(oracle_mod, c)
+    assert np.abs(fast(c, dev) - want).max() <= TOL
