@@ -1,0 +1,52 @@
+"""Training path: the fused apply as a torch.autograd.Function (config 5).
+
+    y = svdlut_apply(rgb, u, s, vt, lw, lb, grid_planes, gw, gb)
+    loss = ((y - target) ** 2).mean(); loss.backward()
+
+Forward: LUT reconstruction from the SVD factors + table packing + the fused
+sm_100a kernel.  Backward: svdlut_fused_bwd (input gradient and
+warp-aggregated shared-memory scatter of the LUT / grid vertex gradients) and
+svdlut_reconstruct_bwd (dU, dS, dVt).  Gradient conventions at cell
+boundaries and the clamp follow SURVEY.md Appendix B (the reference itself
+has no backward).  Accepts batched (B, ...) or unbatched tensors.
+"""
+
+import torch
+
+from . import device
+
+__all__ = ["SvdLutApply", "svdlut_apply"]
+
+
+class SvdLutApply(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, rgb, u, s, vt, lw, lb, grid_planes, gw, gb, y0=0, h_total=None):
+        batched = rgb.dim() == 4
+        planes = device.reconstruct(u, s, vt)
+        if device.fast_supported(planes.shape[-1], grid_planes.shape[-1]):
+            tables = device.pack_tables(planes, lw, lb, grid_planes, gw, gb)
+            out = device.apply(rgb, tables, y0=y0, h_total=h_total)
+        else:
+            out = device.apply_exact(rgb, planes, lw, lb, grid_planes, gw, gb, y0=y0,
+                                     h_total=h_total)
+        ctx.save_for_backward(rgb, u, s, vt, planes, lw, grid_planes, gw)
+        ctx.y0, ctx.h_total, ctx.batched = y0, h_total, batched
+        ctx.shapes = [t.shape for t in (rgb, u, s, vt, lw, lb, grid_planes, gw, gb)]
+        return out if batched else out[0]
+
+    @staticmethod
+    def backward(ctx, gy):
+        rgb, u, s, vt, planes, lw, grid_planes, gw = ctx.saved_tensors
+        gy = gy.contiguous()
+        g = device.fused_backward(rgb, gy, planes, lw, grid_planes, gw, y0=ctx.y0,
+                                  h_total=ctx.h_total, need_gx=ctx.needs_input_grad[0])
+        du, ds, dvt = device.reconstruct_backward(u, s, vt, g["dlut_planes"])
+        grads = [g["gx"], du, ds, dvt, g["dlw"], g["dlb"], g["dgrid_planes"], g["dgw"], g["dgb"]]
+        out = []
+        for gr, shape, need in zip(grads, ctx.shapes, ctx.needs_input_grad[:9]):
+            out.append(gr.reshape(shape) if (need and gr is not None) else None)
+        return (*out, None, None)
+
+
+def svdlut_apply(rgb, u, s, vt, lw, lb, grid_planes, gw, gb, y0=0, h_total=None):
+    return SvdLutApply.apply(rgb, u, s, vt, lw, lb, grid_planes, gw, gb, y0, h_total)

@@ -1,335 +1,525 @@
 // svdlut_bwd.cu — K3/K4: backward of the fused apply and of the LUT
 // reconstruction.  The reference has no backward;
 // the math follows SURVEY.md Appendix B and is pinned against the f64 oracle
-// (oracle_fused_bwd) and finite differences.
+// (oracle_fused_bwd), itself pinned by autograd and finite differences.
 //
-// Structure
-//   pack_vertex_kernel  per image: weight-folded LUT vertices (channel-packed
-//                       float4) and per-channel merged grid planes — the
-//                       tables the input gradient needs.
-//   fused_bwd_kernel    persistent CTA per SM.  Per pixel: recompute the
-//                       brackets, gx from the vertex tables, and scatter-add
-//                       gY·w_uv into UNWEIGHTED per-CTA shared-memory
-//                       accumulators E (LUT: [pair][i][j][c], grids:
-//                       [plane][c][a][b]).  Consecutive pixels of a lane that
-//                       hit the same cell are merged in registers first
-//                       (run-length aggregation), so smooth images issue far
-//                       fewer shared atomics than pixels × corners.  At the
-//                       end of each image phase the CTA flushes its non-zero
-//                       accumulators to a global E with one atomic each.
-//   finalize_kernel     dlut = lw·E, dlw = <T, E>, dgrid[k,q] = gw[k,q]·E[q,k%3],
-//                       dgw = <G, E>, dlb / dgb from the per-image gY sums.
-//   reconstruct_bwd     dU = dT·Vtᵀ·diag S, dS = diag(Uᵀ dT Vtᵀ), dVt = diag S·Uᵀ·dT.
+// fused_bwd_kernel mirrors the forward kernel's structure (svdlut_fwd.cu):
+// persistent CTA per SM over a contiguous row range, the same packed
+// coefficient tables staged by TMA (LUT pairs rg/rb + grids in shared memory,
+// pair gb through the texture path), the same per-row merged grid slots.
+//   gX    from the coefficient form: d/da (A + B a + C b + D a b) = B + D b,
+//         d/db = C + D a; grid slot d/dec = M' + N' ex; the strict clamp of
+//         interp.py:37-40 zeroes the gradient outside [0, 1].
+//   E     UNWEIGHTED scatter sums  E_lut[p][i][j][c] = sum gY_c w_ij and
+//         E_grid[q][c][a][b], accumulated per CTA in shared memory.  Lanes
+//         holding the same cell are aggregated first (warp match + shuffle
+//         group sums), so each distinct cell costs one shared atomic per
+//         value per warp instruction; the xy plane (x-cell almost uniform per
+//         chunk, y-cell uniform per row) is summed in registers per chunk.
+//   flush at the end of each image phase: non-zero shared sums -> global E
+//         (one native f32 RED each).
+// finalize_kernel: dlut = lw * E, dlw = <T, E>, dgrid[k,q] = gw[k,q] * E[q][k%3],
+// dgw = <G, E>, dlb / dgb from the per-image gY sums.
 #include <cstdint>
 #include "svdlut_common.cuh"
 #include "svdlut_internal.h"
 
 namespace svdlut {
 
-constexpr int kBwdThreads = 512;
-constexpr int kRun = 8;  // consecutive pixels per lane (run-length window)
+constexpr int kBwdWarps = 15;
+constexpr int kBPx = 4;
+constexpr int kBChunk = 32 * kBPx;
+constexpr uint32_t kMagic = 0x4B000000u;
 
-struct VtxLayout {
-  int dt, ds;
-  int lut_off;   // float4 [3][dt][dt]
-  int xy_off;    // float4 [ds][ds]
-  int xc_off;    // float  [3][ds][ds]
-  int yc_off;    // float  [3][ds][ds]
-  int total;     // floats (multiple of 4)
-  __host__ __device__ static VtxLayout make(int dt, int ds) {
-    VtxLayout L;
-    L.dt = dt;
-    L.ds = ds;
-    L.lut_off = 0;
-    L.xy_off = 3 * dt * dt * 4;
-    L.xc_off = L.xy_off + ds * ds * 4;
-    L.yc_off = L.xc_off + 3 * ds * ds;
-    L.total = (L.yc_off + 3 * ds * ds + 3) & ~3;
-    return L;
+// Global accumulator layout per image (floats): lut [p 3][i d_t][j d_t][c 3],
+// grid [q 3 (xy|xc|yc)][c 3][a d_s][b d_s], then gsum [4].
+struct AccLayout {
+  int dt, ds, lut_off, grid_off, gsum_off, total;
+  __host__ __device__ static AccLayout make(int dt, int ds) {
+    AccLayout A;
+    A.dt = dt;
+    A.ds = ds;
+    A.lut_off = 0;
+    A.grid_off = 3 * dt * dt * 3;
+    A.gsum_off = A.grid_off + 9 * ds * ds;
+    A.total = (A.gsum_off + 4 + 3) & ~3;
+    return A;
   }
-};
-// E accumulators share the vertex layout (lut [p][i][j][c(4)], xy [a][b][c(4)], xc/yc [c][a][b]).
-
-struct BwdWs {
-  float* vtx;     // batch * VtxLayout.total
-  float* E;       // batch * VtxLayout.total (global accumulators)
-  float* gsum;    // batch * 4 (sum of gY per channel)
-  SpatialBr* col;
-  SpatialBr* row;
 };
 
 static size_t rup(size_t v) { return (v + 255) / 256 * 256; }
 
 size_t bwd_workspace_bytes(int batch, int h, int w, int dt, int ds, int k) {
-  (void)k;
-  const VtxLayout L = VtxLayout::make(dt, ds);
-  return 2 * rup((size_t)batch * L.total * 4) + rup((size_t)batch * 16) +
-         rup((size_t)w * sizeof(SpatialBr)) + rup((size_t)h * sizeof(SpatialBr)) + 256;
+  (void)h;
+  (void)w;
+  const TableLayout L = TableLayout::make(dt, ds);
+  const AccLayout A = AccLayout::make(dt, ds);
+  return rup((size_t)batch * L.bytes()) + rup((size_t)batch * A.total * 4) +
+         rup((size_t)batch * (3 + k) * 4) + rup((size_t)batch * 4) + 256;
 }
-
-static BwdWs carve(void* ws, int batch, int h, int w, const VtxLayout& L) {
-  char* p = (char*)ws;
-  BwdWs W;
-  W.vtx = (float*)p;
-  p += rup((size_t)batch * L.total * 4);
-  W.E = (float*)p;
-  p += rup((size_t)batch * L.total * 4);
-  W.gsum = (float*)p;
-  p += rup((size_t)batch * 16);
-  W.col = (SpatialBr*)p;
-  p += rup((size_t)w * sizeof(SpatialBr));
-  W.row = (SpatialBr*)p;
-  return W;
-}
-
-__global__ void pack_vertex_kernel(const float* __restrict__ lp, const float* __restrict__ lw,
-                                   const float* __restrict__ gp, const float* __restrict__ gw,
-                                   int k, VtxLayout L, float* __restrict__ vtx) {
-  const long long b = blockIdx.y;
-  const int dt = L.dt, ds = L.ds;
-  const float* P = lp + b * 9LL * dt * dt;
-  const float* W = lw + b * 9;
-  const float* G = gp + b * (long long)k * 3 * ds * ds;
-  const float* GW = gw + b * (long long)k * 3;
-  float* V = vtx + b * (long long)L.total;
-  const int n_lut = 3 * dt * dt, n_xy = ds * ds, n_c = 3 * ds * ds;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_lut + n_xy + 2 * n_c;
-       e += gridDim.x * blockDim.x) {
-    if (e < n_lut) {
-      const int p = e / (dt * dt), ij = e - p * dt * dt;
-      float4 v;
-      v.x = W[0 * 3 + p] * P[(0 * 3 + p) * dt * dt + ij];
-      v.y = W[1 * 3 + p] * P[(1 * 3 + p) * dt * dt + ij];
-      v.z = W[2 * 3 + p] * P[(2 * 3 + p) * dt * dt + ij];
-      v.w = 0.f;
-      reinterpret_cast<float4*>(V + L.lut_off)[e] = v;
-    } else if (e < n_lut + n_xy) {
-      const int ab = e - n_lut;
-      float acc[3] = {0.f, 0.f, 0.f};
-      for (int kk = 0; kk < k; ++kk) acc[kk % 3] += GW[kk * 3 + 0] * G[(kk * 3 + 0) * ds * ds + ab];
-      reinterpret_cast<float4*>(V + L.xy_off)[ab] = make_float4(acc[0], acc[1], acc[2], 0.f);
-    } else {
-      int r = e - n_lut - n_xy;
-      const int q = r < n_c ? 1 : 2;
-      if (r >= n_c) r -= n_c;
-      const int c = r / (ds * ds), ab = r - c * ds * ds;
-      float acc = 0.f;
-      for (int kk = c; kk < k; kk += 3) acc += GW[kk * 3 + q] * G[(kk * 3 + q) * ds * ds + ab];
-      V[(q == 1 ? L.xc_off : L.yc_off) + r] = acc;
-    }
-  }
-}
-
-// Per-lane run-length accumulator for one bilinear term with C channels.
-template <int C>
-struct RunAcc {
-  int key;           // packed cell id, -1 = empty
-  float v[4][C];     // corner accumulators (00, 10, 01, 11)
-};
 
 struct BwdParams {
   const float* rgb;
   const float* gy;
   float* gx;
-  int h, w;
-  VtxLayout L;
-  const float* vtx;
-  float* E;
-  float* gsum;
-  const SpatialBr* col;
-  const SpatialBr* row;
-  int rpr;             // runs per row (row split into kRun-pixel runs)
-  long long per_img;   // h * rpr
-  long long total;
+  int batch, h, w, y0;
+  const float* tables;
+  TableLayout L;
+  AccLayout A;
+  cudaTextureObject_t tex;
+  int tex_base;
+  double rcp_w, rcp_h;
+  float* E;            // global accumulators, batch * A.total
+  const float* gmax;   // per image max|gY| (fixed-point scale)
 };
 
-// Flush a run: 4 corners x C channels of shared atomics.  C == 3 tables are
-// float4-strided ([a][b][4]); C == 1 tables are scalar ([a][b]).
-template <int C>
-__device__ __forceinline__ void flush(RunAcc<C>& R, float* base, int stride) {
-  if (R.key < 0) return;
-  constexpr int S = C == 3 ? 4 : 1;
-  const int a = R.key >> 16, b = R.key & 0xffff;
-  float* p00 = base + (a * stride + b) * S;
-  float* p10 = base + ((a + 1) * stride + b) * S;
-  float* p01 = base + (a * stride + b + 1) * S;
-  float* p11 = base + ((a + 1) * stride + b + 1) * S;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    atomicAdd(p00 + c, R.v[0][c]);
-    atomicAdd(p10 + c, R.v[1][c]);
-    atomicAdd(p01 + c, R.v[2][c]);
-    atomicAdd(p11 + c, R.v[3][c]);
-  }
-  R.key = -1;
+__device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float4 blds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, float& delta) {
+  const float t = fminf(__fmul_rz(q, dm1), dm2);
+  const float m = __fadd_rz(t, 8388608.0f);
+  delta = __fmaf_rn(q, dm1, -(m - 8388608.0f));
+  return __float_as_uint(m);
 }
 
-template <int C>
-__device__ __forceinline__ void run_add(RunAcc<C>& R, int key, float* base, int stride,
-                                        const float* g, float a, float b) {
-  if (R.key != key) {
-    flush<C>(R, base, stride);
-    R.key = key;
+// Scatter values are accumulated as 32-bit fixed point: v * S with
+// S = 2^16 / max|gY| of the image, so one contribution is at most 2^16 in
+// magnitude (resolution 1.5e-5 max|gY|).  Conversion is an add of 1.5*2^23
+// (round to nearest even on the FMA pipe).  Shared integer atomics are native
+// (ATOMS.ADD, ~2 cycles per warp instruction with distinct addresses, measured
+// in tools/microbench/atomicbench.cu) whereas shared f32 atomics are CAS loops
+// (7 cycles, and ~multiplicity x worse under sharing).
+//   LUT   one atomic per value per pixel (lanes hold pixels 4 apart, so a warp
+//         instruction's cells rarely collide);
+//   grids per-lane runs over the lane's 4 consecutive pixels, then one loop
+//         over the distinct keys of the warp with full-mask REDUX sums.
+// Shared sums are flushed to the global f32 accumulators at least every
+// kFlushPx pixels: every shared partial stays below (kFlushPx + W) * 2^16 < 2^31
+// for rows up to 24K pixels wide.
+constexpr int kFlushPx = 8192;
+constexpr float kFixedOne = 65536.0f;
+__device__ __forceinline__ int to_fixed(float v, float S) {
+  return __float_as_int(__fmaf_rn(v, S, 12582912.0f)) - 0x4B400000;
+}
+
+// Direct flush of one lane's closed xc/yc run (divergent: only lanes whose
+// guide cell changed mid-chunk come here).
+__device__ __forceinline__ void grid_flush(int key, const float (&v)[8], int c, int jy, int ds,
+                                           float S, int* E_xc, int* E_yc) {
+  const int jx = key >> 8, jc = key & 0xff;
+  int* xc = E_xc + c * ds * ds + jx * ds + jc;
+  atomicAdd(xc, to_fixed(v[0], S)); atomicAdd(xc + ds, to_fixed(v[1], S));
+  atomicAdd(xc + 1, to_fixed(v[2], S)); atomicAdd(xc + ds + 1, to_fixed(v[3], S));
+  int* yc = E_yc + c * ds * ds + jy * ds + jc;
+  atomicAdd(yc, to_fixed(v[4], S)); atomicAdd(yc + ds, to_fixed(v[5], S));
+  atomicAdd(yc + 1, to_fixed(v[6], S)); atomicAdd(yc + ds + 1, to_fixed(v[7], S));
+}
+
+// Warp-uniform loop over the distinct keys held by active lanes: each round
+// sums the matching lanes' values with full-mask REDUX and one lane issues the
+// atomics through `emit(key, sums)`.
+template <int V, typename F>
+__device__ __forceinline__ void warp_key_flush(bool active, int key, const float (&v)[V], float S,
+                                               F emit) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  unsigned todo = __ballot_sync(full, active);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    const int k = __shfl_sync(full, key, src);
+    const bool m = active && key == k;
+    int sum[V];
 #pragma unroll
-    for (int c = 0; c < C; ++c) R.v[0][c] = R.v[1][c] = R.v[2][c] = R.v[3][c] = 0.f;
-  }
-  const float w00 = (1.f - a) * (1.f - b), w10 = a * (1.f - b), w01 = (1.f - a) * b, w11 = a * b;
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    R.v[0][c] = __fmaf_rn(g[c], w00, R.v[0][c]);
-    R.v[1][c] = __fmaf_rn(g[c], w10, R.v[1][c]);
-    R.v[2][c] = __fmaf_rn(g[c], w01, R.v[2][c]);
-    R.v[3][c] = __fmaf_rn(g[c], w11, R.v[3][c]);
+    for (int i = 0; i < V; ++i) sum[i] = __reduce_add_sync(full, m ? to_fixed(v[i], S) : 0);
+    if (lane == src) emit(k, sum);
+    todo &= ~__ballot_sync(full, m);
   }
 }
 
-__global__ void __launch_bounds__(kBwdThreads, 1) fused_bwd_kernel(BwdParams p) {
-  extern __shared__ __align__(16) float sm[];
-  const VtxLayout& L = p.L;
-  float* V = sm;             // vertex tables
-  float* Es = sm + L.total;  // accumulators
-  const int dt = L.dt, ds = L.ds;
+// Merged grid coefficients of channel c at (row jy/ey, x-cell jx, guide cell jc).
+__device__ __forceinline__ float4 bgrid_entry(const float* sm, const TableLayout& L, int c, int jx,
+                                              int jc, int jy, float ey) {
+  const int ds = L.ds;
+  const float4 x = reinterpret_cast<const float4*>(sm + L.xc_off)[(c * (ds - 1) + jx) * (ds - 1) + jc];
+  const float* Y = sm + L.gyc_off + c * ds * ds;
+  const float y00 = Y[jy * ds + jc], y01 = Y[jy * ds + jc + 1];
+  const float y10 = Y[(jy + 1) * ds + jc], y11 = Y[(jy + 1) * ds + jc + 1];
+  const float q0 = __fmaf_rn(ey, y10 - y00, y00), q1 = __fmaf_rn(ey, y11 - y01, y01);
+  const float* X = sm + L.gxy_off;
+  const float v00 = X[(jx * ds + jy) * 3 + c], v01 = X[(jx * ds + jy + 1) * 3 + c];
+  const float v10 = X[((jx + 1) * ds + jy) * 3 + c], v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
+  const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
+  return make_float4(x.x + q0 + r0, x.y + (r1 - r0), x.z + (q1 - q0), x.w);
+}
+
+struct BChunk {
+  float r[kBPx], g[kBPx], b[kBPx], y0[kBPx], y1[kBPx], y2[kBPx];
+};
+
+__device__ __forceinline__ void bload4(const float* p, float* v, int x, int w, bool vec) {
+  if (vec && x + 4 <= w) {
+    const float4 t = __ldcs(reinterpret_cast<const float4*>(p + x));
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(p + min(x + u, w - 1));
+  }
+}
+
+__device__ __forceinline__ void bload_chunk(const float* X, const float* GY, long long pl, int y,
+                                            int x0, int w, int lane, bool vec, BChunk& c) {
+  const long long ro = (long long)y * w;
+  const int x = x0 + 4 * lane;
+  bload4(X + ro, c.r, x, w, vec);
+  bload4(X + pl + ro, c.g, x, w, vec);
+  bload4(X + 2 * pl + ro, c.b, x, w, vec);
+  bload4(GY + ro, c.y0, x, w, vec);
+  bload4(GY + pl + ro, c.y1, x, w, vec);
+  bload4(GY + 2 * pl + ro, c.y2, x, w, vec);
+}
+
+template <int DT, int DS>
+__global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams p) {
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bar_storage;
+  const int dt = DT ? DT : p.L.dt;
+  const int ds = DS ? DS : p.L.ds;
+  const TableLayout L = TableLayout::make(dt, ds);
+  const AccLayout A = AccLayout::make(dt, ds);
+  const uint32_t bar = bsmem_addr(&bar_storage);
+  const uint32_t sbase = bsmem_addr(smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned full = 0xffffffffu;
+
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t table_bytes = (uint32_t)L.staged_bytes();
+  const int nent = (ds - 1) * 3 * (ds - 1);
+  float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
+  float* Es = reinterpret_cast<float*>(slots + 2 * nent);  // A.total floats
   const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
   const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
-  const long long c_begin = (long long)blockIdx.x * p.total / gridDim.x;
-  const long long c_end = (long long)(blockIdx.x + 1) * p.total / gridDim.x;
-  __shared__ float gs[3];
-  const int pa[3] = {0, 0, 1}, pb[3] = {1, 2, 2};
+  const uint32_t cst48 = (uint32_t)L.cst * 48u;
+  const uint32_t pair_bytes = (uint32_t)(dt - 1) * cst48;
+  const uint32_t cst3 = (uint32_t)L.cst * 3u;
+  const uint32_t lutK = sbase + (uint32_t)L.lut_off * 4u - kMagic * (cst48 + 48u);
+  const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;
+  const uint32_t jx_bytes = 3u * chan_bytes;
+  const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
+  const uint32_t slotK0 = bsmem_addr(slots) - kMagic * 16u;
+  int* Ei = reinterpret_cast<int*>(Es);
+  int* E_lut = Ei + A.lut_off;
+  int* E_xy = Ei + A.grid_off;
+  int* E_xc = E_xy + 3 * ds * ds;
+  int* E_yc = E_xc + 3 * ds * ds;
 
-  long long c = c_begin;
-  while (c < c_end) {
-    const int b = (int)(c / p.per_img);
-    const long long phase_end = min(c_end, (long long)(b + 1) * p.per_img);
+  const long long rows_total = (long long)p.batch * p.h;
+  const long long r_begin = (long long)blockIdx.x * rows_total / gridDim.x;
+  const long long r_end = (long long)(blockIdx.x + 1) * rows_total / gridDim.x;
+  const long long pl = (long long)p.h * p.w;
+  const bool vec = ((p.w & 3) == 0) &&
+                   (((uintptr_t)p.rgb | (uintptr_t)p.gy | (uintptr_t)p.gx) & 15) == 0;
+  const int cpr = (p.w + kBChunk - 1) / kBChunk;
+  uint32_t phase = 0;
+
+  long long r = r_begin;
+  while (r < r_end) {
+    const int b = (int)(r / p.h);
+    const int y_first = (int)(r - (long long)b * p.h);
+    const int y_last = (int)(min(r_end, (long long)(b + 1) * p.h) - 1 - (long long)b * p.h);
+    const float* tb = p.tables + (long long)b * L.total_floats;
     __syncthreads();
-    const float4* src = reinterpret_cast<const float4*>(p.vtx + (long long)b * L.total);
-    for (int i = threadIdx.x; i < L.total / 4; i += blockDim.x) {
-      reinterpret_cast<float4*>(V)[i] = __ldg(src + i);
-      reinterpret_cast<float4*>(Es)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    if (threadIdx.x < 3) gs[threadIdx.x] = 0.f;
-    __syncthreads();
-
-    const long long plane = (long long)p.h * p.w;
-    const float* X = p.rgb + (long long)b * 3 * plane;
-    const float* GY = p.gy + (long long)b * 3 * plane;
-    float* GX = p.gx ? p.gx + (long long)b * 3 * plane : nullptr;
-    float gsum_l[3] = {0.f, 0.f, 0.f};
-
-    for (long long t = c + threadIdx.x; t < phase_end; t += blockDim.x) {
-      const long long rem = t - (long long)b * p.per_img;
-      const int y = (int)(rem / p.rpr);
-      const int x0 = (int)(rem - (long long)y * p.rpr) * kRun;
-      const SpatialBr rb = p.row[y];
-      const int jy = rb.i;
-      const float ey = rb.d;
-      RunAcc<3> Rl[3], Rxy;
-      RunAcc<1> Rxc[3], Ryc[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        Rl[q].key = -1;
-        Rxc[q].key = -1;
-        Ryc[q].key = -1;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(table_bytes)
+                   : "memory");
+      for (uint32_t off = 0; off < table_bytes; off += 32768u) {
+        const uint32_t n = min(32768u, table_bytes - off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                sbase + off),
+            "l"(reinterpret_cast<const char*>(tb) + off), "r"(n), "r"(bar)
+            : "memory");
       }
-      Rxy.key = -1;
-      for (int u = 0; u < kRun; ++u) {
-        const int x = x0 + u;
-        if (x >= p.w) break;
-        const long long o = (long long)y * p.w + x;
-        float Xv[3], g[3], q[3];
-        int it[3], is[3];
-        float et[3], es[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          Xv[ch] = X[ch * plane + o];
-          g[ch] = GY[ch * plane + o];
-          gsum_l[ch] += g[ch];
-          q[ch] = clamp01(Xv[ch]);
-          color_bracket(q[ch], tdm1, tdm2, it[ch], et[ch]);
-          color_bracket(q[ch], sdm1, sdm2, is[ch], es[ch]);
+    }
+    for (int i = threadIdx.x; i < A.total; i += blockDim.x) Ei[i] = 0;
+    const float gm = p.gmax[b];
+    const float S = gm > 0.f ? kFixedOne / gm : 1.0f;  // fixed-point scale of this image
+    const float invS = 1.0f / S;
+    float* Eg = p.E + (long long)b * A.total;
+    int px_since_flush = 0;
+    const float* X = p.rgb + (long long)b * 3 * pl;
+    const float* GY = p.gy + (long long)b * 3 * pl;
+    float* GX = p.gx ? p.gx + (long long)b * 3 * pl : nullptr;
+    const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
+                          (uint32_t)(L.lut2_off / 4) - kMagic * (cst3 + 3u);
+    BChunk cur;
+    int cur_y = y_first, cur_k = warp;
+    if (cur_k < cpr) bload_chunk(X, GY, pl, cur_y, cur_k * kBChunk, p.w, lane, vec, cur);
+    asm volatile(
+        "{\n.reg .pred p;\nWAITB_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAITB_%=;\n}\n" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+    phase ^= 1u;
+    {
+      float ey;
+      const int jy = (int)(row_bracket(p.y0 + y_first, p.rcp_h, sdm1, sdm2, ey) - kMagic);
+      for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
+        const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
+        slots[e] = bgrid_entry(smem, L, ch, jx, jc, jy, ey);
+      }
+    }
+    __syncthreads();
+    float gsum0 = 0.f, gsum1 = 0.f, gsum2 = 0.f;
+
+    for (int y = y_first; y <= y_last; ++y) {
+      const int buf = (y - y_first) & 1;
+      float ey;
+      const int jy = (int)(row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey) - kMagic);
+      const uint32_t slotK = slotK0 + (uint32_t)buf * slot_row_bytes;
+      for (; cur_y == y && cur_k < cpr;) {
+        BChunk nxt;
+        int nxt_y = cur_y, nxt_k = cur_k + kBwdWarps;
+        if (nxt_k >= cpr) {
+          nxt_k = warp;
+          ++nxt_y;
         }
-        float gxa[3] = {0.f, 0.f, 0.f}, gxs[3] = {0.f, 0.f, 0.f};
+        if (nxt_y <= y_last && nxt_k < cpr)
+          bload_chunk(X, GY, pl, nxt_y, nxt_k * kBChunk, p.w, lane, vec, nxt);
+        const int xl = cur_k * kBChunk + 4 * lane;
+        float oxr[kBPx], oxg[kBPx], oxb[kBPx];
+        // xy accumulators of this lane for the x-cell of its first pixel
+        float exy = 0.f;
+        const int jx_first = (int)(col_bracket(min(xl, p.w - 1), p.rcp_w, sdm1, sdm2, exy) - kMagic);
+        float axy[12];
 #pragma unroll
-        for (int pr = 0; pr < 3; ++pr) {
-          const int A = pa[pr], Bc = pb[pr];
-          const int ia = it[A], ib = it[Bc];
-          const float da = et[A], db = et[Bc];
-          const float4* T4 = reinterpret_cast<const float4*>(V + L.lut_off) + pr * dt * dt;
-          const float4 v00 = T4[ia * dt + ib], v10 = T4[(ia + 1) * dt + ib];
-          const float4 v01 = T4[ia * dt + ib + 1], v11 = T4[(ia + 1) * dt + ib + 1];
-          // sum_c g_c * dv_c/da and dv_c/db
-          const float d0a = (1.f - db) * (v10.x - v00.x) + db * (v11.x - v01.x);
-          const float d1a = (1.f - db) * (v10.y - v00.y) + db * (v11.y - v01.y);
-          const float d2a = (1.f - db) * (v10.z - v00.z) + db * (v11.z - v01.z);
-          const float d0b = (1.f - da) * (v01.x - v00.x) + da * (v11.x - v10.x);
-          const float d1b = (1.f - da) * (v01.y - v00.y) + da * (v11.y - v10.y);
-          const float d2b = (1.f - da) * (v01.z - v00.z) + da * (v11.z - v10.z);
-          gxa[A] += g[0] * d0a + g[1] * d1a + g[2] * d2a;
-          gxa[Bc] += g[0] * d0b + g[1] * d1b + g[2] * d2b;
-          run_add<3>(Rl[pr], (ia << 16) | ib, Es + L.lut_off + pr * dt * dt * 4, dt, g, da, db);
-        }
-        const SpatialBr cb = p.col[x];
-        const int jx = cb.i;
-        const float ex = cb.d;
-        run_add<3>(Rxy, (jx << 16) | jy, Es + L.xy_off, ds, g, ex, ey);
+        for (int i = 0; i < 12; ++i) axy[i] = 0.f;
+        int run_key[3] = {-1, -1, -1};  // open xc/yc run per channel
+        float run[3][8];
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const int jc = is[ch];
-          const float ec = es[ch];
-          const float* Pxc = V + L.xc_off + ch * ds * ds;
-          const float* Pyc = V + L.yc_off + ch * ds * ds;
-          const float x00 = Pxc[jx * ds + jc], x10 = Pxc[(jx + 1) * ds + jc];
-          const float x01 = Pxc[jx * ds + jc + 1], x11 = Pxc[(jx + 1) * ds + jc + 1];
-          const float y00 = Pyc[jy * ds + jc], y10 = Pyc[(jy + 1) * ds + jc];
-          const float y01 = Pyc[jy * ds + jc + 1], y11 = Pyc[(jy + 1) * ds + jc + 1];
-          gxs[ch] += g[ch] * ((1.f - ex) * (x01 - x00) + ex * (x11 - x10) +
-                              (1.f - ey) * (y01 - y00) + ey * (y11 - y10));
-          const float gc[1] = {g[ch]};
-          run_add<1>(Rxc[ch], (jx << 16) | jc, Es + L.xc_off + ch * ds * ds, ds, gc, ex, ec);
-          run_add<1>(Ryc[ch], (jy << 16) | jc, Es + L.yc_off + ch * ds * ds, ds, gc, ey, ec);
-        }
-        if (GX) {
+        for (int u = 0; u < kBPx; ++u) {
+          const bool valid = xl + u < p.w;
+          const float g0 = valid ? cur.y0[u] : 0.f, g1 = valid ? cur.y1[u] : 0.f,
+                      g2 = valid ? cur.y2[u] : 0.f;
+          gsum0 += g0;
+          gsum1 += g1;
+          gsum2 += g2;
+          const float Xr = cur.r[u], Xg = cur.g[u], Xb = cur.b[u];
+          const float qr = __saturatef(Xr), qg = __saturatef(Xg), qb = __saturatef(Xb);
+          float dr, dg, db;
+          const uint32_t br = bbracket(qr, tdm1, tdm2, dr);
+          const uint32_t bg = bbracket(qg, tdm1, tdm2, dg);
+          const uint32_t bb = bbracket(qb, tdm1, tdm2, db);
+          float ex;
+          const int jx = (int)(col_bracket(min(xl + u, p.w - 1), p.rcp_w, sdm1, sdm2, ex) - kMagic);
+          float er, eg, eb;
+          const uint32_t sr = bbracket(qr, sdm1, sdm2, er);
+          const uint32_t sg = bbracket(qg, sdm1, sdm2, eg);
+          const uint32_t sb = bbracket(qb, sdm1, sdm2, eb);
+          // ---- input gradient from the coefficient cells ----
+          float gar = 0.f, gag = 0.f, gab = 0.f;
+          {
+            const uint32_t a = br * cst48 + lutK + bg * 48u;  // rg
+            const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
+            // B: c0.w c1.x c1.y  C: c1.z c1.w c2.x  D: c2.y c2.z c2.w
+            gar += g0 * __fmaf_rn(c2.y, dg, c0.w) + g1 * __fmaf_rn(c2.z, dg, c1.x) + g2 * __fmaf_rn(c2.w, dg, c1.y);
+            gag += g0 * __fmaf_rn(c2.y, dr, c1.z) + g1 * __fmaf_rn(c2.z, dr, c1.w) + g2 * __fmaf_rn(c2.w, dr, c2.x);
+          }
+          {
+            const uint32_t a = br * cst48 + lutK + bb * 48u + pair_bytes;  // rb
+            const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
+            gar += g0 * __fmaf_rn(c2.y, db, c0.w) + g1 * __fmaf_rn(c2.z, db, c1.x) + g2 * __fmaf_rn(c2.w, db, c1.y);
+            gab += g0 * __fmaf_rn(c2.y, dr, c1.z) + g1 * __fmaf_rn(c2.z, dr, c1.w) + g2 * __fmaf_rn(c2.w, dr, c2.x);
+          }
+          {
+            const int ti = (int)(bg * cst3 + bb * 3u + texK);  // gb via the texture path
+            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
+                         c2 = tex1Dfetch<float4>(p.tex, ti + 2);
+            gag += g0 * __fmaf_rn(c2.y, db, c0.w) + g1 * __fmaf_rn(c2.z, db, c1.x) + g2 * __fmaf_rn(c2.w, db, c1.y);
+            gab += g0 * __fmaf_rn(c2.y, dg, c1.z) + g1 * __fmaf_rn(c2.z, dg, c1.w) + g2 * __fmaf_rn(c2.w, dg, c2.x);
+          }
+          const uint32_t sa = slotK + (uint32_t)jx * jx_bytes;
+          const float4 s0 = blds4(sa + sr * 16u);
+          const float4 s1 = blds4(sa + chan_bytes + sg * 16u);
+          const float4 s2 = blds4(sa + 2u * chan_bytes + sb * 16u);
+          const float gsr = g0 * __fmaf_rn(s0.w, ex, s0.z);
+          const float gsg = g1 * __fmaf_rn(s1.w, ex, s1.z);
+          const float gsb = g2 * __fmaf_rn(s2.w, ex, s2.z);
+          oxr[u] = (Xr < 0.f || Xr > 1.f) ? 0.f : __fmaf_rn(gar, tdm1, gsr * sdm1);
+          oxg[u] = (Xg < 0.f || Xg > 1.f) ? 0.f : __fmaf_rn(gag, tdm1, gsg * sdm1);
+          oxb[u] = (Xb < 0.f || Xb > 1.f) ? 0.f : __fmaf_rn(gab, tdm1, gsb * sdm1);
+
+          // ---- scatter: LUT pairs, one fixed-point atomic per value ----
+          if (valid) {
+            const int ir = (int)(br - kMagic), ig = (int)(bg - kMagic), ib = (int)(bb - kMagic);
 #pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            const float m = (Xv[ch] < 0.f || Xv[ch] > 1.f) ? 0.f : 1.f;  // strict clamp
-            GX[ch * plane + o] = m * (gxa[ch] * tdm1 + gxs[ch] * sdm1);
+            for (int pr = 0; pr < 3; ++pr) {
+              const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
+              const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
+              const float w00 = (1.f - da) * (1.f - dbb), w10 = da * (1.f - dbb);
+              const float w01 = (1.f - da) * dbb, w11 = da * dbb;
+              int* e = E_lut + (pr * dt * dt + ia * dt + ibb) * 3;
+              int* e10 = e + dt * 3;
+              atomicAdd(e, to_fixed(g0 * w00, S)); atomicAdd(e + 1, to_fixed(g1 * w00, S));
+              atomicAdd(e + 2, to_fixed(g2 * w00, S));
+              atomicAdd(e10, to_fixed(g0 * w10, S)); atomicAdd(e10 + 1, to_fixed(g1 * w10, S));
+              atomicAdd(e10 + 2, to_fixed(g2 * w10, S));
+              atomicAdd(e + 3, to_fixed(g0 * w01, S)); atomicAdd(e + 4, to_fixed(g1 * w01, S));
+              atomicAdd(e + 5, to_fixed(g2 * w01, S));
+              atomicAdd(e10 + 3, to_fixed(g0 * w11, S)); atomicAdd(e10 + 4, to_fixed(g1 * w11, S));
+              atomicAdd(e10 + 5, to_fixed(g2 * w11, S));
+            }
+          }
+          // ---- grids: xc + yc runs per channel (key = guide cell; x-cell checked) ----
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float gc = c == 0 ? g0 : (c == 1 ? g1 : g2);
+            const int jc = (int)((c == 0 ? sr : (c == 1 ? sg : sb)) - kMagic);
+            const float ec = c == 0 ? er : (c == 1 ? eg : eb);
+            const int key = valid ? (jx << 8) | jc : -1;
+            if (key != run_key[c]) {
+              if (run_key[c] >= 0) grid_flush(run_key[c], run[c], c, jy, ds, S, E_xc, E_yc);
+              run_key[c] = key;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) run[c][i] = 0.f;
+            }
+            if (valid) {
+              run[c][0] += gc * (1.f - ex) * (1.f - ec);
+              run[c][1] += gc * ex * (1.f - ec);
+              run[c][2] += gc * (1.f - ex) * ec;
+              run[c][3] += gc * ex * ec;
+              run[c][4] += gc * (1.f - ey) * (1.f - ec);
+              run[c][5] += gc * ey * (1.f - ec);
+              run[c][6] += gc * (1.f - ey) * ec;
+              run[c][7] += gc * ey * ec;
+            }
+          }
+          // ---- xy: summed in registers for the lane's first x-cell ----
+          {
+            const float w00 = (1.f - ex) * (1.f - ey), w10 = ex * (1.f - ey);
+            const float w01 = (1.f - ex) * ey, w11 = ex * ey;
+            if (jx == jx_first) {
+              axy[0] += g0 * w00; axy[1] += g1 * w00; axy[2] += g2 * w00;
+              axy[3] += g0 * w10; axy[4] += g1 * w10; axy[5] += g2 * w10;
+              axy[6] += g0 * w01; axy[7] += g1 * w01; axy[8] += g2 * w01;
+              axy[9] += g0 * w11; axy[10] += g1 * w11; axy[11] += g2 * w11;
+            } else if (valid) {  // the lane's pixels straddle an x-cell boundary
+              const float gg[3] = {g0, g1, g2};
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                int* e = E_xy + c * ds * ds + jx * ds + jy;
+                atomicAdd(e, to_fixed(gg[c] * w00, S)); atomicAdd(e + ds, to_fixed(gg[c] * w10, S));
+                atomicAdd(e + 1, to_fixed(gg[c] * w01, S)); atomicAdd(e + ds + 1, to_fixed(gg[c] * w11, S));
+              }
+            }
           }
         }
-      }
+        // ---- end of chunk: the open grid runs and the xy sums, by distinct key ----
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        flush<3>(Rl[q], Es + L.lut_off + q * dt * dt * 4, dt);
-        flush<1>(Rxc[q], Es + L.xc_off + q * ds * ds, ds);
-        flush<1>(Ryc[q], Es + L.yc_off + q * ds * ds, ds);
+        for (int c = 0; c < 3; ++c) {
+          warp_key_flush<8>(run_key[c] >= 0, run_key[c], run[c], S, [&](int key, const int* sum) {
+            const int jx = key >> 8, jc = key & 0xff;
+            int* xc = E_xc + c * ds * ds + jx * ds + jc;
+            atomicAdd(xc, sum[0]); atomicAdd(xc + ds, sum[1]);
+            atomicAdd(xc + 1, sum[2]); atomicAdd(xc + ds + 1, sum[3]);
+            int* yc = E_yc + c * ds * ds + jy * ds + jc;
+            atomicAdd(yc, sum[4]); atomicAdd(yc + ds, sum[5]);
+            atomicAdd(yc + 1, sum[6]); atomicAdd(yc + ds + 1, sum[7]);
+          });
+          run_key[c] = -1;
+        }
+        warp_key_flush<12>(xl < p.w, jx_first, axy, S, [&](int key, const int* sum) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            int* e = E_xy + c * ds * ds + key * ds + jy;
+            atomicAdd(e, sum[c]); atomicAdd(e + ds, sum[3 + c]);
+            atomicAdd(e + 1, sum[6 + c]); atomicAdd(e + ds + 1, sum[9 + c]);
+          }
+        });
+        if (GX) {
+          const long long ro = (long long)cur_y * p.w;
+          if (vec && xl + 4 <= p.w) {
+            __stcs(reinterpret_cast<float4*>(GX + ro + xl), make_float4(oxr[0], oxr[1], oxr[2], oxr[3]));
+            __stcs(reinterpret_cast<float4*>(GX + pl + ro + xl), make_float4(oxg[0], oxg[1], oxg[2], oxg[3]));
+            __stcs(reinterpret_cast<float4*>(GX + 2 * pl + ro + xl), make_float4(oxb[0], oxb[1], oxb[2], oxb[3]));
+          } else {
+#pragma unroll
+            for (int u = 0; u < kBPx; ++u)
+              if (xl + u < p.w) {
+                GX[ro + xl + u] = oxr[u];
+                GX[pl + ro + xl + u] = oxg[u];
+                GX[2 * pl + ro + xl + u] = oxb[u];
+              }
+          }
+        }
+        cur = nxt;
+        cur_y = nxt_y;
+        cur_k = nxt_k;
       }
-      flush<3>(Rxy, Es + L.xy_off, ds);
+      if (y < y_last) {
+        float ey1;
+        const int jy1 = (int)(row_bracket(p.y0 + y + 1, p.rcp_h, sdm1, sdm2, ey1) - kMagic);
+        float4* S = slots + (buf ^ 1) * nent;
+        for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+          const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
+          const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
+          S[e] = bgrid_entry(smem, L, ch, jx, jc, jy1, ey1);
+        }
+      }
+      __syncthreads();
+      px_since_flush += p.w;
+      if (px_since_flush >= kFlushPx && y < y_last) {  // keep shared partials < 2^31
+        for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
+          const int v = Ei[i];
+          if (v != 0) {
+            atomicAdd(Eg + i, (float)v * invS);
+            Ei[i] = 0;
+          }
+        }
+        px_since_flush = 0;
+        __syncthreads();
+      }
     }
-    // per-image gY sums
+    // ---- per-image gY sums and flush of the shared accumulators ----
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float v = gsum_l[ch];
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if ((threadIdx.x & 31) == 0) atomicAdd(&gs[ch], v);
+    for (int off = 16; off > 0; off >>= 1) {
+      gsum0 += __shfl_xor_sync(full, gsum0, off);
+      gsum1 += __shfl_xor_sync(full, gsum1, off);
+      gsum2 += __shfl_xor_sync(full, gsum2, off);
+    }
+    if (lane == 0) {
+      atomicAdd(Eg + A.gsum_off + 0, gsum0);
+      atomicAdd(Eg + A.gsum_off + 1, gsum1);
+      atomicAdd(Eg + A.gsum_off + 2, gsum2);
     }
     __syncthreads();
-    float* Eg = p.E + (long long)b * L.total;
-    for (int i = threadIdx.x; i < L.total; i += blockDim.x) {
-      const float v = Es[i];
-      if (v != 0.f) atomicAdd(Eg + i, v);
+    for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
+      const int v = Ei[i];
+      if (v != 0) atomicAdd(Eg + i, (float)v * invS);
     }
-    if (threadIdx.x < 3) atomicAdd(p.gsum + b * 4 + threadIdx.x, gs[threadIdx.x]);
-    c = phase_end;
+    r += y_last - y_first + 1;
   }
 }
 
 // Converts the unweighted accumulators into parameter gradients.  grid.y = image.
 __global__ void finalize_kernel(const float* __restrict__ lp, const float* __restrict__ lw,
                                 const float* __restrict__ gp, const float* __restrict__ gw, int k,
-                                VtxLayout L, const float* __restrict__ E,
-                                const float* __restrict__ gsum, float* dlp, float* dlw,
+                                AccLayout A, const float* __restrict__ E, float* dlp, float* dlw,
                                 float* dlb, float* dgp, float* dgw, float* dgb) {
   const long long b = blockIdx.y;
-  const int dt = L.dt, ds = L.ds;
-  const float* Eb = E + b * (long long)L.total;
+  const int dt = A.dt, ds = A.ds;
+  const float* Eb = E + b * (long long)A.total;
   const int task = blockIdx.x;  // 0..8: LUT planes (c,p); 9..: grid planes (kk, q)
   __shared__ double red[32];
   double acc = 0.0;
@@ -339,7 +529,7 @@ __global__ void finalize_kernel(const float* __restrict__ lp, const float* __res
     const float w = lw[b * 9 + task];
     float* D = dlp + (b * 9 + task) * (long long)dt * dt;
     for (int ij = threadIdx.x; ij < dt * dt; ij += blockDim.x) {
-      const float e = Eb[L.lut_off + (pr * dt * dt + ij) * 4 + c];
+      const float e = Eb[A.lut_off + (pr * dt * dt + ij) * 3 + c];
       D[ij] = w * e;
       acc += (double)T[ij] * (double)e;
     }
@@ -350,9 +540,7 @@ __global__ void finalize_kernel(const float* __restrict__ lp, const float* __res
     const float w = gw[b * k * 3 + kq];
     float* D = dgp + (b * k * 3 + kq) * (long long)ds * ds;
     for (int ab = threadIdx.x; ab < ds * ds; ab += blockDim.x) {
-      float e;
-      if (q == 0) e = Eb[L.xy_off + ab * 4 + c];
-      else e = Eb[(q == 1 ? L.xc_off : L.yc_off) + c * ds * ds + ab];
+      const float e = Eb[A.grid_off + (q * 3 + c) * ds * ds + ab];
       D[ab] = w * e;
       acc += (double)Gp[ab] * (double)e;
     }
@@ -365,14 +553,40 @@ __global__ void finalize_kernel(const float* __restrict__ lp, const float* __res
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
     if (task < 9) {
       dlw[b * 9 + task] = (float)s;
-      if (task % 3 == 0) dlb[b * 3 + task / 3] = gsum[b * 4 + task / 3];
+      if (task % 3 == 0) dlb[b * 3 + task / 3] = Eb[A.gsum_off + task / 3];
     } else {
       const int kq = task - 9;
       dgw[b * k * 3 + kq] = (float)s;
-      if (kq % 3 == 0) dgb[b * k + kq / 3] = gsum[b * 4 + (kq / 3) % 3];
+      if (kq % 3 == 0) dgb[b * k + kq / 3] = Eb[A.gsum_off + (kq / 3) % 3];
     }
   }
 }
+
+// max|gY| per image (positive floats order like their bit patterns).
+__global__ void absmax_kernel(const float* __restrict__ gy, long long per_img, float* gmax) {
+  const long long b = blockIdx.y;
+  const float* base = gy + b * per_img;
+  float m = 0.f;
+  const bool vec = (per_img % 4 == 0) && ((reinterpret_cast<uintptr_t>(gy) & 15) == 0);
+  if (vec) {
+    const float4* g = reinterpret_cast<const float4*>(base);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_img / 4;
+         i += (long long)gridDim.x * blockDim.x) {
+      const float4 v = __ldcs(g + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  } else {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_img;
+         i += (long long)gridDim.x * blockDim.x)
+      m = fmaxf(m, fabsf(base[i]));
+  }
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(gmax + b), __float_as_int(m));
+}
+
+cudaError_t fwd_texture(const float* tables, int batch, const TableLayout& L, cudaStream_t st,
+                        cudaTextureObject_t* tex, int* tex_base);
+cudaError_t fwd_texture_used(cudaTextureObject_t tex, cudaStream_t st);
 
 cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w, int y0,
                              int h_total, const float* lp, const float* lw, int dt,
@@ -380,51 +594,67 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
                              float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
                              float* dgb, void* ws, size_t ws_bytes, cudaStream_t st) {
   (void)ws_bytes;
-  const VtxLayout L = VtxLayout::make(dt, ds);
-  const size_t smem = (size_t)L.total * 4 * 2;
+  const TableLayout L = TableLayout::make(dt, ds);
+  const AccLayout A = AccLayout::make(dt, ds);
+  const int nent = (ds - 1) * 3 * (ds - 1);
+  const size_t smem = (size_t)L.staged_bytes() + 2 * (size_t)nent * 16 + (size_t)A.total * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
-  BwdWs W = carve(ws, batch, h, w, L);
+  char* wp = (char*)ws;
+  float* tables = (float*)wp;
+  wp += rup((size_t)batch * L.bytes());
+  float* E = (float*)wp;
+  wp += rup((size_t)batch * A.total * 4);
+  float* zb = (float*)wp;  // zero biases (biases do not enter any derivative)
+  wp += rup((size_t)batch * (3 + k) * 4);
+  float* gmax = (float*)wp;
   cudaError_t e;
+  if ((e = cudaMemsetAsync(zb, 0, (size_t)batch * (3 + k) * 4, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(gmax, 0, (size_t)batch * 4, st)) != cudaSuccess) return e;
   {
-    const int items = 3 * dt * dt + 7 * ds * ds;
-    dim3 grid((items + 255) / 256, batch);
-    pack_vertex_kernel<<<grid, 256, 0, st>>>(lp, lw, gp, gw, k, L, W.vtx);
+    const long long per = 3LL * h * w;
+    long long blocks = (per / 4 + 255) / 256;
+    if (blocks > 512) blocks = 512;
+    if (blocks < 1) blocks = 1;
+    dim3 g((unsigned)blocks, batch);
+    absmax_kernel<<<g, 256, 0, st>>>(gy, per, gmax);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  if ((e = cudaMemsetAsync(W.E, 0, (size_t)batch * L.total * 4, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(W.gsum, 0, (size_t)batch * 16, st)) != cudaSuccess) return e;
-  if ((e = launch_spatial(w, h, y0, h_total, ds, W.col, W.row, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(E, 0, (size_t)batch * A.total * 4, st)) != cudaSuccess) return e;
+  if ((e = launch_pack(lp, nullptr, nullptr, nullptr, 0, lw, zb, gp, gw, zb + 3 * batch, k, L, batch,
+                       tables, st)) != cudaSuccess)
+    return e;
   BwdParams p;
   p.rgb = rgb;
   p.gy = gy;
   p.gx = gx;
+  p.batch = batch;
   p.h = h;
   p.w = w;
+  p.y0 = y0;
+  p.tables = tables;
   p.L = L;
-  p.vtx = W.vtx;
-  p.E = W.E;
-  p.gsum = W.gsum;
-  p.col = W.col;
-  p.row = W.row;
-  p.rpr = (w + kRun - 1) / kRun;
-  p.per_img = (long long)h * p.rpr;
-  p.total = (long long)batch * p.per_img;
-  if (p.total > 0) {
+  p.A = A;
+  p.rcp_w = 1.0 / (double)(w - 1);
+  p.rcp_h = 1.0 / (double)(h_total - 1);
+  p.E = E;
+  p.gmax = gmax;
+  if ((e = fwd_texture(tables, batch, L, st, &p.tex, &p.tex_base)) != cudaSuccess) return e;
+  const long long rows = (long long)batch * h;
+  if (rows > 0 && w > 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    long long grid = sms;
-    if (grid > (p.total + kBwdThreads - 1) / kBwdThreads) grid = (p.total + kBwdThreads - 1) / kBwdThreads;
-    if (grid < 1) grid = 1;
-    if ((e = cudaFuncSetAttribute(fused_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)) != cudaSuccess)
+    long long grid = sms < rows ? sms : rows;
+    auto kern = (dt == 33 && ds == 17) ? fused_bwd_kernel<33, 17> : fused_bwd_kernel<0, 0>;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
       return e;
-    fused_bwd_kernel<<<(int)grid, kBwdThreads, smem, st>>>(p);
+    kern<<<(int)grid, kBwdWarps * 32, smem, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = fwd_texture_used(p.tex, st)) != cudaSuccess) return e;
   }
   dim3 fg(9 + 3 * k, batch);
-  finalize_kernel<<<fg, 256, 0, st>>>(lp, lw, gp, gw, k, L, W.E, W.gsum, dlp, dlw, dlb, dgp, dgw,
-                                      dgb);
+  finalize_kernel<<<fg, 256, 0, st>>>(lp, lw, gp, gw, k, A, E, dlp, dlw, dlb, dgp, dgw, dgb);
   return cudaGetLastError();
 }
 

@@ -129,6 +129,8 @@ int svdlut_pack_tables(const float* lut_planes, const float* lw, const float* lb
   if (!lut_planes || !lw || !lb || !grid_planes || !gw || !gb || !tables)
     return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
+  if (!svdlut_fast_supported(d_t, d_s))
+    return fail(SVDLUT_ERR_UNSUPPORTED, "packed tables serve the fast kernel only (d_t=%d d_s=%d)", d_t, d_s);
   const TableLayout L = TableLayout::make(d_t, d_s);
   CUDA_TRY(launch_pack(lut_planes, nullptr, nullptr, nullptr, 0, lw, lb, grid_planes, gw, gb, k, L,
                        batch, (float*)tables, (cudaStream_t)stream),
@@ -148,6 +150,8 @@ int svdlut_pack_tables_factors(const float* u, const float* s, const float* vt, 
   if (!u || !s || !vt || !lw || !lb || !grid_planes || !gw || !gb || !tables)
     return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
   if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
+  if (!svdlut_fast_supported(d_t, d_s))
+    return fail(SVDLUT_ERR_UNSUPPORTED, "packed tables serve the fast kernel only (d_t=%d d_s=%d)", d_t, d_s);
   const TableLayout L = TableLayout::make(d_t, d_s);
   CUDA_TRY(launch_pack(nullptr, u, s, vt, n_s, lw, lb, grid_planes, gw, gb, k, L, batch,
                        (float*)tables, (cudaStream_t)stream),

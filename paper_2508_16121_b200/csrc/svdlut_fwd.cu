@@ -41,6 +41,10 @@ namespace svdlut {
 #ifndef FWD_NW
 #define FWD_NW 15  // 15 x 128 px = 1920: divides 1080p / 4K / 8K rows exactly
 #endif
+#ifndef FWD_NTEX
+#define FWD_NTEX 1  // LUT pairs gathered through the texture path (gb, or rb and gb)
+#endif
+constexpr int kNTex = FWD_NTEX;
 constexpr int kPx = FWD_PX;
 constexpr int kFwdWarps = FWD_NW;
 constexpr int kChunk = 32 * kPx;
@@ -232,7 +236,16 @@ __device__ __forceinline__ float4 grid_entry(const GridG& G, int ds, int c, int 
   return make_float4(x.x + q0 + r0, x.y + (r1 - r0), x.z + (q1 - q0), x.w);
 }
 
-template <int DT, int DS, bool CHECK, int PX, int NW>
+// Shared-memory image of the tables: LUT pairs [0, 3-NTEX) then the grid
+// block (xc, gxy, gyc); the remaining pairs are read through the texture.
+__host__ __device__ inline uint32_t smem_grid_off(const TableLayout& L, int ntex) {
+  return (uint32_t)(3 - ntex) * (uint32_t)L.pair_floats * 4u;
+}
+__host__ __device__ inline uint32_t smem_tables_bytes(const TableLayout& L, int ntex) {
+  return smem_grid_off(L, ntex) + (uint32_t)(L.lut2_off - L.xc_off) * 4u;
+}
+
+template <int DT, int DS, bool CHECK, int PX, int NW, int NTEX>
 __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   constexpr int CH = 32 * PX;  // pixels per warp chunk
   extern __shared__ __align__(128) float smem[];
@@ -249,7 +262,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t table_bytes = (uint32_t)L.staged_bytes();  // smem prefix (all but lut2)
+  const uint32_t lut_smem_bytes = smem_grid_off(L, NTEX);
+  const uint32_t table_bytes = smem_tables_bytes(L, NTEX);
   const int nent = (ds - 1) * 3 * (ds - 1);                  // slot entries per row
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
   // column table: t(x) = RN32(RN32(x/(W-1)) * (d_s-1)) for every column, built once
@@ -264,9 +278,10 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   }
 
   GridG G;
-  G.xc = reinterpret_cast<const float4*>(smem + L.xc_off);
-  G.gxy = smem + L.gxy_off;
-  G.gyc = smem + L.gyc_off;
+  const float* gsm = smem + lut_smem_bytes / 4 - L.xc_off;  // global offset -> smem
+  G.xc = reinterpret_cast<const float4*>(gsm + L.xc_off);
+  G.gxy = gsm + L.gxy_off;
+  G.gyc = gsm + L.gyc_off;
 
   const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
   const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
@@ -302,16 +317,20 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive_expect_tx(bar, table_bytes);
       const char* src = reinterpret_cast<const char*>(tb);
-      for (uint32_t off = 0; off < table_bytes; off += 32768u) {
-        const uint32_t n = min(32768u, table_bytes - off);
-        bulk_g2s(sbase + off, src + off, n, bar);
-      }
+      for (uint32_t off = 0; off < lut_smem_bytes; off += 32768u)  // LUT pairs kept in smem
+        bulk_g2s(sbase + off, src + off, min(32768u, lut_smem_bytes - off), bar);
+      const char* gsrc = src + (size_t)L.xc_off * 4;
+      const uint32_t gbytes = table_bytes - lut_smem_bytes;
+      for (uint32_t off = 0; off < gbytes; off += 32768u)       // grid block
+        bulk_g2s(sbase + lut_smem_bytes + off, gsrc + off, min(32768u, gbytes - off), bar);
     }
     const float* plane0 = p.rgb + (long long)b * 3 * pl;
     float* oplane0 = p.out + (long long)b * 3 * pl;
     // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
+    const uint32_t texKrb = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
+                            (uint32_t)(L.pair_off(1) / 4) - kMagicBits * (cst3 + 3u);
 
     // the first chunk's loads overlap the table copy
     const int cpr = (p.w + CH - 1) / CH;
@@ -379,21 +398,30 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         // use (software pipeline depth 1), hiding the texture latency behind
         // the shared-memory work of the previous pixel.
         float o0[PX], o1[PX], o2[PX];
-        float4 tx0, tx1, tx2;  // in-flight texture cells of the next pixel
-        float tdg, tdb;        // its deltas
+        float4 tx0, tx1, tx2;  // in-flight texture cells (pair gb) of the next pixel
+        float4 ty0, ty1, ty2;  // pair rb when it is on the texture path too
+        float tdg, tdb, tdr;   // their deltas
         {
-          const float qg = __saturatef(cur.g[0]), qb = __saturatef(cur.b[0]);
+          const float qr = __saturatef(cur.r[0]), qg = __saturatef(cur.g[0]), qb = __saturatef(cur.b[0]);
           const uint32_t bg = cbracket(qg, tdm1, tdm2, tdg);
           const uint32_t bb = cbracket(qb, tdm1, tdm2, tdb);
           const int ti = (int)(bg * cst3 + bb * 3u + texK);
           tx0 = tex1Dfetch<float4>(p.tex, ti);
           tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
           tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
+          if (NTEX == 2) {
+            const uint32_t br = cbracket(qr, tdm1, tdm2, tdr);
+            const int tr = (int)(br * cst3 + bb * 3u + texKrb);
+            ty0 = tex1Dfetch<float4>(p.tex, tr);
+            ty1 = tex1Dfetch<float4>(p.tex, tr + 1);
+            ty2 = tex1Dfetch<float4>(p.tex, tr + 2);
+          }
         }
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
           const float4 c0 = tx0, c1 = tx1, c2 = tx2;
-          const float dg = tdg, db = tdb;
+          const float4 e0 = ty0, e1 = ty1, e2 = ty2;
+          const float dg = tdg, db = tdb, drr = tdr;
           if (u + 1 < PX) {
             const float qg1 = __saturatef(cur.g[u + 1]), qb1 = __saturatef(cur.b[u + 1]);
             const uint32_t bg1 = cbracket(qg1, tdm1, tdm2, tdg);
@@ -402,6 +430,13 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
             tx0 = tex1Dfetch<float4>(p.tex, ti);
             tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
             tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
+            if (NTEX == 2) {
+              const uint32_t br1 = cbracket(__saturatef(cur.r[u + 1]), tdm1, tdm2, tdr);
+              const int tr = (int)(br1 * cst3 + bb1 * 3u + texKrb);
+              ty0 = tex1Dfetch<float4>(p.tex, tr);
+              ty1 = tex1Dfetch<float4>(p.tex, tr + 1);
+              ty2 = tex1Dfetch<float4>(p.tex, tr + 2);
+            }
           }
           const float qr = __saturatef(cur.r[u]), qg = __saturatef(cur.g[u]),
                       qb = __saturatef(cur.b[u]);
@@ -412,7 +447,13 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           const uint32_t ur = br * cst48 + lutK;
           float a0, a1, a2;
           lut_term<true>(ur + bg * 48u, dr, dg_, a0, a1, a2);
-          lut_term<false>(ur + bb * 48u + pair_bytes, dr, db_, a0, a1, a2);
+          if (NTEX == 1) {
+            lut_term<false>(ur + bb * 48u + pair_bytes, dr, db_, a0, a1, a2);
+          } else {
+            a0 += __fmaf_rn(db, __fmaf_rn(e2.y, drr, e1.z), __fmaf_rn(e0.w, drr, e0.x));
+            a1 += __fmaf_rn(db, __fmaf_rn(e2.z, drr, e1.w), __fmaf_rn(e1.x, drr, e0.y));
+            a2 += __fmaf_rn(db, __fmaf_rn(e2.w, drr, e2.x), __fmaf_rn(e1.y, drr, e0.z));
+          }
           a0 += __fmaf_rn(db, __fmaf_rn(c2.y, dg, c1.z), __fmaf_rn(c0.w, dg, c0.x));
           a1 += __fmaf_rn(db, __fmaf_rn(c2.z, dg, c1.w), __fmaf_rn(c1.x, dg, c0.y));
           a2 += __fmaf_rn(db, __fmaf_rn(c2.w, dg, c2.x), __fmaf_rn(c1.y, dg, c0.z));
@@ -473,7 +514,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
 size_t fwd_smem_bytes(int dt, int ds) {
   const TableLayout L = TableLayout::make(dt, ds);
   // staged tables + double-buffered per-row grid slots [jx][c][jc] (float4)
-  return (size_t)L.staged_bytes() + 2 * (size_t)(ds - 1) * 3 * (ds - 1) * 16;
+  return (size_t)smem_tables_bytes(L, kNTex) + 2 * (size_t)(ds - 1) * 3 * (ds - 1) * 16;
 }
 
 // Keep at least this much of the 256 KB L1/shared array as L1 so the
@@ -584,11 +625,27 @@ cudaError_t tex_mark_used(cudaTextureObject_t tex, cudaStream_t st) {
 }
 }  // namespace
 
+// Texture object over a batch of packed tables (also used by the backward).
+cudaError_t fwd_texture(const float* tables, int batch, const TableLayout& L, cudaStream_t st,
+                        cudaTextureObject_t* tex, int* tex_base) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int talign = 512;
+  cudaDeviceGetAttribute(&talign, cudaDevAttrTextureAlignment, dev);
+  const uintptr_t tb = reinterpret_cast<uintptr_t>(tables);
+  const uintptr_t base = tb / (uintptr_t)talign * (uintptr_t)talign;
+  const size_t bytes = (size_t)(tb - base) + (size_t)batch * L.bytes();
+  *tex_base = (int)((tb - base) / 16);
+  return tex_for(dev, reinterpret_cast<const void*>(base), bytes, st, tex);
+}
+
+cudaError_t fwd_texture_used(cudaTextureObject_t tex, cudaStream_t st) { return tex_mark_used(tex, st); }
+
 template <int DT, int DS>
 static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t smem,
                                cudaStream_t st) {
-  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps>
-                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps>;
+  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps, kNTex>
+                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps, kNTex>;
   // function attributes are set once per (instantiation, smem size); setting
   // them is not a stream operation, so graph capture does not see it
   static size_t configured[2] = {0, 0};

@@ -58,15 +58,19 @@ __device__ __forceinline__ float lut_entry(const float* __restrict__ U, const fl
 // The LUT planes come either from `lp` (B,3,3,d_t,d_t) or, when lp == NULL,
 // straight from the SVD factors (u, s, vt, n_s) — the fused prologue that
 // skips materialising the planes.
+//   blocks [0, 9)        one LUT plane (c, p) each: the plane is reconstructed
+//                        into shared memory once, then its coefficient cells
+//                        are written (channel c's 4 floats of every cell)
+//   blocks [9, gridDim)  merged grid cells / vertices and padding
 __global__ void pack_kernel(const float* __restrict__ lp, const float* __restrict__ fu,
                             const float* __restrict__ fs, const float* __restrict__ fvt, int ns,
                             const float* __restrict__ lw,
                             const float* __restrict__ lb, const float* __restrict__ gp,
                             const float* __restrict__ gw, const float* __restrict__ gb, int k,
                             TableLayout L, float* __restrict__ tables) {
+  extern __shared__ float Ts[];  // one LUT plane, d_t x d_t
   const long long b = blockIdx.y;
   const int dt = L.dt, ds = L.ds;
-  const float* P = lp ? lp + b * 9LL * dt * dt : nullptr;
   const float* W = lw + b * 9;
   const float* Bl = lb + b * 3;
   const float* G = gp + b * (long long)k * 3 * ds * ds;
@@ -74,53 +78,44 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
   const float* GB = gb + b * (long long)k;
   float* T = tables + b * (long long)L.total_floats;
 
-  const int n_lut = 3 * (dt - 1) * L.cst;  // cells incl. padding
+  if (blockIdx.x < 9) {
+    const int c = blockIdx.x / 3, p = blockIdx.x - 3 * (blockIdx.x / 3);
+    const long long cp = b * 9 + c * 3 + p;
+    for (int e = threadIdx.x; e < dt * dt; e += blockDim.x) {
+      if (lp) {
+        Ts[e] = lp[cp * dt * dt + e];
+      } else {
+        const int i = e / dt, j = e - i * dt;
+        Ts[e] = lut_entry(fu + cp * dt * ns, fs + cp * ns, fvt + cp * ns * dt, dt, ns, i, j);
+      }
+    }
+    __syncthreads();
+    const double w = (double)W[c * 3 + p];
+    float* base = T + L.pair_off(p);
+    for (int e = threadIdx.x; e < (dt - 1) * L.cst; e += blockDim.x) {
+      const int i = e / L.cst, j = e - i * L.cst;
+      Coef q = {0.f, 0.f, 0.f, 0.f};
+      if (j < dt - 1)
+        q = cell_coef(w * Ts[i * dt + j], w * Ts[(i + 1) * dt + j], w * Ts[i * dt + j + 1],
+                      w * Ts[(i + 1) * dt + j + 1]);
+      float* dst = base + e * 12;
+      dst[c] = q.a;
+      dst[3 + c] = q.b;
+      dst[6 + c] = q.c;
+      dst[9 + c] = q.d;
+    }
+    return;
+  }
+
   const int n_xc = 3 * (ds - 1) * (ds - 1);
   const int n_gxy = ds * ds;  // vertices (3 floats each)
   const int n_gyc = 3 * ds * ds;
   const int n_pad = L.lut2_off - (L.gyc_off + n_gyc);
   const int n_tail = L.total_floats - (L.lut2_off + L.pair_floats);
-  const int total = n_lut + n_xc + n_gxy + n_gyc + n_pad + n_tail;
-
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    if (e < n_lut) {
-      const int p = e / ((dt - 1) * L.cst);
-      const int rem = e - p * (dt - 1) * L.cst;
-      const int i = rem / L.cst, j = rem - i * L.cst;
-      float v[12];
-      for (int c = 0; c < 3; ++c) {
-        Coef q = {0.f, 0.f, 0.f, 0.f};
-        if (j < dt - 1) {
-          const double w = (double)W[c * 3 + p];
-          float t00, t10, t01, t11;
-          if (P) {
-            const float* pl = P + (c * 3 + p) * dt * dt;
-            t00 = pl[i * dt + j];
-            t10 = pl[(i + 1) * dt + j];
-            t01 = pl[i * dt + j + 1];
-            t11 = pl[(i + 1) * dt + j + 1];
-          } else {
-            const long long cp = b * 9 + c * 3 + p;
-            const float* U = fu + cp * dt * ns;
-            const float* S = fs + cp * ns;
-            const float* V = fvt + cp * ns * dt;
-            t00 = lut_entry(U, S, V, dt, ns, i, j);
-            t10 = lut_entry(U, S, V, dt, ns, i + 1, j);
-            t01 = lut_entry(U, S, V, dt, ns, i, j + 1);
-            t11 = lut_entry(U, S, V, dt, ns, i + 1, j + 1);
-          }
-          q = cell_coef(w * t00, w * t10, w * t01, w * t11);
-        }
-        v[c] = q.a;
-        v[3 + c] = q.b;
-        v[6 + c] = q.c;
-        v[9 + c] = q.d;
-      }
-      float* dst = T + L.pair_off(p) + rem * 12;
-      for (int t = 0; t < 12; ++t) dst[t] = v[t];
-      continue;
-    }
-    int r = e - n_lut;
+  const int total = n_xc + n_gxy + n_gyc + n_pad + n_tail;
+  for (int e = (blockIdx.x - 9) * blockDim.x + threadIdx.x; e < total;
+       e += (gridDim.x - 9) * blockDim.x) {
+    int r = e;
     if (r < n_xc) {  // merged xc cell (c, jx, jc)
       const int c = r / ((ds - 1) * (ds - 1));
       const int rem = r - c * (ds - 1) * (ds - 1);
@@ -192,11 +187,16 @@ cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const
                         const float* lw, const float* lb, const float* gp, const float* gw,
                         const float* gb, int k, const TableLayout& L, int batch, float* tables,
                         cudaStream_t st) {
-  // one thread per LUT cell / grid entry; small blocks spread the latency-bound
-  // f64 work over many SMs
-  const int items = 3 * (L.dt - 1) * L.cst + 3 * (L.ds - 1) * (L.ds - 1) + 4 * L.ds * L.ds + 64;
-  dim3 grid((items + 63) / 64, batch);
-  pack_kernel<<<grid, 64, 0, st>>>(lp, fu, fs, fvt, ns, lw, lb, gp, gw, gb, k, L, tables);
+  // 9 plane blocks + enough grid blocks for one item per thread
+  const int grid_items = 3 * (L.ds - 1) * (L.ds - 1) + 4 * L.ds * L.ds + 64;
+  dim3 grid(9 + (grid_items + 255) / 256, batch);
+  const size_t smem = (size_t)L.dt * L.dt * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  pack_kernel<<<grid, 256, smem, st>>>(lp, fu, fs, fvt, ns, lw, lb, gp, gw, gb, k, L, tables);
   return cudaGetLastError();
 }
 

@@ -55,9 +55,15 @@ def test_fused_backward_vs_oracle(dev, oracle_mod, w, h, d_t, d_s, k, low, high)
     for mine, theirs in names.items():
         got = g[mine][0].cpu().numpy()
         close(got, ref[theirs], mine)
+    # touched-vertex pattern: every vertex whose reference gradient exceeds the
+    # tolerance is touched here too, and nothing untouched by the reference is
+    # touched here (fixed-point accumulation may round sub-tolerance sums to 0)
     for mine, theirs in (("dlut_planes", "dlp"), ("dgrid_planes", "dgp")):
         got = g[mine][0].cpu().numpy()
-        assert np.array_equal(got != 0, ref[theirs] != 0), mine
+        want = ref[theirs]
+        big = np.abs(want) > RTOL * np.abs(want).max()
+        assert np.all(got[big] != 0), mine
+        assert np.all(got[want == 0] == 0), mine
 
 
 def test_fused_backward_smooth_1080p_batch(dev, oracle_mod):
@@ -101,3 +107,45 @@ def test_reconstruct_backward_vs_oracle(dev, oracle_mod):
         close(du[0].cpu().numpy(), rdu, "du")
         close(ds[0].cpu().numpy(), rds, "ds")
         close(dvt[0].cpu().numpy(), rdvt, "dvt")
+
+
+def test_autograd_matches_oracle_and_trains(dev, oracle_mod):
+    """Config-5 style step through torch.autograd: L2 loss vs X^0.8."""
+    import torch
+
+    from paper_2508_16121_b200 import synth
+    from paper_2508_16121_b200.autograd import svdlut_apply
+
+    case = synth.make_batch([21, 22], h=72, w=128)
+    leaves = {k: T(getattr(case, k), dev).requires_grad_(True)
+              for k in ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")}
+    rgb = T(case.rgb, dev).requires_grad_(True)
+    target = (T(case.rgb, dev).clamp_min(0) ** 0.8).detach()
+    y = svdlut_apply(rgb, leaves["u"], leaves["s"], leaves["vt"], leaves["lw"], leaves["lb"],
+                     leaves["grid_planes"], leaves["gw"], leaves["gb"])
+    loss = ((y - target) ** 2).mean()
+    loss.backward()
+    gy = (2.0 * (y - target) / y.numel()).detach()
+    for b in range(2):
+        planes = oracle_mod.reconstruct(case.u[b], case.s[b], case.vt[b])
+        ref = oracle_mod.fused_bwd(case.rgb[b], gy[b].cpu().numpy(), planes, case.lw[b],
+                                   case.grid_planes[b], case.gw[b])
+        close(rgb.grad[b].cpu().numpy(), ref["gx"], "gx")
+        close(leaves["grid_planes"].grad[b].cpu().numpy(), ref["dgp"], "dgrid")
+        close(leaves["lw"].grad[b].cpu().numpy(), ref["dlw"], "dlw")
+        du, ds_, dvt = oracle_mod.reconstruct_bwd(case.u[b], case.s[b], case.vt[b], ref["dlp"])
+        close(leaves["u"].grad[b].cpu().numpy(), du, "du")
+        close(leaves["s"].grad[b].cpu().numpy(), ds_, "ds")
+        close(leaves["vt"].grad[b].cpu().numpy(), dvt, "dvt")
+    # a few SGD steps on the tables decrease the loss
+    opt = torch.optim.SGD(list(leaves.values()), lr=0.5)
+    losses = []
+    for _ in range(5):
+        opt.zero_grad()
+        y = svdlut_apply(rgb.detach(), leaves["u"], leaves["s"], leaves["vt"], leaves["lw"],
+                         leaves["lb"], leaves["grid_planes"], leaves["gw"], leaves["gb"])
+        l = ((y - target) ** 2).mean()
+        l.backward()
+        opt.step()
+        losses.append(float(l))
+    assert losses[-1] < losses[0]
