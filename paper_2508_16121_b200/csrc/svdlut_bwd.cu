@@ -157,7 +157,7 @@ __device__ __forceinline__ float4 bgrid_entry(const float* sm, const TableLayout
   const float v00 = X[(jx * ds + jy) * 3 + c], v01 = X[(jx * ds + jy + 1) * 3 + c];
   const float v10 = X[((jx + 1) * ds + jy) * 3 + c], v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
   const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
-  return make_float4(x.x + q0 + r0, x.y + (r1 - r0), x.z + (q1 - q0), x.w);
+  return make_float4(x.x + q0 + r0, x.z + (q1 - q0), x.y + (r1 - r0), x.w);  // {M, M', N, N'}
 }
 
 struct BChunk {
@@ -332,30 +332,30 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           {
             const uint32_t a = br * cst48 + lutK + bg * 48u;  // rg
             const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
-            // B: c0.w c1.x c1.y  C: c1.z c1.w c2.x  D: c2.y c2.z c2.w
-            gar += g0 * __fmaf_rn(c2.y, dg, c0.w) + g1 * __fmaf_rn(c2.z, dg, c1.x) + g2 * __fmaf_rn(c2.w, dg, c1.y);
-            gag += g0 * __fmaf_rn(c2.y, dr, c1.z) + g1 * __fmaf_rn(c2.z, dr, c1.w) + g2 * __fmaf_rn(c2.w, dr, c2.x);
+            // cell_index: B c0.z c0.w c2.y  C c1.x c1.y c2.z  D c1.z c1.w c2.w
+            gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.y);
+            gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.z);
           }
           {
             const uint32_t a = br * cst48 + lutK + bb * 48u + pair_bytes;  // rb
             const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
-            gar += g0 * __fmaf_rn(c2.y, db, c0.w) + g1 * __fmaf_rn(c2.z, db, c1.x) + g2 * __fmaf_rn(c2.w, db, c1.y);
-            gab += g0 * __fmaf_rn(c2.y, dr, c1.z) + g1 * __fmaf_rn(c2.z, dr, c1.w) + g2 * __fmaf_rn(c2.w, dr, c2.x);
+            gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.y);
+            gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.z);
           }
           {
             const int ti = (int)(bg * cst3 + bb * 3u + texK);  // gb via the texture path
             const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
                          c2 = tex1Dfetch<float4>(p.tex, ti + 2);
-            gag += g0 * __fmaf_rn(c2.y, db, c0.w) + g1 * __fmaf_rn(c2.z, db, c1.x) + g2 * __fmaf_rn(c2.w, db, c1.y);
-            gab += g0 * __fmaf_rn(c2.y, dg, c1.z) + g1 * __fmaf_rn(c2.z, dg, c1.w) + g2 * __fmaf_rn(c2.w, dg, c2.x);
+            gag += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.y);
+            gab += g0 * __fmaf_rn(c1.z, dg, c1.x) + g1 * __fmaf_rn(c1.w, dg, c1.y) + g2 * __fmaf_rn(c2.w, dg, c2.z);
           }
           const uint32_t sa = slotK + (uint32_t)jx * jx_bytes;
           const float4 s0 = blds4(sa + sr * 16u);
           const float4 s1 = blds4(sa + chan_bytes + sg * 16u);
           const float4 s2 = blds4(sa + 2u * chan_bytes + sb * 16u);
-          const float gsr = g0 * __fmaf_rn(s0.w, ex, s0.z);
-          const float gsg = g1 * __fmaf_rn(s1.w, ex, s1.z);
-          const float gsb = g2 * __fmaf_rn(s2.w, ex, s2.z);
+          const float gsr = g0 * __fmaf_rn(s0.w, ex, s0.y);  // slot {M, M', N, N'}
+          const float gsg = g1 * __fmaf_rn(s1.w, ex, s1.y);
+          const float gsb = g2 * __fmaf_rn(s2.w, ex, s2.y);
           oxr[u] = (Xr < 0.f || Xr > 1.f) ? 0.f : __fmaf_rn(gar, tdm1, gsr * sdm1);
           oxg[u] = (Xg < 0.f || Xg > 1.f) ? 0.f : __fmaf_rn(gag, tdm1, gsg * sdm1);
           oxb[u] = (Xb < 0.f || Xb > 1.f) ? 0.f : __fmaf_rn(gab, tdm1, gsb * sdm1);

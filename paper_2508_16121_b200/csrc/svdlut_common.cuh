@@ -24,7 +24,8 @@ constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 // ---- packed per-image table layout (floats; every block 16 B aligned) ------
 //
 //   lut01 [pair rg|rb][i d_t-1][j cst][12]  LUT coefficient cells, 3 channels
-//         packed {A0 A1 A2 B0 | B1 B2 C0 C1 | C2 D0 D1 D2},
+//         packed {A0 A1 B0 B1 | C0 C1 D0 D1 | A2 B2 C2 D2} (cell_index):
+//         channels 0/1 as float2 pairs for the packed FP32x2 pipe,
 //         v_c(a,b) = A_c + B_c*da + C_c*db + D_c*da*db   (weights lw folded in)
 //   xc    [c 3][jx d_s-1][jc d_s-1][4]   merged xc grid of output channel c,
 //         {A,B,C,D} over (ex, ec)        (sum over k%3==c of gw[k,1]*G[k,1])
@@ -43,6 +44,9 @@ constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 // the 3x3 cell neighbourhood a noisy pixel run touches maps to distinct bank
 // groups (offsets {0, +-1, +-cst, +-cst+-1} mod 8 collide only for the two
 // opposite diagonals).
+// Position of coefficient k (0 A, 1 B, 2 C, 3 D) of output channel c in a cell.
+__host__ __device__ constexpr int cell_index(int c, int k) { return c < 2 ? 2 * k + c : 8 + k; }
+
 struct TableLayout {
   int dt, ds, cst;
   int pair_floats;                               // one LUT pair

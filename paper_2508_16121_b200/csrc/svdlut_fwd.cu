@@ -41,13 +41,10 @@ namespace svdlut {
 #ifndef FWD_NW
 #define FWD_NW 15  // 15 x 128 px = 1920: divides 1080p / 4K / 8K rows exactly
 #endif
-#ifndef FWD_NTEX
-#define FWD_NTEX 1  // LUT pairs gathered through the texture path (gb, or rb and gb)
-#endif
-constexpr int kNTex = FWD_NTEX;
 constexpr int kPx = FWD_PX;
 constexpr int kFwdWarps = FWD_NW;
 constexpr int kChunk = 32 * kPx;
+constexpr int kRing = 3;  // per-row grid slot buffers
 constexpr uint32_t kMagicBits = 0x4B000000u;  // bits of 2^23
 
 struct FwdParams {
@@ -82,6 +79,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   asm volatile(
@@ -130,34 +130,29 @@ __device__ __forceinline__ uint32_t cbracket(float q, float dm1, float dm2, floa
   return __float_as_uint(m);
 }
 
-// o_c (+)= A_c + B_c*a + C_c*b + D_c*a*b; cell = {A0 A1 A2 B0|B1 B2 C0 C1|C2 D0 D1 D2}
+// One LUT pair's contribution A + B a + (C + D a) b for the three channels;
+// cell = {A0 A1 B0 B1 | C0 C1 D0 D1 | A2 B2 C2 D2} (cell_index in
+// svdlut_common.cuh): channels 0/1 on the FP32x2 pipe.
 template <bool FIRST>
-__device__ __forceinline__ void lut_term(uint32_t a, float da, float db, float& o0, float& o1,
-                                         float& o2) {
-  const float4 c0 = lds4(a), c1 = lds4(a + 16), c2 = lds4(a + 32);
-  const float v0 = __fmaf_rn(db, __fmaf_rn(c2.y, da, c1.z), __fmaf_rn(c0.w, da, c0.x));
-  const float v1 = __fmaf_rn(db, __fmaf_rn(c2.z, da, c1.w), __fmaf_rn(c1.x, da, c0.y));
-  const float v2 = __fmaf_rn(db, __fmaf_rn(c2.w, da, c2.x), __fmaf_rn(c1.y, da, c0.z));
+__device__ __forceinline__ void cell_term(const float4& c0, const float4& c1, const float4& c2,
+                                          float da, float db, float2& acc01, float& acc2) {
+  const float2 a2 = make_float2(da, da);
+  const float2 t = __ffma2_rn(make_float2(c0.z, c0.w), a2, make_float2(c0.x, c0.y));
+  const float2 s = __ffma2_rn(make_float2(c1.z, c1.w), a2, make_float2(c1.x, c1.y));
+  const float v2 = __fmaf_rn(db, __fmaf_rn(c2.w, da, c2.z), __fmaf_rn(c2.y, da, c2.x));
   if (FIRST) {
-    o0 = v0;
-    o1 = v1;
-    o2 = v2;
+    acc01 = __ffma2_rn(s, make_float2(db, db), t);
+    acc2 = v2;
   } else {
-    o0 += v0;
-    o1 += v1;
-    o2 += v2;
+    acc01 = __ffma2_rn(s, make_float2(db, db), __fadd2_rn(t, acc01));
+    acc2 += v2;
   }
 }
 
-// Same term with the cell read through the texture path (texel index t).
-__device__ __forceinline__ void lut_term_tex(cudaTextureObject_t tex, int t, float da, float db,
-                                             float& o0, float& o1, float& o2) {
-  const float4 c0 = tex1Dfetch<float4>(tex, t);
-  const float4 c1 = tex1Dfetch<float4>(tex, t + 1);
-  const float4 c2 = tex1Dfetch<float4>(tex, t + 2);
-  o0 += __fmaf_rn(db, __fmaf_rn(c2.y, da, c1.z), __fmaf_rn(c0.w, da, c0.x));
-  o1 += __fmaf_rn(db, __fmaf_rn(c2.z, da, c1.w), __fmaf_rn(c1.x, da, c0.y));
-  o2 += __fmaf_rn(db, __fmaf_rn(c2.w, da, c2.x), __fmaf_rn(c1.y, da, c0.z));
+// Merged grid slot {M, M', N, N'}: M + N ex + (M' + N' ex) ec.
+__device__ __forceinline__ float slot_term(const float4& g, float ex, float ec) {
+  const float2 pq = __ffma2_rn(make_float2(g.z, g.w), make_float2(ex, ex), make_float2(g.x, g.y));
+  return __fmaf_rn(ec, pq.y, pq.x);
 }
 
 template <int PX>
@@ -220,7 +215,7 @@ struct GridG {
 };
 
 // Merged grid coefficients of channel c at (row bracket jy/ey, x-cell jx, guide cell jc):
-//   {M, N, M', N'} with term = M + N*ex + (M' + N'*ex)*ec  (biases included)
+//   {M, M', N, N'} with term = M + N*ex + (M' + N'*ex)*ec  (biases included)
 __device__ __forceinline__ float4 grid_entry(const GridG& G, int ds, int c, int jx, int jc, int jy,
                                              float ey) {
   const float4 x = G.xc[(c * (ds - 1) + jx) * (ds - 1) + jc];
@@ -233,19 +228,19 @@ __device__ __forceinline__ float4 grid_entry(const GridG& G, int ds, int c, int 
   const float v10 = X[((jx + 1) * ds + jy) * 3 + c];
   const float v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
   const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
-  return make_float4(x.x + q0 + r0, x.y + (r1 - r0), x.z + (q1 - q0), x.w);
+  return make_float4(x.x + q0 + r0, x.z + (q1 - q0), x.y + (r1 - r0), x.w);
 }
 
-// Shared-memory image of the tables: LUT pairs [0, 3-NTEX) then the grid
-// block (xc, gxy, gyc); the remaining pairs are read through the texture.
-__host__ __device__ inline uint32_t smem_grid_off(const TableLayout& L, int ntex) {
-  return (uint32_t)(3 - ntex) * (uint32_t)L.pair_floats * 4u;
+// Shared-memory image of the tables: LUT pairs rg, rb then the grid block
+// (xc, gxy, gyc); pair gb is read through the texture path.
+__host__ __device__ inline uint32_t smem_grid_off(const TableLayout& L) {
+  return 2u * (uint32_t)L.pair_floats * 4u;
 }
-__host__ __device__ inline uint32_t smem_tables_bytes(const TableLayout& L, int ntex) {
-  return smem_grid_off(L, ntex) + (uint32_t)(L.lut2_off - L.xc_off) * 4u;
+__host__ __device__ inline uint32_t smem_tables_bytes(const TableLayout& L) {
+  return smem_grid_off(L) + (uint32_t)(L.lut2_off - L.xc_off) * 4u;
 }
 
-template <int DT, int DS, bool CHECK, int PX, int NW, int NTEX>
+template <int DT, int DS, bool CHECK, int PX, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   constexpr int CH = 32 * PX;  // pixels per warp chunk
   extern __shared__ __align__(128) float smem[];
@@ -258,16 +253,21 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
 
+  // slot ring: full[i] completes when every warp wrote its share of the row in
+  // buffer i, empty[i] when every warp finished reading it
+  __shared__ __align__(8) uint64_t ring_bar[2 * kRing];
+  const uint32_t full0 = smem_addr(&ring_bar[0]), empty0 = smem_addr(&ring_bar[kRing]);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    for (int i = 0; i < 2 * kRing; ++i) mbar_init(smem_addr(&ring_bar[i]), NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t lut_smem_bytes = smem_grid_off(L, NTEX);
-  const uint32_t table_bytes = smem_tables_bytes(L, NTEX);
+  const uint32_t lut_smem_bytes = smem_grid_off(L);
+  const uint32_t table_bytes = smem_tables_bytes(L);
   const int nent = (ds - 1) * 3 * (ds - 1);                  // slot entries per row
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
   // column table: t(x) = RN32(RN32(x/(W-1)) * (d_s-1)) for every column, built once
-  float* col_t = reinterpret_cast<float*>(slots + 2 * nent);
+  float* col_t = reinterpret_cast<float*>(slots + kRing * nent);
   const uint32_t col_addr = smem_addr(col_t);
   if (p.col_smem) {
     const int wpad = (p.w + 3) & ~3;
@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const bool vec_ok = ((p.w & 3) == 0) &&
                       ((reinterpret_cast<uintptr_t>(p.rgb) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0;
   uint32_t phase = 0;
+  uint32_t nrow = 0;  // CTA row ordinal (slot ring position)
   bool bad = false;
 
   long long r = r_begin;
@@ -329,8 +330,6 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
-    const uint32_t texKrb = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
-                            (uint32_t)(L.pair_off(1) / 4) - kMagicBits * (cst3 + 3u);
 
     // the first chunk's loads overlap the table copy
     const int cpr = (p.w + CH - 1) / CH;
@@ -339,23 +338,30 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     if (cur_k < cpr) load_chunk<PX>(plane0, pl, cur_y, cur_k * CH, p.w, lane, vec_ok, cur);
     mbar_wait(bar, phase);
     phase ^= 1u;
-    // slots of the first row (buffer 0)
-    {
+    // This warp's share of the slots of row y (CTA row ordinal n) into ring
+    // buffer n % kRing.  Row n+2 is produced once row n is done, so warps may
+    // drift apart by a row instead of meeting at a CTA barrier every row.
+    auto produce = [&](uint32_t n, int y) {
       float ey;
-      const int jy = (int)(row_bracket(p.y0 + y_first, p.rcp_h, sdm1, sdm2, ey) - kMagicBits);
-      for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+      const int jy = (int)(row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey) - kMagicBits);
+      float4* S = slots + (n % kRing) * nent;
+      for (int e = warp * 32 + lane; e < nent; e += NW * 32) {
         const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
         const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-        slots[e] = grid_entry(G, ds, ch, jx, jc, jy, ey);
+        S[e] = grid_entry(G, ds, ch, jx, jc, jy, ey);
       }
-    }
-    __syncthreads();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full0 + 8u * (n % kRing));
+    };
+    const uint32_t n0 = nrow;
+    const int cnt = y_last - y_first + 1;
+    produce(n0, y_first);
+    if (cnt > 1) produce(n0 + 1, y_first + 1);
 
     for (int y = y_first; y <= y_last; ++y) {
-      const int buf = (y - y_first) & 1;
-      float ey;
-      (void)row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey);
-      const uint32_t slotK = slotK0 + (uint32_t)buf * slot_row_bytes;
+      const uint32_t n = n0 + (uint32_t)(y - y_first);
+      mbar_wait(full0 + 8u * (n % kRing), (n / kRing) & 1u);
+      const uint32_t slotK = slotK0 + (n % kRing) * slot_row_bytes;
       // ---- this warp's chunks of row y: k = warp, warp + W, ... ----
       for (; cur_y == y && cur_k < cpr;) {
         ChunkIn<PX> nxt;
@@ -398,45 +404,27 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         // use (software pipeline depth 1), hiding the texture latency behind
         // the shared-memory work of the previous pixel.
         float o0[PX], o1[PX], o2[PX];
-        float4 tx0, tx1, tx2;  // in-flight texture cells (pair gb) of the next pixel
-        float4 ty0, ty1, ty2;  // pair rb when it is on the texture path too
-        float tdg, tdb, tdr;   // their deltas
+        float4 tx0, tx1, tx2;  // in-flight texture cells of the next pixel
+        float tdg, tdb;        // its deltas
         {
-          const float qr = __saturatef(cur.r[0]), qg = __saturatef(cur.g[0]), qb = __saturatef(cur.b[0]);
-          const uint32_t bg = cbracket(qg, tdm1, tdm2, tdg);
-          const uint32_t bb = cbracket(qb, tdm1, tdm2, tdb);
+          const uint32_t bg = cbracket(__saturatef(cur.g[0]), tdm1, tdm2, tdg);
+          const uint32_t bb = cbracket(__saturatef(cur.b[0]), tdm1, tdm2, tdb);
           const int ti = (int)(bg * cst3 + bb * 3u + texK);
           tx0 = tex1Dfetch<float4>(p.tex, ti);
           tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
           tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
-          if (NTEX == 2) {
-            const uint32_t br = cbracket(qr, tdm1, tdm2, tdr);
-            const int tr = (int)(br * cst3 + bb * 3u + texKrb);
-            ty0 = tex1Dfetch<float4>(p.tex, tr);
-            ty1 = tex1Dfetch<float4>(p.tex, tr + 1);
-            ty2 = tex1Dfetch<float4>(p.tex, tr + 2);
-          }
         }
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
           const float4 c0 = tx0, c1 = tx1, c2 = tx2;
-          const float4 e0 = ty0, e1 = ty1, e2 = ty2;
-          const float dg = tdg, db = tdb, drr = tdr;
+          const float dg = tdg, db = tdb;
           if (u + 1 < PX) {
-            const float qg1 = __saturatef(cur.g[u + 1]), qb1 = __saturatef(cur.b[u + 1]);
-            const uint32_t bg1 = cbracket(qg1, tdm1, tdm2, tdg);
-            const uint32_t bb1 = cbracket(qb1, tdm1, tdm2, tdb);
+            const uint32_t bg1 = cbracket(__saturatef(cur.g[u + 1]), tdm1, tdm2, tdg);
+            const uint32_t bb1 = cbracket(__saturatef(cur.b[u + 1]), tdm1, tdm2, tdb);
             const int ti = (int)(bg1 * cst3 + bb1 * 3u + texK);
             tx0 = tex1Dfetch<float4>(p.tex, ti);
             tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
             tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
-            if (NTEX == 2) {
-              const uint32_t br1 = cbracket(__saturatef(cur.r[u + 1]), tdm1, tdm2, tdr);
-              const int tr = (int)(br1 * cst3 + bb1 * 3u + texKrb);
-              ty0 = tex1Dfetch<float4>(p.tex, tr);
-              ty1 = tex1Dfetch<float4>(p.tex, tr + 1);
-              ty2 = tex1Dfetch<float4>(p.tex, tr + 2);
-            }
           }
           const float qr = __saturatef(cur.r[u]), qg = __saturatef(cur.g[u]),
                       qb = __saturatef(cur.b[u]);
@@ -445,18 +433,17 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           const uint32_t bg = cbracket(qg, tdm1, tdm2, dg_);
           const uint32_t bb = cbracket(qb, tdm1, tdm2, db_);
           const uint32_t ur = br * cst48 + lutK;
-          float a0, a1, a2;
-          lut_term<true>(ur + bg * 48u, dr, dg_, a0, a1, a2);
-          if (NTEX == 1) {
-            lut_term<false>(ur + bb * 48u + pair_bytes, dr, db_, a0, a1, a2);
-          } else {
-            a0 += __fmaf_rn(db, __fmaf_rn(e2.y, drr, e1.z), __fmaf_rn(e0.w, drr, e0.x));
-            a1 += __fmaf_rn(db, __fmaf_rn(e2.z, drr, e1.w), __fmaf_rn(e1.x, drr, e0.y));
-            a2 += __fmaf_rn(db, __fmaf_rn(e2.w, drr, e2.x), __fmaf_rn(e1.y, drr, e0.z));
+          float2 acc01;
+          float acc2;
+          {  // pair rg (shared memory)
+            const uint32_t ad = ur + bg * 48u;
+            cell_term<true>(lds4(ad), lds4(ad + 16), lds4(ad + 32), dr, dg_, acc01, acc2);
           }
-          a0 += __fmaf_rn(db, __fmaf_rn(c2.y, dg, c1.z), __fmaf_rn(c0.w, dg, c0.x));
-          a1 += __fmaf_rn(db, __fmaf_rn(c2.z, dg, c1.w), __fmaf_rn(c1.x, dg, c0.y));
-          a2 += __fmaf_rn(db, __fmaf_rn(c2.w, dg, c2.x), __fmaf_rn(c1.y, dg, c0.z));
+          {  // pair rb (shared memory)
+            const uint32_t ad = ur + bb * 48u + pair_bytes;
+            cell_term<false>(lds4(ad), lds4(ad + 16), lds4(ad + 32), dr, db_, acc01, acc2);
+          }
+          cell_term<false>(c0, c1, c2, dg, db, acc01, acc2);  // pair gb (texture path)
           // grids: one merged (xy + xc + yc) coefficient cell per channel
           float er, eg, eb;
           const uint32_t sr = cbracket(qr, sdm1, sdm2, er);
@@ -464,12 +451,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           const uint32_t sb = cbracket(qb, sdm1, sdm2, eb);
           const float ex = exs[u];
           const uint32_t sa = slotK + (uint32_t)jxs[u] * jx_bytes;
-          const float4 g0 = lds4(sa + sr * 16u);
-          const float4 g1 = lds4(sa + chan_bytes + sg * 16u);
-          const float4 g2 = lds4(sa + 2u * chan_bytes + sb * 16u);
-          o0[u] = a0 + __fmaf_rn(er, __fmaf_rn(g0.w, ex, g0.z), __fmaf_rn(g0.y, ex, g0.x));
-          o1[u] = a1 + __fmaf_rn(eg, __fmaf_rn(g1.w, ex, g1.z), __fmaf_rn(g1.y, ex, g1.x));
-          o2[u] = a2 + __fmaf_rn(eb, __fmaf_rn(g2.w, ex, g2.z), __fmaf_rn(g2.y, ex, g2.x));
+          o0[u] = acc01.x + slot_term(lds4(sa + sr * 16u), ex, er);
+          o1[u] = acc01.y + slot_term(lds4(sa + chan_bytes + sg * 16u), ex, eg);
+          o2[u] = acc2 + slot_term(lds4(sa + 2u * chan_bytes + sb * 16u), ex, eb);
           if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
         }
         const long long rowoff = (long long)cur_y * p.w;
@@ -491,19 +475,16 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         cur_y = nxt_y;
         cur_k = nxt_k;
       }
-      // ---- slots of row y+1 into the other buffer (free since the last barrier) ----
-      if (y < y_last) {
-        float ey1;
-        const int jy1 = (int)(row_bracket(p.y0 + y + 1, p.rcp_h, sdm1, sdm2, ey1) - kMagicBits);
-        float4* S = slots + (buf ^ 1) * nent;
-        for (int e = threadIdx.x; e < nent; e += blockDim.x) {
-          const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
-          const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-          S[e] = grid_entry(G, ds, ch, jx, jc, jy1, ey1);
-        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8u * (n % kRing));
+      if (y + 2 <= y_last) {
+        // buffer (n+2) % kRing last held row n-1 (of this image segment when
+        // y > y_first; otherwise the segment-start barrier covers it)
+        if (y > y_first) mbar_wait(empty0 + 8u * ((n - 1) % kRing), ((n - 1) / kRing) & 1u);
+        produce(n + 2, y + 2);
       }
-      __syncthreads();
     }
+    nrow = n0 + (uint32_t)cnt;
     r += y_last - y_first + 1;
   }
   if (CHECK) {
@@ -514,7 +495,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
 size_t fwd_smem_bytes(int dt, int ds) {
   const TableLayout L = TableLayout::make(dt, ds);
   // staged tables + double-buffered per-row grid slots [jx][c][jc] (float4)
-  return (size_t)smem_tables_bytes(L, kNTex) + 2 * (size_t)(ds - 1) * 3 * (ds - 1) * 16;
+  return (size_t)smem_tables_bytes(L) + kRing * (size_t)(ds - 1) * 3 * (ds - 1) * 16;
 }
 
 // Keep at least this much of the 256 KB L1/shared array as L1 so the
@@ -644,8 +625,8 @@ cudaError_t fwd_texture_used(cudaTextureObject_t tex, cudaStream_t st) { return 
 template <int DT, int DS>
 static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t smem,
                                cudaStream_t st) {
-  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps, kNTex>
-                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps, kNTex>;
+  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps>
+                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps>;
   // function attributes are set once per (instantiation, smem size); setting
   // them is not a stream operation, so graph capture does not see it
   static size_t configured[2] = {0, 0};

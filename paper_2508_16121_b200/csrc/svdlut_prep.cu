@@ -99,10 +99,10 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
         q = cell_coef(w * Ts[i * dt + j], w * Ts[(i + 1) * dt + j], w * Ts[i * dt + j + 1],
                       w * Ts[(i + 1) * dt + j + 1]);
       float* dst = base + e * 12;
-      dst[c] = q.a;
-      dst[3 + c] = q.b;
-      dst[6 + c] = q.c;
-      dst[9 + c] = q.d;
+      dst[cell_index(c, 0)] = q.a;
+      dst[cell_index(c, 1)] = q.b;
+      dst[cell_index(c, 2)] = q.c;
+      dst[cell_index(c, 3)] = q.d;
     }
     return;
   }
