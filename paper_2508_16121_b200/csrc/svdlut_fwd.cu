@@ -277,6 +277,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     }
   }
 
+  // inputs and tables may come from the previous kernel in the stream (PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
   GridG G;
   const float* gsm = smem + lut_smem_bytes / 4 - L.xc_off;  // global offset -> smem
   G.xc = reinterpret_cast<const float4*>(gsm + L.xc_off);
@@ -641,8 +644,20 @@ static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t 
     if (e != cudaSuccess) return e;
     configured[check] = smem;
   }
-  kern<<<grid, kFwdWarps * 32, smem, st>>>(p);
-  return cudaGetLastError();
+  // Programmatic dependent launch: the kernel's prologue (barriers, column
+  // table) may overlap the tail of the table-packing kernel before it; every
+  // global access comes after griddepcontrol.wait.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFwdWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,

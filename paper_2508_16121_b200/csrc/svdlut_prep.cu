@@ -54,21 +54,26 @@ __device__ __forceinline__ float lut_entry(const float* __restrict__ U, const fl
   return (float)acc;
 }
 
+constexpr int kPackBand = 4;  // LUT cell rows per pack block
+
 // Packs one image's tables (layout in svdlut_common.cuh).  grid.y = image.
 // The LUT planes come either from `lp` (B,3,3,d_t,d_t) or, when lp == NULL,
 // straight from the SVD factors (u, s, vt, n_s) — the fused prologue that
 // skips materialising the planes.
-//   blocks [0, 9)        one LUT plane (c, p) each: the plane is reconstructed
-//                        into shared memory once, then its coefficient cells
-//                        are written (channel c's 4 floats of every cell)
-//   blocks [9, gridDim)  merged grid cells / vertices and padding
+//   blocks [0, 9*nbands) one band of kPackBand cell rows of LUT plane (c, p):
+//                        the band's vertex rows are reconstructed into shared
+//                        memory, then channel c's 4 floats of each cell written
+//   remaining blocks     merged grid cells / vertices and padding
 __global__ void pack_kernel(const float* __restrict__ lp, const float* __restrict__ fu,
                             const float* __restrict__ fs, const float* __restrict__ fvt, int ns,
                             const float* __restrict__ lw,
                             const float* __restrict__ lb, const float* __restrict__ gp,
                             const float* __restrict__ gw, const float* __restrict__ gb, int k,
                             TableLayout L, float* __restrict__ tables) {
-  extern __shared__ float Ts[];  // one LUT plane, d_t x d_t
+  extern __shared__ float Ts[];  // vertex rows of one LUT plane band
+  // let the fused kernel that follows launch and run its prologue (it waits
+  // for this grid's completion before reading the tables)
+  asm volatile("griddepcontrol.launch_dependents;");
   const long long b = blockIdx.y;
   const int dt = L.dt, ds = L.ds;
   const float* W = lw + b * 9;
@@ -78,27 +83,32 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
   const float* GB = gb + b * (long long)k;
   float* T = tables + b * (long long)L.total_floats;
 
-  if (blockIdx.x < 9) {
-    const int c = blockIdx.x / 3, p = blockIdx.x - 3 * (blockIdx.x / 3);
+  const int nbands = (dt - 1 + kPackBand - 1) / kPackBand;
+  if (blockIdx.x < 9 * nbands) {
+    // plane (c, p), cell rows [i0, i1): vertex rows [i0, i1] staged in smem
+    const int cpi = blockIdx.x / nbands, band = blockIdx.x - cpi * nbands;
+    const int c = cpi / 3, p = cpi - 3 * c;
+    const int i0 = band * kPackBand, i1 = min(i0 + kPackBand, dt - 1);
     const long long cp = b * 9 + c * 3 + p;
-    for (int e = threadIdx.x; e < dt * dt; e += blockDim.x) {
+    const int nv = (i1 - i0 + 1) * dt;
+    for (int e = threadIdx.x; e < nv; e += blockDim.x) {
+      const int i = i0 + e / dt, j = e - (e / dt) * dt;
       if (lp) {
-        Ts[e] = lp[cp * dt * dt + e];
+        Ts[e] = lp[cp * dt * dt + i * dt + j];
       } else {
-        const int i = e / dt, j = e - i * dt;
         Ts[e] = lut_entry(fu + cp * dt * ns, fs + cp * ns, fvt + cp * ns * dt, dt, ns, i, j);
       }
     }
     __syncthreads();
     const double w = (double)W[c * 3 + p];
     float* base = T + L.pair_off(p);
-    for (int e = threadIdx.x; e < (dt - 1) * L.cst; e += blockDim.x) {
-      const int i = e / L.cst, j = e - i * L.cst;
+    for (int e = threadIdx.x; e < (i1 - i0) * L.cst; e += blockDim.x) {
+      const int il = e / L.cst, j = e - il * L.cst;
       Coef q = {0.f, 0.f, 0.f, 0.f};
       if (j < dt - 1)
-        q = cell_coef(w * Ts[i * dt + j], w * Ts[(i + 1) * dt + j], w * Ts[i * dt + j + 1],
-                      w * Ts[(i + 1) * dt + j + 1]);
-      float* dst = base + e * 12;
+        q = cell_coef(w * Ts[il * dt + j], w * Ts[(il + 1) * dt + j], w * Ts[il * dt + j + 1],
+                      w * Ts[(il + 1) * dt + j + 1]);
+      float* dst = base + ((i0 + il) * L.cst + j) * 12;
       dst[cell_index(c, 0)] = q.a;
       dst[cell_index(c, 1)] = q.b;
       dst[cell_index(c, 2)] = q.c;
@@ -113,8 +123,9 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
   const int n_pad = L.lut2_off - (L.gyc_off + n_gyc);
   const int n_tail = L.total_floats - (L.lut2_off + L.pair_floats);
   const int total = n_xc + n_gxy + n_gyc + n_pad + n_tail;
-  for (int e = (blockIdx.x - 9) * blockDim.x + threadIdx.x; e < total;
-       e += (gridDim.x - 9) * blockDim.x) {
+  const int gb0 = 9 * nbands;
+  for (int e = (blockIdx.x - gb0) * blockDim.x + threadIdx.x; e < total;
+       e += (gridDim.x - gb0) * blockDim.x) {
     int r = e;
     if (r < n_xc) {  // merged xc cell (c, jx, jc)
       const int c = r / ((ds - 1) * (ds - 1));
@@ -187,10 +198,11 @@ cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const
                         const float* lw, const float* lb, const float* gp, const float* gw,
                         const float* gb, int k, const TableLayout& L, int batch, float* tables,
                         cudaStream_t st) {
-  // 9 plane blocks + enough grid blocks for one item per thread
+  // 9 planes x row bands + enough grid blocks for one item per thread
   const int grid_items = 3 * (L.ds - 1) * (L.ds - 1) + 4 * L.ds * L.ds + 64;
-  dim3 grid(9 + (grid_items + 255) / 256, batch);
-  const size_t smem = (size_t)L.dt * L.dt * sizeof(float);
+  const int nbands = (L.dt - 1 + kPackBand - 1) / kPackBand;
+  dim3 grid(9 * nbands + (grid_items + 255) / 256, batch);
+  const size_t smem = (size_t)(kPackBand + 1) * L.dt * sizeof(float);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
