@@ -41,6 +41,9 @@ namespace svdlut {
 #ifndef FWD_NW
 #define FWD_NW 15  // 15 x 128 px = 1920: divides 1080p / 4K / 8K rows exactly
 #endif
+#ifndef FWD_L2PF
+#define FWD_L2PF 1  // rows of L2 prefetch distance for the input planes (0: off)
+#endif
 constexpr int kPx = FWD_PX;
 constexpr int kFwdWarps = FWD_NW;
 constexpr int kChunk = 32 * kPx;
@@ -79,6 +82,22 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
+}
+// Bulk L2 prefetch of [p, p + bytes) (16 B granules), no completion tracking.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// Prefetches row y of the three input planes into L2 (16-byte aligned cover
+// of the row, clipped to the plane).
+__device__ __forceinline__ void prefetch_row(const float* plane0, long long pl, int y, int w) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(plane0 + (long long)y * w) & ~(uintptr_t)15;
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(plane0 + (long long)(y + 1) * w) + 15) & ~(uintptr_t)15;
+  const uintptr_t end = reinterpret_cast<uintptr_t>(plane0 + pl) & ~(uintptr_t)15;
+  const uint32_t bytes = (uint32_t)((hi < end ? hi : end) - lo);
+  if (bytes == 0) return;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    prefetch_l2(reinterpret_cast<const void*>(lo + (uintptr_t)c * (uintptr_t)pl * 4u), bytes);
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -363,6 +382,11 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
 
     for (int y = y_first; y <= y_last; ++y) {
       const uint32_t n = n0 + (uint32_t)(y - y_first);
+      if (FWD_L2PF > 0 && threadIdx.x == blockDim.x - 32) {
+        if (y == y_first)
+          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) prefetch_row(plane0, pl, yy, p.w);
+        if (y + FWD_L2PF <= y_last) prefetch_row(plane0, pl, y + FWD_L2PF, p.w);
+      }
       mbar_wait(full0 + 8u * (n % kRing), (n / kRing) & 1u);
       const uint32_t slotK = slotK0 + (n % kRing) * slot_row_bytes;
       // ---- this warp's chunks of row y: k = warp, warp + W, ... ----
