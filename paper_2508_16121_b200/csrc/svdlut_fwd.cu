@@ -54,6 +54,7 @@ struct FwdParams {
   const float* rgb;
   float* out;
   int batch, h, w;
+  long long pl_in, pl_out;  // plane strides in floats (h*w for packed images)
   int y0;                   // first row of this strip in an image of h_total rows
   const float* tables;
   TableLayout L;
@@ -88,16 +89,18 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 // Prefetches row y of the three input planes into L2 (16-byte aligned cover
-// of the row, clipped to the plane).
-__device__ __forceinline__ void prefetch_row(const float* plane0, long long pl, int y, int w) {
-  const uintptr_t lo = reinterpret_cast<uintptr_t>(plane0 + (long long)y * w) & ~(uintptr_t)15;
-  const uintptr_t hi = (reinterpret_cast<uintptr_t>(plane0 + (long long)(y + 1) * w) + 15) & ~(uintptr_t)15;
-  const uintptr_t end = reinterpret_cast<uintptr_t>(plane0 + pl) & ~(uintptr_t)15;
-  const uint32_t bytes = (uint32_t)((hi < end ? hi : end) - lo);
-  if (bytes == 0) return;
+// of each plane's row, clipped to that plane).
+__device__ __forceinline__ void prefetch_row(const float* plane0, long long pl, long long plane_len,
+                                             int y, int w) {
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
-    prefetch_l2(reinterpret_cast<const void*>(lo + (uintptr_t)c * (uintptr_t)pl * 4u), bytes);
+  for (int c = 0; c < 3; ++c) {
+    const float* pc = plane0 + c * pl;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(pc + (long long)y * w) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(pc + (long long)(y + 1) * w) + 15) & ~(uintptr_t)15;
+    const uintptr_t end = reinterpret_cast<uintptr_t>(pc + plane_len) & ~(uintptr_t)15;
+    const uintptr_t top = hi < end ? hi : end;
+    if (top > lo) prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(top - lo));
+  }
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -321,8 +324,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const long long rows_total = (long long)p.batch * p.h;
   const long long r_begin = (long long)blockIdx.x * rows_total / gridDim.x;
   const long long r_end = (long long)(blockIdx.x + 1) * rows_total / gridDim.x;
-  const long long pl = (long long)p.h * p.w;
-  const bool vec_ok = ((p.w & 3) == 0) &&
+  const long long pl = p.pl_in, opl = p.pl_out;  // plane strides (floats)
+  const long long plane_len = (long long)p.h * p.w;
+  const bool vec_ok = ((p.w & 3) == 0) && ((pl & 3) == 0) && ((opl & 3) == 0) &&
                       ((reinterpret_cast<uintptr_t>(p.rgb) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0;
   uint32_t phase = 0;
   uint32_t nrow = 0;  // CTA row ordinal (slot ring position)
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         bulk_g2s(sbase + lut_smem_bytes + off, gsrc + off, min(32768u, gbytes - off), bar);
     }
     const float* plane0 = p.rgb + (long long)b * 3 * pl;
-    float* oplane0 = p.out + (long long)b * 3 * pl;
+    float* oplane0 = p.out + (long long)b * 3 * opl;
     // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
@@ -384,8 +388,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       const uint32_t n = n0 + (uint32_t)(y - y_first);
       if (FWD_L2PF > 0 && threadIdx.x == blockDim.x - 32) {
         if (y == y_first)
-          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) prefetch_row(plane0, pl, yy, p.w);
-        if (y + FWD_L2PF <= y_last) prefetch_row(plane0, pl, y + FWD_L2PF, p.w);
+          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) prefetch_row(plane0, pl, plane_len, yy, p.w);
+        if (y + FWD_L2PF <= y_last) prefetch_row(plane0, pl, plane_len, y + FWD_L2PF, p.w);
       }
       mbar_wait(full0 + 8u * (n % kRing), (n / kRing) & 1u);
       const uint32_t slotK = slotK0 + (n % kRing) * slot_row_bytes;
@@ -486,15 +490,15 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         const long long rowoff = (long long)cur_y * p.w;
         if (vec_ok && xl + PX <= p.w) {
           stg_stream_vec<PX>(oplane0 + rowoff + xl, o0);
-          stg_stream_vec<PX>(oplane0 + pl + rowoff + xl, o1);
-          stg_stream_vec<PX>(oplane0 + 2 * pl + rowoff + xl, o2);
+          stg_stream_vec<PX>(oplane0 + opl + rowoff + xl, o1);
+          stg_stream_vec<PX>(oplane0 + 2 * opl + rowoff + xl, o2);
         } else {
 #pragma unroll
           for (int u = 0; u < PX; ++u) {
             if (xl + u < p.w) {
               __stcs(oplane0 + rowoff + xl + u, o0[u]);
-              __stcs(oplane0 + pl + rowoff + xl + u, o1[u]);
-              __stcs(oplane0 + 2 * pl + rowoff + xl + u, o2[u]);
+              __stcs(oplane0 + opl + rowoff + xl + u, o1[u]);
+              __stcs(oplane0 + 2 * opl + rowoff + xl + u, o2[u]);
             }
           }
         }
@@ -686,7 +690,7 @@ static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t 
 
 cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,
                              int h_total, const float* tables, const TableLayout& L,
-                             int* nonfinite, cudaStream_t st) {
+                             int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (g_num_sms == 0) {
@@ -699,6 +703,8 @@ cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int
   p.batch = batch;
   p.h = h;
   p.w = w;
+  p.pl_in = pl_in > 0 ? pl_in : (long long)h * w;
+  p.pl_out = pl_out > 0 ? pl_out : (long long)h * w;
   p.y0 = y0;
   p.tables = tables;
   p.L = L;

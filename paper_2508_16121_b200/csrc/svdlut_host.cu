@@ -1,10 +1,13 @@
 // svdlut_host.cu — host-buffer entry point (svdlut_enhance_host) and its
 // context: the end-to-end path a host caller (the reference's numpy Image)
 // goes through.  H2D of the image, table prologue, fused apply and D2H of the
-// result run as a pipeline over row strips on two streams, so the PCIe copies
-// in both directions overlap each other and the kernels (strips are
-// independent thanks to the (y0, h_total) contract).
+// result run as a pipeline over row strips on three streams (copy-in,
+// compute, copy-out) chained by per-strip events, so the H2D engine streams
+// strip after strip, the D2H engine follows one strip behind and the kernels
+// run in between (strips are independent thanks to the (y0, h_total)
+// contract).  The step is then bound by the PCIe copies alone.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -19,11 +22,13 @@ extern "C" int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, in
                                           float* out, void* workspace, size_t workspace_bytes,
                                           int* nonfinite, int variant, void* stream);
 
+constexpr int kMaxStrips = 32;
+
 struct svdlut_ctx {
   int device = 0;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  cudaEvent_t ev_tables = nullptr;
-  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // copy-in, compute, copy-out
+  cudaEvent_t ev_in[kMaxStrips] = {};
+  cudaEvent_t ev_k[kMaxStrips] = {};
   void* d_img = nullptr;  // input strips followed by output strips
   size_t d_img_bytes = 0;
   void* d_par = nullptr;  // parameters + packed tables + workspaces
@@ -58,11 +63,12 @@ svdlut_ctx* svdlut_ctx_create(int device) {
     return nullptr;
   }
   bool ok = true;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i)
     ok &= cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) == cudaSuccess;
-    ok &= cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; i < kMaxStrips; ++i) {
+    ok &= cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) == cudaSuccess;
+    ok &= cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming) == cudaSuccess;
   }
-  ok &= cudaEventCreateWithFlags(&c->ev_tables, cudaEventDisableTiming) == cudaSuccess;
   ok &= cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault) == cudaSuccess;
   if (!ok) {
     svdlut_ctx_destroy(c);
@@ -74,17 +80,18 @@ svdlut_ctx* svdlut_ctx_create(int device) {
 void svdlut_ctx_destroy(svdlut_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     if (c->st[i]) cudaStreamSynchronize(c->st[i]);
   }
   if (c->d_img) cudaFree(c->d_img);
   if (c->d_par) cudaFree(c->d_par);
   if (c->h_flag) cudaFreeHost(c->h_flag);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i)
     if (c->st[i]) cudaStreamDestroy(c->st[i]);
-    if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+  for (int i = 0; i < kMaxStrips; ++i) {
+    if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+    if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
   }
-  if (c->ev_tables) cudaEventDestroy(c->ev_tables);
   delete c;
 }
 
@@ -121,55 +128,65 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   char* d_tables = (char*)ctx->d_par + rup(par_floats * 4);
   int* d_flag = (int*)(d_tables + rup(tb));
 
-  cudaStream_t s0 = ctx->st[0];
-  // ---- parameters + table prologue on stream 0 -----------------------------
+  cudaStream_t s_in = ctx->st[0], s_k = ctx->st[1], s_out = ctx->st[2];
+  // ---- parameters + table prologue on the compute stream --------------------
   float* dst[6] = {d_lut, d_lw, d_lb, d_grid, d_gw, d_gb};
   const float* src[6] = {lut_planes, lw, lb, grid_planes, gw, gb};
   const size_t cnt[6] = {n_lut, 9, 3, n_grid, 3ull * k, (size_t)k};
   for (int i = 0; i < 6; ++i)
-    if (cudaMemcpyAsync(dst[i], src[i], cnt[i] * 4, cudaMemcpyHostToDevice, s0) != cudaSuccess)
+    if (cudaMemcpyAsync(dst[i], src[i], cnt[i] * 4, cudaMemcpyHostToDevice, s_k) != cudaSuccess)
       return SVDLUT_ERR_CUDA;
-  if (cudaMemsetAsync(d_flag, 0, sizeof(int), s0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (cudaMemsetAsync(d_flag, 0, sizeof(int), s_k) != cudaSuccess) return SVDLUT_ERR_CUDA;
   if (fast) {
-    int rc = svdlut_pack_tables(d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb, k, d_s, 1, d_tables, s0);
+    int rc = svdlut_pack_tables(d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb, k, d_s, 1, d_tables, s_k);
     if (rc != SVDLUT_OK) return rc;
   }
-  if (cudaEventRecord(ctx->ev_tables, s0) != cudaSuccess) return SVDLUT_ERR_CUDA;
 
-  // ---- strip pipeline -------------------------------------------------------
+  // ---- strip pipeline: H2D (s_in) -> kernel (s_k) -> D2H (s_out) ------------
+  // ~12 MB strips at 4K (8 strips): every copy has a fixed setup cost of
+  // several microseconds, so fewer, larger copies win until the pipeline
+  // fill (first H2D) and drain (last D2H) start to dominate.
   const size_t plane = (size_t)h * w;
-  const int n_strips = h >= 64 ? (h >= 1024 ? 8 : 4) : 1;
+  const size_t img_b = 3 * plane * 4;
+  static const size_t strip_b = [] {
+    const char* e = getenv("SVDLUT_STRIP_KB");  // development knob
+    const long v = e ? atol(e) : 0;
+    return v > 0 ? (size_t)v << 10 : (size_t)12 << 20;
+  }();
+  int n_strips = (int)((img_b + strip_b - 1) / strip_b);
+  if (n_strips > kMaxStrips) n_strips = kMaxStrips;
+  if (n_strips > h) n_strips = h;
+  if (n_strips < 1) n_strips = 1;
   for (int s = 0; s < n_strips; ++s) {
     const int r0 = (int)((long long)h * s / n_strips), r1 = (int)((long long)h * (s + 1) / n_strips);
     const int hs = r1 - r0;
-    if (hs == 0) continue;
-    cudaStream_t st = ctx->st[s & 1];
-    if (cudaStreamWaitEvent(st, ctx->ev_tables, 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
     float* din = d_in + (size_t)3 * r0 * w;    // strip-major device layout (3, hs, w)
     float* dout = d_out + (size_t)3 * r0 * w;
-    // 3 channel rows of the strip: one 2D copy (pitch = plane)
+    // the strip's 3 channel slabs: one 2D copy (host pitch = plane)
     if (cudaMemcpy2DAsync(din, (size_t)hs * w * 4, rgb + (size_t)r0 * w, plane * 4,
-                          (size_t)hs * w * 4, 3, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                          (size_t)hs * w * 4, 3, cudaMemcpyHostToDevice, s_in) != cudaSuccess)
       return SVDLUT_ERR_CUDA;
+    if (cudaEventRecord(ctx->ev_in[s], s_in) != cudaSuccess) return SVDLUT_ERR_CUDA;
+    if (cudaStreamWaitEvent(s_k, ctx->ev_in[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
     int rc;
     if (fast) {
       rc = svdlut_fused_fwd_packed_ex(din, 1, hs, w, r0, h, d_tables, d_t, d_s, dout, nullptr, 0,
-                                      d_flag, -1, st);
+                                      d_flag, -1, s_k);
     } else {
       rc = svdlut_fused_fwd_exact(din, 1, hs, w, r0, h, d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb,
-                                  k, d_s, dout, st);
+                                  k, d_s, dout, s_k);
     }
     if (rc != SVDLUT_OK) return rc;
+    if (cudaEventRecord(ctx->ev_k[s], s_k) != cudaSuccess) return SVDLUT_ERR_CUDA;
+    if (cudaStreamWaitEvent(s_out, ctx->ev_k[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
     if (cudaMemcpy2DAsync(out + (size_t)r0 * w, plane * 4, dout, (size_t)hs * w * 4,
-                          (size_t)hs * w * 4, 3, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+                          (size_t)hs * w * 4, 3, cudaMemcpyDeviceToHost, s_out) != cudaSuccess)
       return SVDLUT_ERR_CUDA;
   }
-  cudaStream_t s1 = ctx->st[1];
-  if (cudaEventRecord(ctx->ev_done[1], s1) != cudaSuccess) return SVDLUT_ERR_CUDA;
-  if (cudaStreamWaitEvent(s0, ctx->ev_done[1], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
-  if (cudaMemcpyAsync(ctx->h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s0) != cudaSuccess)
+  // the last kernel's event already orders every flag write before s_out
+  if (cudaMemcpyAsync(ctx->h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s_out) != cudaSuccess)
     return SVDLUT_ERR_CUDA;
-  if (cudaStreamSynchronize(s0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (cudaStreamSynchronize(s_out) != cudaSuccess) return SVDLUT_ERR_CUDA;
   if (nonfinite) *nonfinite = fast ? *ctx->h_flag : 0;
   return SVDLUT_OK;
 }

@@ -19,7 +19,8 @@ cudaError_t launch_spatial(int w, int h, int y0, int h_total, int ds, SpatialBr*
 // kernel (rows of a strip y0.. of an image with h_total rows).
 cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,
                              int h_total, const float* tables, const TableLayout& L,
-                             int* nonfinite, cudaStream_t st);
+                             int* nonfinite, cudaStream_t st, long long pl_in = 0,
+                             long long pl_out = 0);
 
 cudaError_t launch_fused_exact(const float* rgb, float* out, int batch, int h, int w, int y0,
                                int h_total, const float* lp, const float* lw, const float* lb,

@@ -81,3 +81,27 @@ def host_call():
 
 
 print(f"enhance_host    {timeit(host_call):7.3f} ms")
+
+if os.environ.get("SVDLUT_STRIP_KB"):
+    print(f"strip_kb={os.environ['SVDLUT_STRIP_KB']} enhance_host {timeit(host_call, 20):7.3f} ms")
+
+if os.environ.get("PROBE_PIPE"):
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    flat_in, flat_d, flat_out = pin_in.view(-1), d.view(-1), pin_out.view(-1)
+
+    def pipe(n):
+        evs = []
+        step = flat_in.numel() // n
+        for i in range(n):
+            sl = slice(i * step, (i + 1) * step if i < n - 1 else flat_in.numel())
+            with torch.cuda.stream(s_in):
+                flat_d[sl].copy_(flat_in[sl], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_in)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(e)
+                flat_out[sl].copy_(flat_d[sl], non_blocking=True)
+        torch.cuda.synchronize()
+
+    for n in (1, 4, 8, 16, 32):
+        print(f"copy pipeline n={n:2d}  {timeit(lambda: pipe(n)):7.3f} ms")
