@@ -210,30 +210,37 @@ def main():
         device.apply(ins[i % N_ROT], tables, out=outs[i % N_ROT], variant=a.variant)
         return tables
 
-    # One CUDA graph per rotating buffer set: a step is a single graph launch
-    # (factors->tables prologue + fused apply = 2 kernels), so host launch
-    # latency never gates the device.
-    graphs, apply_graphs = [], []
+    # CUDA graphs: G_r holds r consecutive steps (factors->tables prologue +
+    # fused apply = 2 kernels each, over the rotating buffer sets 0..r-1), so
+    # host launch latency never gates the device and consecutive steps run
+    # back to back; K steps are replayed as floor(K/4) x G_4 + G_(K mod 4).
+    step_graphs, apply_graph = {}, None
     tables0 = eager_step(0)
     if not a.no_graph:
         for i in range(N_ROT):
             eager_step(i)
         torch.cuda.synchronize(dev)
-        for i in range(N_ROT):
+        for r in range(1, N_ROT + 1):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, capture_error_mode="relaxed"):
-                eager_step(i)
-            graphs.append(g)
-            g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g2, capture_error_mode="relaxed"):
+                for i in range(r):
+                    eager_step(i)
+            step_graphs[r] = g
+        apply_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(apply_graph, capture_error_mode="relaxed"):
+            for i in range(N_ROT):
                 device.apply(ins[i], tables0, out=outs[i], variant=a.variant)
-            apply_graphs.append(g2)
 
-    def step(i):
-        if graphs:
-            graphs[i % N_ROT].replay()
+    def run_steps(n, start=0):
+        """n consecutive steps (graph replays when graphs are on)."""
+        if step_graphs:
+            for _ in range(n // N_ROT):
+                step_graphs[N_ROT].replay()
+            if n % N_ROT:
+                step_graphs[n % N_ROT].replay()
         else:
-            eager_step(i)
+            for i in range(n):
+                eager_step(start + i)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -248,24 +255,19 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    for i in range(max(3, a.warmup)):
-        step(i)
+    run_steps(max(3, a.warmup))
     barrier()
     sampler = ClockSampler(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with sampler:
         e0.record(stream)
-        for i in range(a.steps):
-            step(i)
+        run_steps(a.steps)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         # keep the clock sampler under load for >= 0.3 s (the timed region is short)
         t_end = time.perf_counter() + 0.3
-        i = 0
         while time.perf_counter() < t_end:
-            for _ in range(20):
-                step(i)
-                i += 1
+            run_steps(20)
             torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / a.steps
     ms = max_over_ranks(ms)
@@ -273,14 +275,15 @@ def main():
 
     # ---- roofline: the apply (brackets + fused kernel) alone, event-timed ---------
     torch.cuda.synchronize(dev)
-    kreps = max(20, a.steps)
+    kreps = N_ROT * max(5, a.steps // N_ROT)
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k0.record(stream)
-    for i in range(kreps):
-        if apply_graphs:
-            apply_graphs[i % N_ROT].replay()
+    for i in range(kreps // N_ROT):
+        if apply_graph is not None:
+            apply_graph.replay()
         else:
-            device.apply(ins[i % N_ROT], tables0, out=outs[i % N_ROT], variant=a.variant)
+            for j in range(N_ROT):
+                device.apply(ins[j], tables0, out=outs[j], variant=a.variant)
     k1.record(stream)
     torch.cuda.synchronize(dev)
     kms = k0.elapsed_time(k1) / kreps
@@ -346,7 +349,7 @@ def main():
             "data": "synthetic (seeded smooth field, SURVEY.md §8d recipe)",
             "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": 2 * a.steps, "clocks": sampler.summary(),
-            "launch": "cuda graph per step" if graphs else "eager",
+            "launch": "cuda graphs of 4 steps" if step_graphs else "eager",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

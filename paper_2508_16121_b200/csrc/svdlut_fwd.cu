@@ -3,26 +3,30 @@
 // Replaces transform._fused_impl (reference transform.py:215-300).
 //
 // Design:
-//   * One persistent CTA per SM; the packed tables of one image (≈182 KB at
-//     d_t=33 / d_s=17) live in shared memory, staged by TMA bulk copies
-//     (`cp.async.bulk`, completion on an mbarrier).  A CTA owns a contiguous
-//     range of 128-pixel row chunks over (image, row, chunk) and re-stages
-//     only when the range crosses an image boundary.
-//   * Inside an image phase every warp owns a contiguous sub-range of chunks
-//     and software-pipelines the next chunk's global loads under the current
-//     chunk's math.  Lane l handles pixels x0 + l + 32u (u < 4), so one warp
-//     instruction covers 32 consecutive pixels: neighbouring pixels of a
-//     smooth image hit the same or adjacent LUT cells, which the shared-memory
-//     pipe serves with few wavefronts.
-//   * Grid terms: the y-direction is interpolated once per row, per warp, into
-//     warp-private 1-D tables (yc: over the guide, xy: over x), so per pixel and
-//     channel the grids cost one xc coefficient cell (LDS.128) + one yc knot
-//     pair (LDS.64); xy is one channel-packed LDS.128 + LDS.64 per pixel.
-//   * LUT: 3 channel-packed coefficient cells (3×LDS.128 each) with weights
-//     folded in; every term is v = A + B·a + C·b + D·a·b.
+//   * One persistent CTA per SM (15 warps); LUT pairs rg, rb and the grid
+//     block of one image (≈180 KB at d_t=33 / d_s=17) live in shared memory,
+//     staged by TMA bulk copies (`cp.async.bulk`, mbarrier completion); pair
+//     gb is gathered through the texture path, which runs beside the
+//     shared-memory pipe.  A CTA owns a contiguous range of rows over
+//     (image, row) and re-stages only when the range crosses an image.
+//   * Warps take 128-pixel chunks of a row (lane = 4 consecutive pixels,
+//     128-bit streaming loads/stores).  One thread per CTA bulk-prefetches
+//     the input rows two rows ahead into L2 (`cp.async.bulk.prefetch.L2`), so
+//     the chunk loads issued at the top of each chunk hit L2 and no registers
+//     are spent on a register-level prefetch (measured: 73 -> 67.6 µs).
+//   * Per pixel, all nine shared-memory gathers (rg, rb cells: 3 × LDS.128
+//     each; one merged grid slot per channel) are issued back to back, the
+//     three texture gathers of pair gb one pixel ahead.  LUT cells hold
+//     channel-packed coefficients with the weights folded in:
+//     v = A + B·a + C·b + D·a·b (channels 0/1 on the FP32x2 pipe).
+//   * Grid terms: per row, the CTA interpolates xy + xc + yc along y into
+//     merged slots {M, M', N, N'} per (x-cell, channel, guide cell) in a ring
+//     of three row buffers (mbarrier handshakes, warps may drift by a row).
 //   * Integer work stays on 32-bit shared addresses; the colour floor is an
 //     add of 2^23 (svdlut_common.cuh), so the index bits feed IMADs directly.
-//   * Streaming I/O: 24 B/pixel of HBM traffic (3 f32 in, 3 f32 out).
+//   * Streaming I/O: 24 B/pixel of HBM traffic (3 f32 in, 3 f32 out).  The
+//     kernel is bound by the shared-memory pipe (~87% of active cycles, 1.6
+//     wavefronts per pixel), not by HBM — DESIGN.md §3 has the budget.
 #include <cstdint>
 #include <mutex>
 #include <vector>
@@ -42,7 +46,13 @@ namespace svdlut {
 #define FWD_NW 15  // 15 x 128 px = 1920: divides 1080p / 4K / 8K rows exactly
 #endif
 #ifndef FWD_L2PF
-#define FWD_L2PF 1  // rows of L2 prefetch distance for the input planes (0: off)
+#define FWD_L2PF 2  // rows of L2 prefetch distance for the input planes (0: off)
+#endif
+#ifndef FWD_REGPF
+#define FWD_REGPF 0  // next chunk's pixels prefetched into registers under this chunk's math
+#endif
+#ifndef FWD_CHUNKSPLIT
+#define FWD_CHUNKSPLIT 0  // 1: CTA ranges in 128-px chunks (measured slower); 0: whole rows
 #endif
 constexpr int kPx = FWD_PX;
 constexpr int kFwdWarps = FWD_NW;
@@ -321,9 +331,22 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const uint32_t slotK0 = smem_addr(slots) - kMagicBits * 16u;
 
   // contiguous range of global rows (image b, row y) for this CTA
+  // contiguous range of global chunks g = (image b, row y) * cpr + k for this
+  // CTA: rows r_begin .. r_end-1, the first and last possibly partial
+  const int cpr = (p.w + CH - 1) / CH;
+  const long long chunks_total = (long long)p.batch * p.h * cpr;
+#if FWD_CHUNKSPLIT
+  const long long g_begin = (long long)blockIdx.x * chunks_total / gridDim.x;
+  const long long g_end = (long long)(blockIdx.x + 1) * chunks_total / gridDim.x;
+#else
   const long long rows_total = (long long)p.batch * p.h;
-  const long long r_begin = (long long)blockIdx.x * rows_total / gridDim.x;
-  const long long r_end = (long long)(blockIdx.x + 1) * rows_total / gridDim.x;
+  const long long g_begin = (long long)blockIdx.x * rows_total / gridDim.x * cpr;
+  const long long g_end = (long long)(blockIdx.x + 1) * rows_total / gridDim.x * cpr;
+#endif
+  const long long r_begin = g_begin / cpr;
+  const long long r_end = (g_end + cpr - 1) / cpr;
+  const int k_first = (int)(g_begin - r_begin * cpr);
+  const int k_last = (int)(g_end - (r_end - 1) * cpr);  // exclusive, in the last row
   const long long pl = p.pl_in, opl = p.pl_out;  // plane strides (floats)
   const long long plane_len = (long long)p.h * p.w;
   const bool vec_ok = ((p.w & 3) == 0) && ((pl & 3) == 0) && ((opl & 3) == 0) &&
@@ -357,11 +380,23 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
 
+    // chunk range [klo, khi) of row y of this segment; the warp takes
+    // klo + warp, klo + warp + NW, ...
+    const long long rb0 = (long long)b * p.h;
+    auto klo = [&](int y) { return rb0 + y == r_begin ? k_first : 0; };
+    auto khi = [&](int y) { return rb0 + y == r_end - 1 ? k_last : cpr; };
+    // move (y, k) forward to this warp's next chunk (y > y_last: none left)
+    auto settle = [&](int& y, int& k) {
+      while (y <= y_last && k >= khi(y)) {
+        ++y;
+        k = y <= y_last ? klo(y) + warp : 0;
+      }
+    };
     // the first chunk's loads overlap the table copy
-    const int cpr = (p.w + CH - 1) / CH;
     ChunkIn<PX> cur;
-    int cur_y = y_first, cur_k = warp;
-    if (cur_k < cpr) load_chunk<PX>(plane0, pl, cur_y, cur_k * CH, p.w, lane, vec_ok, cur);
+    int cur_y = y_first, cur_k = klo(y_first) + warp;
+    settle(cur_y, cur_k);
+    if (cur_y <= y_last) load_chunk<PX>(plane0, pl, cur_y, cur_k * CH, p.w, lane, vec_ok, cur);
     mbar_wait(bar, phase);
     phase ^= 1u;
     // This warp's share of the slots of row y (CTA row ordinal n) into ring
@@ -394,15 +429,13 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       mbar_wait(full0 + 8u * (n % kRing), (n / kRing) & 1u);
       const uint32_t slotK = slotK0 + (n % kRing) * slot_row_bytes;
       // ---- this warp's chunks of row y: k = warp, warp + W, ... ----
-      for (; cur_y == y && cur_k < cpr;) {
+      for (; cur_y == y;) {
         ChunkIn<PX> nxt;
         int nxt_y = cur_y, nxt_k = cur_k + NW;
-        if (nxt_k >= cpr) {
-          nxt_k = warp;
-          ++nxt_y;
-        }
-        if (nxt_y <= y_last && nxt_k < cpr)
-          load_chunk<PX>(plane0, pl, nxt_y, nxt_k * CH, p.w, lane, vec_ok, nxt);
+        settle(nxt_y, nxt_k);
+#if FWD_REGPF
+        if (nxt_y <= y_last) load_chunk<PX>(plane0, pl, nxt_y, nxt_k * CH, p.w, lane, vec_ok, nxt);
+#endif
 
         const int xl = cur_k * CH + PX * lane;
         int jxs[PX];
@@ -463,28 +496,31 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           const uint32_t br = cbracket(qr, tdm1, tdm2, dr);
           const uint32_t bg = cbracket(qg, tdm1, tdm2, dg_);
           const uint32_t bb = cbracket(qb, tdm1, tdm2, db_);
-          const uint32_t ur = br * cst48 + lutK;
-          float2 acc01;
-          float acc2;
-          {  // pair rg (shared memory)
-            const uint32_t ad = ur + bg * 48u;
-            cell_term<true>(lds4(ad), lds4(ad + 16), lds4(ad + 32), dr, dg_, acc01, acc2);
-          }
-          {  // pair rb (shared memory)
-            const uint32_t ad = ur + bb * 48u + pair_bytes;
-            cell_term<false>(lds4(ad), lds4(ad + 16), lds4(ad + 32), dr, db_, acc01, acc2);
-          }
-          cell_term<false>(c0, c1, c2, dg, db, acc01, acc2);  // pair gb (texture path)
-          // grids: one merged (xy + xc + yc) coefficient cell per channel
           float er, eg, eb;
           const uint32_t sr = cbracket(qr, sdm1, sdm2, er);
           const uint32_t sg = cbracket(qg, sdm1, sdm2, eg);
           const uint32_t sb = cbracket(qb, sdm1, sdm2, eb);
-          const float ex = exs[u];
+          const uint32_t ur = br * cst48 + lutK;
+          const uint32_t ag = ur + bg * 48u, ab = ur + bb * 48u + pair_bytes;
           const uint32_t sa = slotK + (uint32_t)jxs[u] * jx_bytes;
-          o0[u] = acc01.x + slot_term(lds4(sa + sr * 16u), ex, er);
-          o1[u] = acc01.y + slot_term(lds4(sa + chan_bytes + sg * 16u), ex, eg);
-          o2[u] = acc2 + slot_term(lds4(sa + 2u * chan_bytes + sb * 16u), ex, eb);
+          // every shared-memory gather of the pixel back to back (lds4 is
+          // volatile, so program order is issue order): nine LDS.128 in
+          // flight per warp instead of one cell's three at a time
+          const float4 rg0 = lds4(ag), rg1 = lds4(ag + 16), rg2 = lds4(ag + 32);
+          const float4 rb0 = lds4(ab), rb1 = lds4(ab + 16), rb2 = lds4(ab + 32);
+          const float4 s0 = lds4(sa + sr * 16u);
+          const float4 s1 = lds4(sa + chan_bytes + sg * 16u);
+          const float4 s2 = lds4(sa + 2u * chan_bytes + sb * 16u);
+          float2 acc01;
+          float acc2;
+          cell_term<true>(rg0, rg1, rg2, dr, dg_, acc01, acc2);    // pair rg (shared memory)
+          cell_term<false>(rb0, rb1, rb2, dr, db_, acc01, acc2);   // pair rb (shared memory)
+          cell_term<false>(c0, c1, c2, dg, db, acc01, acc2);       // pair gb (texture path)
+          // grids: one merged (xy + xc + yc) coefficient cell per channel
+          const float ex = exs[u];
+          o0[u] = acc01.x + slot_term(s0, ex, er);
+          o1[u] = acc01.y + slot_term(s1, ex, eg);
+          o2[u] = acc2 + slot_term(s2, ex, eb);
           if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
         }
         const long long rowoff = (long long)cur_y * p.w;
@@ -502,7 +538,11 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
             }
           }
         }
+#if FWD_REGPF
         cur = nxt;
+#else
+        if (nxt_y <= y_last) load_chunk<PX>(plane0, pl, nxt_y, nxt_k * CH, p.w, lane, vec_ok, cur);
+#endif
         cur_y = nxt_y;
         cur_k = nxt_k;
       }
@@ -723,7 +763,8 @@ cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int
   cudaError_t e = tex_for(dev, reinterpret_cast<const void*>(base), bytes, st, &p.tex);
   if (e != cudaSuccess) return e;
   long long grid = g_num_sms;
-  if (grid > rows) grid = rows;
+  const long long chunks = rows * ((w + kChunk - 1) / kChunk);
+  if (grid > chunks) grid = chunks;
   size_t smem = fwd_smem_bytes(L.dt, L.ds);
   const size_t col_bytes = (size_t)((w + 3) & ~3) * 4;
   p.col_smem = smem + col_bytes <= kSmemForL1Tex ? 1 : 0;
