@@ -30,6 +30,23 @@ constexpr int kBwdWarps = 15;
 constexpr int kBPx = 4;
 constexpr int kBChunk = 32 * kBPx;
 constexpr uint32_t kMagic = 0x4B000000u;
+constexpr int kBwdL2Rows = 2;  // rows of L2 prefetch distance (X and gY planes)
+
+// Bulk L2 prefetch of row y of three planes (16-byte aligned cover, clipped
+// to each plane), no completion tracking.
+__device__ __forceinline__ void bprefetch_row(const float* plane0, long long pl, int y, int w) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float* pc = plane0 + c * pl;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(pc + (long long)y * w) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(pc + (long long)(y + 1) * w) + 15) & ~(uintptr_t)15;
+    const uintptr_t end = reinterpret_cast<uintptr_t>(pc + pl) & ~(uintptr_t)15;
+    const uintptr_t top = hi < end ? hi : end;
+    if (top > lo)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(top - lo))
+                   : "memory");
+  }
+}
 
 // Global accumulator layout per image (floats): lut [p 3][i d_t][j d_t][c 3],
 // grid [q 3 (xy|xc|yc)][c 3][a d_s][b d_s], then gsum [4].
@@ -123,27 +140,6 @@ __device__ __forceinline__ void grid_flush(int key, const float (&v)[8], int c, 
   atomicAdd(yc + 1, to_fixed(v[6], S)); atomicAdd(yc + ds + 1, to_fixed(v[7], S));
 }
 
-// Warp-uniform loop over the distinct keys held by active lanes: each round
-// sums the matching lanes' values with full-mask REDUX and one lane issues the
-// atomics through `emit(key, sums)`.
-template <int V, typename F>
-__device__ __forceinline__ void warp_key_flush(bool active, int key, const float (&v)[V], float S,
-                                               F emit) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  unsigned todo = __ballot_sync(full, active);
-  while (todo) {
-    const int src = __ffs(todo) - 1;
-    const int k = __shfl_sync(full, key, src);
-    const bool m = active && key == k;
-    int sum[V];
-#pragma unroll
-    for (int i = 0; i < V; ++i) sum[i] = __reduce_add_sync(full, m ? to_fixed(v[i], S) : 0);
-    if (lane == src) emit(k, sum);
-    todo &= ~__ballot_sync(full, m);
-  }
-}
-
 // Merged grid coefficients of channel c at (row jy/ey, x-cell jx, guide cell jc).
 __device__ __forceinline__ float4 bgrid_entry(const float* sm, const TableLayout& L, int c, int jx,
                                               int jc, int jy, float ey) {
@@ -229,7 +225,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const long long pl = (long long)p.h * p.w;
   const bool vec = ((p.w & 3) == 0) &&
                    (((uintptr_t)p.rgb | (uintptr_t)p.gy | (uintptr_t)p.gx) & 15) == 0;
-  const int cpr = (p.w + kBChunk - 1) / kBChunk;
   uint32_t phase = 0;
 
   long long r = r_begin;
@@ -263,9 +258,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     float* GX = p.gx ? p.gx + (long long)b * 3 * pl : nullptr;
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagic * (cst3 + 3u);
-    BChunk cur;
-    int cur_y = y_first, cur_k = warp;
-    if (cur_k < cpr) bload_chunk(X, GY, pl, cur_y, cur_k * kBChunk, p.w, lane, vec, cur);
     asm volatile(
         "{\n.reg .pred p;\nWAITB_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAITB_%=;\n}\n" ::"r"(bar),
         "r"(phase)
@@ -285,19 +277,28 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
 
     for (int y = y_first; y <= y_last; ++y) {
       const int buf = (y - y_first) & 1;
+      if (threadIdx.x == blockDim.x - 32) {
+        for (int yy = (y == y_first ? y + 1 : y + kBwdL2Rows); yy <= y + kBwdL2Rows && yy <= y_last; ++yy) {
+          bprefetch_row(X, pl, yy, p.w);
+          bprefetch_row(GY, pl, yy, p.w);
+        }
+      }
       float ey;
       const int jy = (int)(row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey) - kMagic);
       const uint32_t slotK = slotK0 + (uint32_t)buf * slot_row_bytes;
-      for (; cur_y == y && cur_k < cpr;) {
-        BChunk nxt;
-        int nxt_y = cur_y, nxt_k = cur_k + kBwdWarps;
-        if (nxt_k >= cpr) {
-          nxt_k = warp;
-          ++nxt_y;
-        }
-        if (nxt_y <= y_last && nxt_k < cpr)
-          bload_chunk(X, GY, pl, nxt_y, nxt_k * kBChunk, p.w, lane, vec, nxt);
-        const int xl = cur_k * kBChunk + 4 * lane;
+      // Spread lane mapping: the CTA walks the row in 4-pixel slots; lane l of
+      // warp w takes slot s0 + l * kBwdWarps + w, so the 32 lanes of one warp
+      // instruction sit kBwdWarps * 4 = 60 px apart.  On smooth images that
+      // makes their LUT cells (and so the shared atomics' addresses) nearly
+      // independent; with neighbouring lanes 4 px apart a warp instruction had
+      // ~10 lanes on the same address, which ATOMS serializes (measured cost:
+      // max lanes per bank, same-address lanes not merged).
+      const int slots4 = (p.w + 3) >> 2;
+      for (int s0 = 0; s0 < slots4; s0 += kBwdWarps * 32) {
+        const int xl = 4 * (s0 + lane * kBwdWarps + warp);
+        if (xl >= p.w) continue;
+        BChunk cur;
+        bload_chunk(X, GY, pl, y, xl - 4 * lane, p.w, lane, vec, cur);
         float oxr[kBPx], oxg[kBPx], oxb[kBPx];
         // xy accumulators of this lane for the x-cell of its first pixel
         float exy = 0.f;
@@ -425,30 +426,22 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
             }
           }
         }
-        // ---- end of chunk: the open grid runs and the xy sums, by distinct key ----
+        // ---- end of the lane's 4 pixels: open grid runs and the xy sums ----
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          warp_key_flush<8>(run_key[c] >= 0, run_key[c], run[c], S, [&](int key, const int* sum) {
-            const int jx = key >> 8, jc = key & 0xff;
-            int* xc = E_xc + c * ds * ds + jx * ds + jc;
-            atomicAdd(xc, sum[0]); atomicAdd(xc + ds, sum[1]);
-            atomicAdd(xc + 1, sum[2]); atomicAdd(xc + ds + 1, sum[3]);
-            int* yc = E_yc + c * ds * ds + jy * ds + jc;
-            atomicAdd(yc, sum[4]); atomicAdd(yc + ds, sum[5]);
-            atomicAdd(yc + 1, sum[6]); atomicAdd(yc + ds + 1, sum[7]);
-          });
-          run_key[c] = -1;
-        }
-        warp_key_flush<12>(xl < p.w, jx_first, axy, S, [&](int key, const int* sum) {
+        for (int c = 0; c < 3; ++c)
+          if (run_key[c] >= 0) grid_flush(run_key[c], run[c], c, jy, ds, S, E_xc, E_yc);
+        {
+          int* e = E_xy + jx_first * ds + jy;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            int* e = E_xy + c * ds * ds + key * ds + jy;
-            atomicAdd(e, sum[c]); atomicAdd(e + ds, sum[3 + c]);
-            atomicAdd(e + 1, sum[6 + c]); atomicAdd(e + ds + 1, sum[9 + c]);
+            atomicAdd(e + c * ds * ds, to_fixed(axy[c], S));
+            atomicAdd(e + c * ds * ds + ds, to_fixed(axy[3 + c], S));
+            atomicAdd(e + c * ds * ds + 1, to_fixed(axy[6 + c], S));
+            atomicAdd(e + c * ds * ds + ds + 1, to_fixed(axy[9 + c], S));
           }
-        });
+        }
         if (GX) {
-          const long long ro = (long long)cur_y * p.w;
+          const long long ro = (long long)y * p.w;
           if (vec && xl + 4 <= p.w) {
             __stcs(reinterpret_cast<float4*>(GX + ro + xl), make_float4(oxr[0], oxr[1], oxr[2], oxr[3]));
             __stcs(reinterpret_cast<float4*>(GX + pl + ro + xl), make_float4(oxg[0], oxg[1], oxg[2], oxg[3]));
@@ -463,9 +456,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               }
           }
         }
-        cur = nxt;
-        cur_y = nxt_y;
-        cur_k = nxt_k;
       }
       if (y < y_last) {
         float ey1;
