@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="BASELINE.json config (2 = headline; 3 batched 16x4K per-image shards, "
+                         "4 8K row strips, 5 training step on 8x1080p)")
     return ap.parse_args()
 
 
@@ -178,6 +181,8 @@ def main():
     a = parse()
     if a.impl == "reference":
         return run_reference_arm(a)
+    if a.config != 2:
+        return run_secondary(a)
     import torch
 
     rank, world, local = dist_env()
@@ -350,6 +355,125 @@ def main():
             "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": 2 * a.steps, "clocks": sampler.summary(),
             "launch": "cuda graphs of 4 steps" if step_graphs else "eager",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+# --------------------------------------------------------------------------- configs 3-5
+def run_secondary(a):
+    """BASELINE.json configs 3 (16 x 4K, per-image shards), 4 (one 8K image in
+    row strips with (y0, H_total)) and 5 (training step: forward + L2 loss
+    against X^0.8 + backward on 8 x 1080p, per-image shards).  Same timing
+    rules as the headline: W warm-up steps, K steps between barriers, CUDA
+    events on the launching stream, max over ranks; inputs >> L2."""
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+    import __graft_entry__
+
+    __graft_entry__.build_library()
+    from paper_2508_16121_b200 import device, parallel, synth
+
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    keys = ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")
+    if a.config == 3:
+        n_img = 16
+        lo, hi = parallel.image_block(n_img, world, rank)
+        case = synth.make_batch(list(range(lo, hi)))
+        h, w, units = 2160, 3840, (hi - lo)
+        desc = (f"config3: 16 x 3x2160x3840 fp32 smooth fields, per-image shards "
+                f"({hi - lo} per rank), own tables per image")
+    elif a.config == 4:
+        full = synth.make_case(0, h=4320, w=7680)
+        y0, y1 = parallel.strip_rows(4320, world, rank)
+        case = synth.Case(full.rgb[None, :, y0:y1].copy(), *(getattr(full, k)[None] for k in keys))
+        h, w, units = y1 - y0, 7680, 1
+        desc = f"config4: one 3x4320x7680 fp32 image, row strip {y0}:{y1} per rank, (y0, H_total)"
+    else:
+        n_img = 8
+        lo, hi = parallel.image_block(n_img, world, rank)
+        case = synth.make_batch(list(range(lo, hi)), h=1080, w=1920)
+        h, w, units = 1080, 1920, (hi - lo)
+        desc = (f"config5: training step on 8 x 3x1080x1920 (per-image shards, {hi - lo} per rank): "
+                f"forward + L2 loss vs X^0.8 + backward (gX, dU/dS/dVt, grids, weights)")
+    rgb = T(case.rgb)
+    prm = {k: T(getattr(case, k)) for k in keys}
+    y0_strip = parallel.strip_rows(4320, world, rank)[0] if a.config == 4 else 0
+    h_total = 4320 if a.config == 4 else h
+    out = torch.empty_like(rgb)
+    target = rgb.clamp_min(0) ** 0.8 if a.config == 5 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if a.config != 5:
+            tables = device.pack_tables_factors(prm["u"], prm["s"], prm["vt"], prm["lw"], prm["lb"],
+                                                prm["grid_planes"], prm["gw"], prm["gb"])
+            device.apply(rgb, tables, out=out, y0=y0_strip, h_total=h_total)
+            return
+        planes = device.reconstruct(prm["u"], prm["s"], prm["vt"])
+        tables = device.pack_tables(planes, prm["lw"], prm["lb"], prm["grid_planes"], prm["gw"],
+                                    prm["gb"])
+        y = device.apply(rgb, tables, out=out)
+        gy = (y - target).mul_(2.0 / y.numel())
+        g = device.fused_backward(rgb, gy, planes, prm["lw"], prm["grid_planes"], prm["gw"])
+        device.reconstruct_backward(prm["u"], prm["s"], prm["vt"], g["dlut_planes"])
+
+    graph = None
+    if not a.no_graph:
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+            step()
+    run = graph.replay if graph is not None else step
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, a.warmup)):
+        run()
+    barrier()
+    sampler = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for _ in range(a.steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    total_px = {3: 16 * 2160 * 3840, 4: 4320 * 7680, 5: 8 * 1080 * 1920}[a.config]
+    bpp = 60 if a.config == 5 else BYTES_PER_PX
+    if rank == 0:
+        line = {
+            "metric": ("megapixels/sec training step (fwd + L2 loss + bwd) at 1080p fp32"
+                       if a.config == 5 else METRIC + (" (batched 16)" if a.config == 3 else " (8K strips)")),
+            "value": round(total_px / (ms * 1e-3) / 1e6, 3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "strong" if a.config == 4 else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded smooth fields, SURVEY.md §8d)",
+            "config": {"workload": desc, "global_batch": {3: 16, 4: 1, 5: 8}[a.config], "height": h_total,
+                       "width": w, "parallelism": f"dp{world}",
+                       "l2": "inputs >> L2 (no reuse between steps)"},
+            "algorithmic_bytes_per_px": bpp,
+            "achieved_gbs": round(bpp * total_px / (ms * 1e-3) / 1e9, 1),
+            "gpu_launches": None, "clocks": sampler.summary(),
+            "launch": "cuda graph per step" if graph is not None else "eager",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

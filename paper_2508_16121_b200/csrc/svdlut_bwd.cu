@@ -119,9 +119,10 @@ __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, floa
 //   grids per-lane runs over the lane's 4 consecutive pixels, then one loop
 //         over the distinct keys of the warp with full-mask REDUX sums.
 // Shared sums are flushed to the global f32 accumulators at least every
-// kFlushPx pixels: every shared partial stays below (kFlushPx + W) * 2^16 < 2^31
-// for rows up to 24K pixels wide.
-constexpr int kFlushPx = 8192;
+// row that could take one partial past 2^31: every shared partial is a sum
+// of at most one contribution (|v| <= 2^16) per pixel, so at most
+// kMaxFlushPx pixels may accumulate between flushes (rows <= kMaxFlushPx px).
+constexpr int kMaxFlushPx = 32767;
 constexpr float kFixedOne = 65536.0f;
 __device__ __forceinline__ int to_fixed(float v, float S) {
   return __float_as_int(__fmaf_rn(v, S, 12582912.0f)) - 0x4B400000;
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       }
       __syncthreads();
       px_since_flush += p.w;
-      if (px_since_flush >= kFlushPx && y < y_last) {  // keep shared partials < 2^31
+      if (px_since_flush + p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
         for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
           const int v = Ei[i];
           if (v != 0) {

@@ -264,6 +264,8 @@ int svdlut_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w,
   if ((rc = check_k(k)) != SVDLUT_OK) return rc;
   if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
   if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
+  if (w > 32767)
+    return fail(SVDLUT_ERR_UNSUPPORTED, "backward rows are limited to 32767 pixels (got %d)", w);
   if (batch == 0) return SVDLUT_OK;
   if (!rgb || !gy || !lut_planes || !lw || !grid_planes || !gw || !dlut_planes || !dlw || !dlb ||
       !dgrid_planes || !dgw || !dgb)
