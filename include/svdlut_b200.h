@@ -14,6 +14,7 @@
  *   svdlut_indices            per-pixel cell selection (interp.py:35-45,
  *                             transform.py:144-149) for the bit-exact index test
  *   svdlut_enhance_host       host-buffer entry (H2D + apply + D2H pipelined)
+ *   svdlut_reconstruct_host   host-buffer svd.reconstruct_lut (svd.py:210-220)
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  `stream` is a
@@ -156,7 +157,8 @@ svdlut_ctx* svdlut_ctx_create(int device);
 void svdlut_ctx_destroy(svdlut_ctx* ctx);
 
 /* One image from HOST memory to HOST memory: H2D of rgb + tables, pack,
- * apply, D2H of out, pipelined over row strips on two streams.  Host buffers
+ * apply, D2H of out, pipelined over row strips on three streams (copy-in,
+ * compute, copy-out).  Host buffers
  * may be pinned (DMA directly) or pageable (staged).  Blocks until `out` is
  * written.  exact != 0 selects the f64 kernel.  *nonfinite (optional) is set
  * to 1 if any output sample is NaN/Inf. */
@@ -164,6 +166,13 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
                         const float* lut_planes, const float* lw, const float* lb, int d_t,
                         const float* grid_planes, const float* gw, const float* gb, int k,
                         int d_s, float* out, int exact, int* nonfinite);
+
+/* reconstruct_lut (svd.py:210-220) from HOST factors to HOST planes: one H2D
+ * of (u, s, vt) through the context's pinned staging, svdlut_reconstruct,
+ * one D2H.  Shapes as svdlut_reconstruct with B = batch.  Blocks until
+ * `planes` is written. */
+int svdlut_reconstruct_host(svdlut_ctx* ctx, const float* u, const float* s, const float* vt,
+                            int batch, int d_t, int n_s, float* planes);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,7 @@ _SIGS = {
     "svdlut_ctx_destroy": (None, [_vp]),
     "svdlut_enhance_host": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _vp,
                                  _i, ctypes.POINTER(_i)]),
+    "svdlut_reconstruct_host": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp]),
 }
 
 EXPORTS = tuple(_SIGS)

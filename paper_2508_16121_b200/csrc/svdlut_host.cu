@@ -6,6 +6,7 @@
 // strip after strip, the D2H engine follows one strip behind and the kernels
 // run in between (strips are independent thanks to the (y0, h_total)
 // contract).  The step is then bound by the PCIe copies alone.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -34,6 +35,8 @@ struct svdlut_ctx {
   void* d_par = nullptr;  // parameters + packed tables + workspaces
   size_t d_par_bytes = 0;
   int* h_flag = nullptr;  // pinned flag readback
+  float* h_stage = nullptr;  // pinned staging for small host transfers
+  size_t h_stage_bytes = 0;
   std::mutex mu;
 };
 
@@ -86,6 +89,7 @@ void svdlut_ctx_destroy(svdlut_ctx* c) {
   if (c->d_img) cudaFree(c->d_img);
   if (c->d_par) cudaFree(c->d_par);
   if (c->h_flag) cudaFreeHost(c->h_flag);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   for (int i = 0; i < 3; ++i)
     if (c->st[i]) cudaStreamDestroy(c->st[i]);
   for (int i = 0; i < kMaxStrips; ++i) {
@@ -143,22 +147,42 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   }
 
   // ---- strip pipeline: H2D (s_in) -> kernel (s_k) -> D2H (s_out) ------------
-  // ~12 MB strips at 4K (8 strips): every copy has a fixed setup cost of
-  // several microseconds, so fewer, larger copies win until the pipeline
-  // fill (first H2D) and drain (last D2H) start to dominate.
+  // ~12 MB strips at 4K: every copy has a fixed setup cost of several
+  // microseconds, so fewer, larger copies win; the first and the last strip
+  // are a quarter of that, because the pipeline fill (first H2D) and drain
+  // (last D2H) run one PCIe direction alone.
   const size_t plane = (size_t)h * w;
-  const size_t img_b = 3 * plane * 4;
   static const size_t strip_b = [] {
     const char* e = getenv("SVDLUT_STRIP_KB");  // development knob
     const long v = e ? atol(e) : 0;
     return v > 0 ? (size_t)v << 10 : (size_t)12 << 20;
   }();
-  int n_strips = (int)((img_b + strip_b - 1) / strip_b);
-  if (n_strips > kMaxStrips) n_strips = kMaxStrips;
-  if (n_strips > h) n_strips = h;
-  if (n_strips < 1) n_strips = 1;
+  int bounds[kMaxStrips + 1];
+  int n_strips = 0;
+  {
+    const int unit = (int)std::max<size_t>(1, strip_b / ((size_t)3 * w * 4));  // rows per strip
+    const int edge = std::max(1, unit / 4);
+    bounds[0] = 0;
+    if (h <= 2 * edge + unit) {
+      bounds[n_strips = 1] = h;
+    } else {
+      const int mid = h - 2 * edge;
+      const int n_mid = std::min(kMaxStrips - 2, (mid + unit - 1) / unit);
+      bounds[++n_strips] = edge;
+      for (int i = 1; i <= n_mid; ++i) bounds[++n_strips] = edge + (int)((long long)mid * i / n_mid);
+      bounds[++n_strips] = h;
+    }
+  }
+  // SVDLUT_TRACE=1 (development): per-strip H2D / kernel / D2H completion
+  // times relative to the start of the call, printed to stderr
+  static const bool trace = getenv("SVDLUT_TRACE") != nullptr;
+  cudaEvent_t tev[3 * kMaxStrips + 1];
+  if (trace) {
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[3 * kMaxStrips], s_k);
+  }
   for (int s = 0; s < n_strips; ++s) {
-    const int r0 = (int)((long long)h * s / n_strips), r1 = (int)((long long)h * (s + 1) / n_strips);
+    const int r0 = bounds[s], r1 = bounds[s + 1];
     const int hs = r1 - r0;
     float* din = d_in + (size_t)3 * r0 * w;    // strip-major device layout (3, hs, w)
     float* dout = d_out + (size_t)3 * r0 * w;
@@ -166,6 +190,7 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
     if (cudaMemcpy2DAsync(din, (size_t)hs * w * 4, rgb + (size_t)r0 * w, plane * 4,
                           (size_t)hs * w * 4, 3, cudaMemcpyHostToDevice, s_in) != cudaSuccess)
       return SVDLUT_ERR_CUDA;
+    if (trace) cudaEventRecord(tev[3 * s], s_in);
     if (cudaEventRecord(ctx->ev_in[s], s_in) != cudaSuccess) return SVDLUT_ERR_CUDA;
     if (cudaStreamWaitEvent(s_k, ctx->ev_in[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
     int rc;
@@ -177,17 +202,68 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
                                   k, d_s, dout, s_k);
     }
     if (rc != SVDLUT_OK) return rc;
+    if (trace) cudaEventRecord(tev[3 * s + 1], s_k);
     if (cudaEventRecord(ctx->ev_k[s], s_k) != cudaSuccess) return SVDLUT_ERR_CUDA;
     if (cudaStreamWaitEvent(s_out, ctx->ev_k[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
     if (cudaMemcpy2DAsync(out + (size_t)r0 * w, plane * 4, dout, (size_t)hs * w * 4,
                           (size_t)hs * w * 4, 3, cudaMemcpyDeviceToHost, s_out) != cudaSuccess)
       return SVDLUT_ERR_CUDA;
+    if (trace) cudaEventRecord(tev[3 * s + 2], s_out);
+  }
+  if (trace) {
+    cudaStreamSynchronize(s_out);
+    for (int s = 0; s < n_strips; ++s) {
+      float t[3];
+      for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], tev[3 * kMaxStrips], tev[3 * s + i]);
+      fprintf(stderr, "strip %2d  h2d done %7.3f  kernel done %7.3f  d2h done %7.3f ms\n", s, t[0], t[1], t[2]);
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
   }
   // the last kernel's event already orders every flag write before s_out
   if (cudaMemcpyAsync(ctx->h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s_out) != cudaSuccess)
     return SVDLUT_ERR_CUDA;
   if (cudaStreamSynchronize(s_out) != cudaSuccess) return SVDLUT_ERR_CUDA;
   if (nonfinite) *nonfinite = fast ? *ctx->h_flag : 0;
+  return SVDLUT_OK;
+}
+
+int svdlut_reconstruct_host(svdlut_ctx* ctx, const float* u, const float* s, const float* vt,
+                            int batch, int d_t, int n_s, float* planes) {
+  if (!ctx || !u || !s || !vt || !planes) return SVDLUT_ERR_INVALID_ARGUMENT;
+  if (batch < 0) return SVDLUT_ERR_DIMENSION_MISMATCH;
+  if (d_t < 2) return SVDLUT_ERR_BAD_VERTEX_COUNT;
+  if (n_s < 1 || n_s > d_t) return SVDLUT_ERR_DIMENSION_MISMATCH;
+  if (batch == 0) return SVDLUT_OK;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  const size_t nu = (size_t)batch * 9 * d_t * n_s, ns = (size_t)batch * 9 * n_s;
+  const size_t np = (size_t)batch * 9 * d_t * d_t;
+  const size_t in_f = 2 * nu + ns, stage_f = in_f > np ? in_f : np;
+  if (ctx->h_stage_bytes < stage_f * 4) {
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->h_stage_bytes = 0;
+    if (cudaHostAlloc((void**)&ctx->h_stage, stage_f * 4, cudaHostAllocDefault) != cudaSuccess)
+      return SVDLUT_ERR_CUDA;
+    ctx->h_stage_bytes = stage_f * 4;
+  }
+  if (ensure(&ctx->d_par, &ctx->d_par_bytes, rup(in_f * 4) + rup(np * 4)) != cudaSuccess)
+    return SVDLUT_ERR_CUDA;
+  float* st = ctx->h_stage;
+  memcpy(st, u, nu * 4);
+  memcpy(st + nu, s, ns * 4);
+  memcpy(st + nu + ns, vt, nu * 4);
+  float* d_in = (float*)ctx->d_par;
+  float* d_planes = (float*)((char*)ctx->d_par + rup(in_f * 4));
+  cudaStream_t sk = ctx->st[1];
+  if (cudaMemcpyAsync(d_in, st, in_f * 4, cudaMemcpyHostToDevice, sk) != cudaSuccess)
+    return SVDLUT_ERR_CUDA;
+  const int rc = svdlut_reconstruct(d_in, d_in + nu, d_in + nu + ns, batch, d_t, n_s, d_planes, sk);
+  if (rc != SVDLUT_OK) return rc;
+  if (cudaMemcpyAsync(st, d_planes, np * 4, cudaMemcpyDeviceToHost, sk) != cudaSuccess)
+    return SVDLUT_ERR_CUDA;
+  if (cudaStreamSynchronize(sk) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  memcpy(planes, st, np * 4);
   return SVDLUT_OK;
 }
 
