@@ -10,6 +10,9 @@ Patched names (the reference's own call sites):
   svdlut.transform.fused_enhance   transform.py:308   (tests import it by name)
   svdlut.network.fused_enhance     network.py:42      (bound at import by run_model)
   svdlut.svd.reconstruct_lut       svd.py:210         (called via module attribute)
+  svdlut.network.run_model         network.py:179     (only with generator=True: the
+                                                      backbone and heads run on the
+                                                      GPU too, network.py here)
 
 The wrappers keep the reference signatures, allocate the output raster
 through ``svdlut.transform._alloc_raster`` (so ``_raster_hook`` observes exactly
@@ -49,8 +52,11 @@ def _translate(ref_errors):
     return deco
 
 
-def install(package="svdlut", exact=False):
-    """Patch the reference package in place; returns a Handle to undo it."""
+def install(package="svdlut", exact=False, generator=False):
+    """Patch the reference package in place; returns a Handle to undo it.
+
+    generator=True also routes ``network.run_model`` through the GPU generator
+    path (resize + backbone + heads in PyTorch on device, then pack + apply)."""
     ref = importlib.import_module(package)
     ref_transform = importlib.import_module(f"{package}.transform")
     ref_network = importlib.import_module(f"{package}.network")
@@ -69,10 +75,19 @@ def install(package="svdlut", exact=False):
     def reconstruct_lut(svdlut):
         return b200_svd.reconstruct_lut(svdlut)
 
+    from . import network as b200_network
+
+    @_translate(ref_errors)
+    def run_model(img, params, fused=True, threads=1):
+        return b200_network.run_model(img, params, fused=fused, threads=threads)
+
+    patches = [(ref_transform, "fused_enhance", fused_enhance),
+               (ref_network, "fused_enhance", fused_enhance),
+               (ref_svd, "reconstruct_lut", reconstruct_lut)]
+    if generator:
+        patches.append((ref_network, "run_model", run_model))
     saved = {}
-    for mod, name, fn in ((ref_transform, "fused_enhance", fused_enhance),
-                          (ref_network, "fused_enhance", fused_enhance),
-                          (ref_svd, "reconstruct_lut", reconstruct_lut)):
+    for mod, name, fn in patches:
         saved[(mod, name)] = getattr(mod, name)
         setattr(mod, name, fn)
     del ref

@@ -1,0 +1,130 @@
+"""Generator path (network.py): parameters, backbone and heads against the
+reference's own outputs (tests/golden/make_network_golden.py and the c1_*
+vectors of make_golden.py), then the full image-adaptive pipeline on the GPU.
+
+CPU tests run the same torch code on the CPU; the GPU tests run it on cuda:0
+(TF32 off) followed by the sm_100a pack + apply kernels."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+SMALL = dict(m=4, d_t=17, d_s=9, k=3, n_s=4, m_s=5, m_t=6, m_sw=3, m_tw=2)
+CTX_TOL = 1e-6     # context / head outputs (values ~0.05; observed ~1e-8)
+OUT_TOL = 1e-5     # end-to-end image (BASELINE north star)
+HEADS = [("u", "u"), ("s", "s"), ("vt", "vt"), ("lw", "lw"), ("lb", "lb"), ("grid_planes", "gp"),
+         ("gw", "gw"), ("gb", "gb")]
+
+
+@pytest.fixture(scope="module")
+def ngold():
+    return np.load(os.path.join(ROOT, "tests", "golden", "network_golden.npz"))
+
+
+def c1_input():
+    rng = np.random.default_rng(0)
+    return rng.random((3, 480, 720), dtype=np.float32)
+
+
+def sm_input():
+    rng = np.random.default_rng(7)
+    return rng.random((3, 200, 300), dtype=np.float32)
+
+
+@pytest.mark.parametrize("seed,tag", [(0, "default"), (3, "small")])
+def test_random_init_bit_identical_to_reference(ngold, seed, tag):
+    from paper_2508_16121_b200 import network
+
+    hp = network.HyperParams() if tag == "default" else network.HyperParams(**SMALL)
+    params = network.random_init(seed, hp)
+    h = hashlib.sha256()
+    for name in network.expected_shapes(hp):
+        h.update(params.tensors[name].tobytes())
+    assert h.hexdigest() == str(ngold[f"init_{seed}_{tag}_sha"])
+    assert network.param_count(hp) == sum(t.size for t in params.tensors.values())
+
+
+def test_hyperparameter_validation():
+    from paper_2508_16121_b200 import network
+    from paper_2508_16121_b200.errors import DimensionMismatch, InvalidArgument
+
+    for bad in (dict(m=0), dict(d_t=1), dict(k=4), dict(n_s=40), dict(m_t=0), dict(n_sw=2)):
+        with pytest.raises(InvalidArgument):
+            network.HyperParams(**bad)
+    p = network.random_init(0, network.HyperParams(**SMALL))
+    t = dict(p.tensors)
+    t.pop("lut_gen.fc2.bias")
+    with pytest.raises(DimensionMismatch):
+        network.ModelParams(p.hyper, t)
+
+
+def _check_generator(gen, rgb, gold, prefix):
+    import torch
+
+    ctx = gen.backbone(torch.from_numpy(rgb)[None].to(gen.device))
+    assert np.abs(ctx[0].cpu().numpy() - gold[f"{prefix}_ctx"]).max() <= CTX_TOL
+    heads = gen.heads(ctx)
+    for ours, theirs in HEADS:
+        assert np.abs(heads[ours][0].cpu().numpy() - gold[f"{prefix}_{theirs}"]).max() <= CTX_TOL
+
+
+def test_backbone_and_heads_cpu(golden, ngold):
+    """The torch restatement on the CPU reproduces the reference's context and
+    head outputs (default hyperparameters on 720x480 -> downsampling resize;
+    the small set on 300x200 -> upsampling rows)."""
+    from paper_2508_16121_b200 import network
+
+    _check_generator(network.Generator(network.random_init(0), "cpu"), c1_input(), golden, "c1")
+    _check_generator(network.Generator(network.random_init(3, network.HyperParams(**SMALL)), "cpu"),
+                     sm_input(), ngold, "sm")
+
+
+@pytest.mark.gpu
+def test_backbone_and_heads_gpu(golden, ngold):
+    import __graft_entry__
+    from paper_2508_16121_b200 import network
+
+    __graft_entry__.build_library()
+    _check_generator(network.Generator(network.random_init(0), "cuda"), c1_input(), golden, "c1")
+    _check_generator(network.Generator(network.random_init(3, network.HyperParams(**SMALL)), "cuda"),
+                     sm_input(), ngold, "sm")
+
+
+@pytest.mark.gpu
+def test_run_model_end_to_end_gpu(golden, ngold):
+    """Config 1: reference run_model(720x480, random_init(0)) reproduced by the
+    GPU generator + fused kernel within 1e-5 (and the small set likewise)."""
+    import __graft_entry__
+    from paper_2508_16121_b200 import network
+    from paper_2508_16121_b200.core_types import Image
+
+    __graft_entry__.build_library()
+    y = network.run_model(Image(720, 480, c1_input()), network.random_init(0))
+    assert np.abs(y.data[:, ::7, ::11] - golden["c1_out_sub"]).max() <= OUT_TOL
+    p_small = network.random_init(3, network.HyperParams(**SMALL))
+    y = network.run_model(Image(300, 200, sm_input()), p_small)
+    assert np.abs(y.data[:, ::3, ::5] - ngold["sm_out_sub"]).max() <= OUT_TOL
+
+
+@pytest.mark.gpu
+def test_batched_enhance_equals_per_image():
+    """Generator.enhance on a batch == per-image calls (each image gets its own
+    context, heads and tables; cuDNN may pick another algorithm per batch
+    size, so within the end-to-end tolerance rather than bitwise)."""
+    import torch
+
+    import __graft_entry__
+    from paper_2508_16121_b200 import network
+
+    __graft_entry__.build_library()
+    gen = network.Generator(network.random_init(1), "cuda")
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy(rng.random((3, 3, 96, 160), dtype=np.float32)).cuda()
+    yb = gen.enhance(x)
+    for i in range(3):
+        yi = gen.enhance(x[i:i + 1].contiguous())[0]
+        assert float((yb[i] - yi).abs().max()) <= OUT_TOL

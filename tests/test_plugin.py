@@ -95,3 +95,18 @@ def test_raster_hook_sees_exactly_the_output(ref):
         ref.transform._raster_hook = None
         h.uninstall()
     assert allocs == [(3, 24, 32)]
+
+
+def test_generator_option_patches_run_model(ref):
+    from paper_2508_16121_b200 import plugin
+
+    orig = ref.network.run_model
+    h = plugin.install()
+    assert ref.network.run_model is orig  # default: only the apply path
+    h.uninstall()
+    h = plugin.install(generator=True)
+    try:
+        assert ref.network.run_model is not orig
+    finally:
+        h.uninstall()
+    assert ref.network.run_model is orig
