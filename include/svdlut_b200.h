@@ -15,6 +15,10 @@
  *                             transform.py:144-149) for the bit-exact index test
  *   svdlut_enhance_host       host-buffer entry (H2D + apply + D2H pipelined)
  *   svdlut_reconstruct_host   host-buffer svd.reconstruct_lut (svd.py:210-220)
+ *   svdlut_fused_fwd_io       fused apply with PNM sample formats in/out:
+ *                             decode of pnm.load (pnm.py:72-80) and the
+ *                             quantization of pnm.save (pnm.py:83-108) fused
+ *   svdlut_enhance_host_io    host-buffer entry with the same formats
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  `stream` is a
@@ -111,6 +115,19 @@ int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0
                                size_t workspace_bytes, int* nonfinite, int variant, void* stream);
 
 /* Reference-shaped entry: pack + apply.  `workspace` >= svdlut_workspace_bytes. */
+/* Sample formats of the _io entry points.  F32: planar float32 (B,3,H,W).
+ * U8 / U16BE: PNM P6 payload order (B,H,W,3), uint8 (maxval 255) or
+ * big-endian uint16 (maxval 65535).  Integer input decodes as
+ * f32(f64(v) / maxval) (pnm.py:79); integer output quantizes as
+ * floor(clip(y, 0, 1) * maxval + 0.5) in exact arithmetic (pnm.py:83-86). */
+enum { SVDLUT_FMT_F32 = 0, SVDLUT_FMT_U8 = 1, SVDLUT_FMT_U16BE = 2 };
+
+/* As svdlut_fused_fwd_packed_ex with explicit sample formats (any pair).  Integer images need 4-byte (U8) / 8-byte
+ * (U16BE) aligned buffers for the vector path (any alignment works). */
+int svdlut_fused_fwd_io(const void* in, int in_fmt, int batch, int h, int w, int y0, int h_total,
+                        const void* tables, int d_t, int d_s, void* out, int out_fmt, int* nonfinite,
+                        void* stream);
+
 int svdlut_fused_fwd(const float* rgb, int batch, int h, int w, int y0, int h_total,
                      const float* lut_planes, const float* lw, const float* lb, int d_t,
                      const float* grid_planes, const float* gw, const float* gb, int k, int d_s,
@@ -166,6 +183,13 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
                         const float* lut_planes, const float* lw, const float* lb, int d_t,
                         const float* grid_planes, const float* gw, const float* gb, int k,
                         int d_s, float* out, int exact, int* nonfinite);
+
+/* svdlut_enhance_host with sample formats (fast kernel only): e.g. a PNM
+ * payload in, a PNM payload out — 6 B/pixel over PCIe instead of 24 (U8). */
+int svdlut_enhance_host_io(svdlut_ctx* ctx, const void* in, int in_fmt, int h, int w,
+                           const float* lut_planes, const float* lw, const float* lb, int d_t,
+                           const float* grid_planes, const float* gw, const float* gb, int k, int d_s,
+                           void* out, int out_fmt, int* nonfinite);
 
 /* reconstruct_lut (svd.py:210-220) from HOST factors to HOST planes: one H2D
  * of (u, s, vt) through the context's pinned staging, svdlut_reconstruct,

@@ -196,6 +196,26 @@ int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0
                                workspace_bytes, nonfinite, variant, (cudaStream_t)stream);
 }
 
+int svdlut_fused_fwd_io(const void* in, int in_fmt, int batch, int h, int w, int y0, int h_total,
+                        const void* tables, int d_t, int d_s, void* out, int out_fmt, int* nonfinite,
+                        void* stream) {
+  int rc;
+  if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
+  if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
+  if (!fused_fwd_formats_supported(in_fmt, out_fmt))
+    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "unsupported sample formats (in %d, out %d)", in_fmt, out_fmt);
+  if (!svdlut_fast_supported(d_t, d_s))
+    return fail(SVDLUT_ERR_UNSUPPORTED, "tables for d_t=%d d_s=%d exceed shared memory", d_t, d_s);
+  if ((long long)batch * h * w == 0) return SVDLUT_OK;
+  if (!in || !tables || !out) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
+  const TableLayout L = TableLayout::make(d_t, d_s);
+  CUDA_TRY(launch_fused_fwd_io(in, in_fmt, out, out_fmt, batch, h, w, y0, h_total, (const float*)tables,
+                               L, nonfinite, (cudaStream_t)stream),
+           "fused forward (sample formats)");
+  return SVDLUT_OK;
+}
+
 int svdlut_fused_fwd(const float* rgb, int batch, int h, int w, int y0, int h_total,
                      const float* lut_planes, const float* lw, const float* lb, int d_t,
                      const float* grid_planes, const float* gw, const float* gb, int k, int d_s,

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "svdlut_common.cuh"
+#include "svdlut_io.cuh"
 #include "svdlut_internal.h"
 
 namespace svdlut {
@@ -61,10 +62,10 @@ constexpr int kRing = 3;  // per-row grid slot buffers
 constexpr uint32_t kMagicBits = 0x4B000000u;  // bits of 2^23
 
 struct FwdParams {
-  const float* rgb;
-  float* out;
+  const void* in;           // input samples (format IN of the kernel)
+  void* out;                // output samples (format OUT)
   int batch, h, w;
-  long long pl_in, pl_out;  // plane strides in floats (h*w for packed images)
+  long long pl_in, pl_out;  // f32 plane strides in floats (h*w for packed images)
   int y0;                   // first row of this strip in an image of h_total rows
   const float* tables;
   TableLayout L;
@@ -94,24 +95,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
-// Bulk L2 prefetch of [p, p + bytes) (16 B granules), no completion tracking.
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-// Prefetches row y of the three input planes into L2 (16-byte aligned cover
-// of each plane's row, clipped to that plane).
-__device__ __forceinline__ void prefetch_row(const float* plane0, long long pl, long long plane_len,
-                                             int y, int w) {
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float* pc = plane0 + c * pl;
-    const uintptr_t lo = reinterpret_cast<uintptr_t>(pc + (long long)y * w) & ~(uintptr_t)15;
-    const uintptr_t hi = (reinterpret_cast<uintptr_t>(pc + (long long)(y + 1) * w) + 15) & ~(uintptr_t)15;
-    const uintptr_t end = reinterpret_cast<uintptr_t>(pc + plane_len) & ~(uintptr_t)15;
-    const uintptr_t top = hi < end ? hi : end;
-    if (top > lo) prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(top - lo));
-  }
-}
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -136,21 +119,6 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
 __device__ __forceinline__ float2 lds2(uint32_t a) {
   float2 v;
   asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-  return v;
-}
-
-// Streaming 128-bit load that does not allocate in L1 (keeps L1 for the
-// texture-path LUT pair).
-__device__ __forceinline__ float4 ldg_stream4(const float* p) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ float ldg_stream(const float* p) {
-  float v;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
 
@@ -192,53 +160,6 @@ struct ChunkIn {
   float r[PX], g[PX], b[PX];  // PX consecutive pixels per lane
 };
 
-template <int PX>
-__device__ __forceinline__ void ldg_stream_vec(const float* p, float* v) {
-  if (PX == 4) {
-    const float4 t = ldg_stream4(p);
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  } else if (PX == 2) {
-    float2 t;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(t.x), "=f"(t.y) : "l"(p));
-    v[0] = t.x; v[1] = t.y;
-  } else {
-    v[0] = ldg_stream(p);
-  }
-}
-
-template <int PX>
-__device__ __forceinline__ void stg_stream_vec(float* p, const float* v) {
-  if (PX == 4) {
-    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
-  } else if (PX == 2) {
-    __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
-  } else {
-    __stcs(p, v[0]);
-  }
-}
-
-// Lane owns pixels x0 + PX*lane + u (u < PX): vector loads when the row is
-// aligned, clamped scalar loads otherwise (and at the right edge).
-template <int PX>
-__device__ __forceinline__ void load_chunk(const float* plane0, long long pl, int y, int x0, int w,
-                                           int lane, bool vec_ok, ChunkIn<PX>& in) {
-  const long long rowoff = (long long)y * w;
-  const int x = x0 + PX * lane;
-  if (vec_ok && x + PX <= w) {
-    ldg_stream_vec<PX>(plane0 + rowoff + x, in.r);
-    ldg_stream_vec<PX>(plane0 + pl + rowoff + x, in.g);
-    ldg_stream_vec<PX>(plane0 + 2 * pl + rowoff + x, in.b);
-  } else {
-#pragma unroll
-    for (int u = 0; u < PX; ++u) {
-      const int xx = min(x + u, w - 1);
-      in.r[u] = ldg_stream(plane0 + rowoff + xx);
-      in.g[u] = ldg_stream(plane0 + pl + rowoff + xx);
-      in.b[u] = ldg_stream(plane0 + 2 * pl + rowoff + xx);
-    }
-  }
-}
-
 // Grid part of one image's tables (shared memory copy; slot builds / wide path).
 struct GridG {
   const float4* xc;   // [c][jx][jc] {A,B,C,D}
@@ -272,8 +193,9 @@ __host__ __device__ inline uint32_t smem_tables_bytes(const TableLayout& L) {
   return smem_grid_off(L) + (uint32_t)(L.lut2_off - L.xc_off) * 4u;
 }
 
-template <int DT, int DS, bool CHECK, int PX, int NW>
+template <int DT, int DS, bool CHECK, int PX, int NW, int IN, int OUT>
 __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
+  static_assert(PX == 4 || (IN == kF32 && OUT == kF32), "integer formats use 4-pixel lanes");
   constexpr int CH = 32 * PX;  // pixels per warp chunk
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar_storage;
@@ -349,8 +271,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const int k_last = (int)(g_end - (r_end - 1) * cpr);  // exclusive, in the last row
   const long long pl = p.pl_in, opl = p.pl_out;  // plane strides (floats)
   const long long plane_len = (long long)p.h * p.w;
-  const bool vec_ok = ((p.w & 3) == 0) && ((pl & 3) == 0) && ((opl & 3) == 0) &&
-                      ((reinterpret_cast<uintptr_t>(p.rgb) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0;
+  const bool vec_in = ((p.w & 3) == 0) && Src<IN>::aligned(p.in, pl);
+  const bool vec_out = ((p.w & 3) == 0) && Dst<OUT>::aligned(p.out, opl);
   uint32_t phase = 0;
   uint32_t nrow = 0;  // CTA row ordinal (slot ring position)
   bool bad = false;
@@ -374,8 +296,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       for (uint32_t off = 0; off < gbytes; off += 32768u)       // grid block
         bulk_g2s(sbase + lut_smem_bytes + off, gsrc + off, min(32768u, gbytes - off), bar);
     }
-    const float* plane0 = p.rgb + (long long)b * 3 * pl;
-    float* oplane0 = p.out + (long long)b * 3 * opl;
+    const void* src = Src<IN>::image(p.in, b, pl);
+    void* dst = Dst<OUT>::image(p.out, b, opl);
     // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
@@ -396,7 +318,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     ChunkIn<PX> cur;
     int cur_y = y_first, cur_k = klo(y_first) + warp;
     settle(cur_y, cur_k);
-    if (cur_y <= y_last) load_chunk<PX>(plane0, pl, cur_y, cur_k * CH, p.w, lane, vec_ok, cur);
+    if (cur_y <= y_last)
+      Src<IN>::template load<PX>(src, pl, cur_y, cur_k * CH + PX * lane, p.w, vec_in, cur.r, cur.g, cur.b);
     mbar_wait(bar, phase);
     phase ^= 1u;
     // This warp's share of the slots of row y (CTA row ordinal n) into ring
@@ -423,8 +346,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       const uint32_t n = n0 + (uint32_t)(y - y_first);
       if (FWD_L2PF > 0 && threadIdx.x == blockDim.x - 32) {
         if (y == y_first)
-          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) prefetch_row(plane0, pl, plane_len, yy, p.w);
-        if (y + FWD_L2PF <= y_last) prefetch_row(plane0, pl, plane_len, y + FWD_L2PF, p.w);
+          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) Src<IN>::prefetch_row(src, pl, plane_len, yy, p.w);
+        if (y + FWD_L2PF <= y_last) Src<IN>::prefetch_row(src, pl, plane_len, y + FWD_L2PF, p.w);
       }
       mbar_wait(full0 + 8u * (n % kRing), (n / kRing) & 1u);
       const uint32_t slotK = slotK0 + (n % kRing) * slot_row_bytes;
@@ -434,7 +357,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         int nxt_y = cur_y, nxt_k = cur_k + NW;
         settle(nxt_y, nxt_k);
 #if FWD_REGPF
-        if (nxt_y <= y_last) load_chunk<PX>(plane0, pl, nxt_y, nxt_k * CH, p.w, lane, vec_ok, nxt);
+        if (nxt_y <= y_last)
+          Src<IN>::template load<PX>(src, pl, nxt_y, nxt_k * CH + PX * lane, p.w, vec_in, nxt.r, nxt.g, nxt.b);
 #endif
 
         const int xl = cur_k * CH + PX * lane;
@@ -523,25 +447,12 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           o2[u] = acc2 + slot_term(s2, ex, eb);
           if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
         }
-        const long long rowoff = (long long)cur_y * p.w;
-        if (vec_ok && xl + PX <= p.w) {
-          stg_stream_vec<PX>(oplane0 + rowoff + xl, o0);
-          stg_stream_vec<PX>(oplane0 + opl + rowoff + xl, o1);
-          stg_stream_vec<PX>(oplane0 + 2 * opl + rowoff + xl, o2);
-        } else {
-#pragma unroll
-          for (int u = 0; u < PX; ++u) {
-            if (xl + u < p.w) {
-              __stcs(oplane0 + rowoff + xl + u, o0[u]);
-              __stcs(oplane0 + opl + rowoff + xl + u, o1[u]);
-              __stcs(oplane0 + 2 * opl + rowoff + xl + u, o2[u]);
-            }
-          }
-        }
+        Dst<OUT>::template store<PX>(dst, opl, cur_y, xl, p.w, vec_out, o0, o1, o2);
 #if FWD_REGPF
         cur = nxt;
 #else
-        if (nxt_y <= y_last) load_chunk<PX>(plane0, pl, nxt_y, nxt_k * CH, p.w, lane, vec_ok, cur);
+        if (nxt_y <= y_last)
+          Src<IN>::template load<PX>(src, pl, nxt_y, nxt_k * CH + PX * lane, p.w, vec_in, cur.r, cur.g, cur.b);
 #endif
         cur_y = nxt_y;
         cur_k = nxt_k;
@@ -693,11 +604,11 @@ cudaError_t fwd_texture(const float* tables, int batch, const TableLayout& L, cu
 
 cudaError_t fwd_texture_used(cudaTextureObject_t tex, cudaStream_t st) { return tex_mark_used(tex, st); }
 
-template <int DT, int DS>
+template <int DT, int DS, int IN, int OUT>
 static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t smem,
                                cudaStream_t st) {
-  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps>
-                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps>;
+  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps, IN, OUT>
+                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps, IN, OUT>;
   // function attributes are set once per (instantiation, smem size); setting
   // them is not a stream operation, so graph capture does not see it
   static size_t configured[2] = {0, 0};
@@ -728,9 +639,32 @@ static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t 
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
+template <int IN, int OUT>
+static cudaError_t launch_fmt(const FwdParams& p, const TableLayout& L, bool chk, int grid, size_t smem,
+                              cudaStream_t st) {
+  if (L.dt == 33 && L.ds == 17) return launch_dims<33, 17, IN, OUT>(p, chk, grid, smem, st);
+  if (IN == kF32 && OUT == kF32 && L.dt == 17 && L.ds == 8)
+    return launch_dims<17, 8, IN, OUT>(p, chk, grid, smem, st);
+  return launch_dims<0, 0, IN, OUT>(p, chk, grid, smem, st);
+}
+
+bool fused_fwd_formats_supported(int in_fmt, int out_fmt) {
+  if (in_fmt < kF32 || in_fmt > kU16 || out_fmt < kF32 || out_fmt > kU16) return false;
+  if (in_fmt == kF32 && out_fmt == kF32) return true;
+  return kPx == 4;
+}
+
 cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,
                              int h_total, const float* tables, const TableLayout& L,
                              int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
+  return launch_fused_fwd_io(rgb, kF32, out, kF32, batch, h, w, y0, h_total, tables, L, nonfinite,
+                             st, pl_in, pl_out);
+}
+
+cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
+                                int w, int y0, int h_total, const float* tables, const TableLayout& L,
+                                int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
+  if (!fused_fwd_formats_supported(in_fmt, out_fmt)) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
   if (g_num_sms == 0) {
@@ -738,7 +672,7 @@ cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   FwdParams p;
-  p.rgb = rgb;
+  p.in = in;
   p.out = out;
   p.batch = batch;
   p.h = h;
@@ -770,9 +704,26 @@ cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int
   p.col_smem = smem + col_bytes <= kSmemForL1Tex ? 1 : 0;
   if (p.col_smem) smem += col_bytes;
   const bool chk = nonfinite != nullptr;
-  if (L.dt == 33 && L.ds == 17) e = launch_dims<33, 17>(p, chk, (int)grid, smem, st);
-  else if (L.dt == 17 && L.ds == 8) e = launch_dims<17, 8>(p, chk, (int)grid, smem, st);
-  else e = launch_dims<0, 0>(p, chk, (int)grid, smem, st);
+  const int g = (int)grid;
+  const int fmt = in_fmt * 3 + out_fmt;
+  if (fmt == kF32 * 3 + kF32) {
+    e = launch_fmt<kF32, kF32>(p, L, chk, g, smem, st);
+  } else {
+#if FWD_PX == 4
+    switch (fmt) {
+      case kU8 * 3 + kU8: e = launch_fmt<kU8, kU8>(p, L, chk, g, smem, st); break;
+      case kU16 * 3 + kU16: e = launch_fmt<kU16, kU16>(p, L, chk, g, smem, st); break;
+      case kU8 * 3 + kF32: e = launch_fmt<kU8, kF32>(p, L, chk, g, smem, st); break;
+      case kU16 * 3 + kF32: e = launch_fmt<kU16, kF32>(p, L, chk, g, smem, st); break;
+      case kF32 * 3 + kU8: e = launch_fmt<kF32, kU8>(p, L, chk, g, smem, st); break;
+      case kF32 * 3 + kU16: e = launch_fmt<kF32, kU16>(p, L, chk, g, smem, st); break;
+      case kU8 * 3 + kU16: e = launch_fmt<kU8, kU16>(p, L, chk, g, smem, st); break;
+      default: e = launch_fmt<kU16, kU8>(p, L, chk, g, smem, st); break;
+    }
+#else
+    e = cudaErrorInvalidValue;
+#endif
+  }
   if (e != cudaSuccess) return e;
   return tex_mark_used(p.tex, st);
 }

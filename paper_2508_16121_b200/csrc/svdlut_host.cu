@@ -14,14 +14,11 @@
 
 #include "../../include/svdlut_b200.h"
 #include "svdlut_common.cuh"
+#include "svdlut_io.cuh"
 #include "svdlut_internal.h"
 
 using namespace svdlut;
 
-extern "C" int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0,
-                                          int h_total, const void* tables, int d_t, int d_s,
-                                          float* out, void* workspace, size_t workspace_bytes,
-                                          int* nonfinite, int variant, void* stream);
 
 constexpr int kMaxStrips = 32;
 
@@ -99,11 +96,19 @@ void svdlut_ctx_destroy(svdlut_ctx* c) {
   delete c;
 }
 
-int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
-                        const float* lut_planes, const float* lw, const float* lb, int d_t,
-                        const float* grid_planes, const float* gw, const float* gb, int k,
-                        int d_s, float* out, int exact, int* nonfinite) {
+}  // extern "C"
+
+// Host-buffer pipeline for every sample format (svdlut_io.cuh): f32 planar
+// images move as strip-major (3, hs, w) slabs (one 2D copy per strip), HWC
+// integer images as contiguous row ranges.
+static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h, int w,
+                             const float* lut_planes, const float* lw, const float* lb, int d_t,
+                             const float* grid_planes, const float* gw, const float* gb, int k,
+                             int d_s, void* out, int out_fmt, int exact, int* nonfinite) {
   if (!ctx) return SVDLUT_ERR_INVALID_ARGUMENT;
+  if (!fused_fwd_formats_supported(in_fmt, out_fmt)) return SVDLUT_ERR_INVALID_ARGUMENT;
+  if ((in_fmt != kF32 || out_fmt != kF32) && (exact || !svdlut_fast_supported(d_t, d_s)))
+    return SVDLUT_ERR_UNSUPPORTED;  // integer formats: fast kernel only
   if (!rgb || !out || !lut_planes || !lw || !lb || !grid_planes || !gw || !gb)
     return SVDLUT_ERR_INVALID_ARGUMENT;
   if (k % 3 != 0 || k < 1) return k < 1 ? SVDLUT_ERR_DIMENSION_MISMATCH : SVDLUT_ERR_BAD_GRID_COUNT;
@@ -118,11 +123,13 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   const size_t par_floats = n_lut + 9 + 3 + n_grid + 3ull * k + k;
   const size_t tb = fast ? svdlut_table_bytes(d_t, d_s) : 0;
   const size_t par_bytes = rup(par_floats * 4) + rup(tb) + 256;
-  const size_t img_bytes = 2 * rup((size_t)3 * h * w * 4);
+  const size_t ib = fmt_bytes(in_fmt), ob = fmt_bytes(out_fmt);
+  const size_t in_bytes = (size_t)3 * h * w * ib, out_bytes = (size_t)3 * h * w * ob;
+  const size_t img_bytes = rup(in_bytes) + rup(out_bytes);
   if (ensure(&ctx->d_img, &ctx->d_img_bytes, img_bytes) != cudaSuccess) return SVDLUT_ERR_CUDA;
   if (ensure(&ctx->d_par, &ctx->d_par_bytes, par_bytes) != cudaSuccess) return SVDLUT_ERR_CUDA;
-  float* d_in = (float*)ctx->d_img;
-  float* d_out = (float*)((char*)ctx->d_img + rup((size_t)3 * h * w * 4));
+  char* d_in = (char*)ctx->d_img;
+  char* d_out = (char*)ctx->d_img + rup(in_bytes);
   float* d_lut = (float*)ctx->d_par;
   float* d_lw = d_lut + n_lut;
   float* d_lb = d_lw + 9;
@@ -152,15 +159,21 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   // are a quarter of that, because the pipeline fill (first H2D) and drain
   // (last D2H) run one PCIe direction alone.
   const size_t plane = (size_t)h * w;
-  static const size_t strip_b = [] {
-    const char* e = getenv("SVDLUT_STRIP_KB");  // development knob
+  const TableLayout L = TableLayout::make(d_t, d_s);
+  static const size_t strip_env = [] {
+    const char* e = getenv("SVDLUT_STRIP_KB");  // development knob: fixed strip size
     const long v = e ? atol(e) : 0;
-    return v > 0 ? (size_t)v << 10 : (size_t)12 << 20;
+    return v > 0 ? (size_t)v << 10 : (size_t)0;
   }();
   int bounds[kMaxStrips + 1];
   int n_strips = 0;
   {
-    const int unit = (int)std::max<size_t>(1, strip_b / ((size_t)3 * w * 4));  // rows per strip
+    // about 4 strips per image (plus the edges), 2..12 MB each (measured best
+    // for 4K f32, u16 and u8 payloads), sized by the larger direction
+    const size_t row_b = (size_t)3 * w * std::max(ib, ob);
+    const size_t target =
+        strip_env ? strip_env : std::min((size_t)12 << 20, std::max((size_t)2 << 20, row_b * h / 4));
+    const int unit = (int)std::max<size_t>(1, target / row_b);  // rows per strip
     const int edge = std::max(1, unit / 4);
     bounds[0] = 0;
     if (h <= 2 * edge + unit) {
@@ -184,30 +197,41 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   for (int s = 0; s < n_strips; ++s) {
     const int r0 = bounds[s], r1 = bounds[s + 1];
     const int hs = r1 - r0;
-    float* din = d_in + (size_t)3 * r0 * w;    // strip-major device layout (3, hs, w)
-    float* dout = d_out + (size_t)3 * r0 * w;
-    // the strip's 3 channel slabs: one 2D copy (host pitch = plane)
-    if (cudaMemcpy2DAsync(din, (size_t)hs * w * 4, rgb + (size_t)r0 * w, plane * 4,
-                          (size_t)hs * w * 4, 3, cudaMemcpyHostToDevice, s_in) != cudaSuccess)
+    // device layout: f32 strip-major (3, hs, w) at the strip's offset; HWC
+    // rows [r0, r1) contiguous, as on the host
+    char* din = d_in + (size_t)3 * r0 * w * ib;
+    char* dout = d_out + (size_t)3 * r0 * w * ob;
+    if (in_fmt == kF32) {  // the strip's 3 channel slabs: one 2D copy (host pitch = plane)
+      if (cudaMemcpy2DAsync(din, (size_t)hs * w * 4, (const float*)rgb + (size_t)r0 * w, plane * 4,
+                            (size_t)hs * w * 4, 3, cudaMemcpyHostToDevice, s_in) != cudaSuccess)
+        return SVDLUT_ERR_CUDA;
+    } else if (cudaMemcpyAsync(din, (const char*)rgb + (size_t)3 * r0 * w * ib, (size_t)3 * hs * w * ib,
+                               cudaMemcpyHostToDevice, s_in) != cudaSuccess) {
       return SVDLUT_ERR_CUDA;
+    }
     if (trace) cudaEventRecord(tev[3 * s], s_in);
     if (cudaEventRecord(ctx->ev_in[s], s_in) != cudaSuccess) return SVDLUT_ERR_CUDA;
     if (cudaStreamWaitEvent(s_k, ctx->ev_in[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
-    int rc;
     if (fast) {
-      rc = svdlut_fused_fwd_packed_ex(din, 1, hs, w, r0, h, d_tables, d_t, d_s, dout, nullptr, 0,
-                                      d_flag, -1, s_k);
+      if (launch_fused_fwd_io(din, in_fmt, dout, out_fmt, 1, hs, w, r0, h, (const float*)d_tables, L,
+                              d_flag, s_k) != cudaSuccess)
+        return SVDLUT_ERR_CUDA;
     } else {
-      rc = svdlut_fused_fwd_exact(din, 1, hs, w, r0, h, d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb,
-                                  k, d_s, dout, s_k);
+      const int rc = svdlut_fused_fwd_exact((const float*)din, 1, hs, w, r0, h, d_lut, d_lw, d_lb, d_t,
+                                            d_grid, d_gw, d_gb, k, d_s, (float*)dout, s_k);
+      if (rc != SVDLUT_OK) return rc;
     }
-    if (rc != SVDLUT_OK) return rc;
     if (trace) cudaEventRecord(tev[3 * s + 1], s_k);
     if (cudaEventRecord(ctx->ev_k[s], s_k) != cudaSuccess) return SVDLUT_ERR_CUDA;
     if (cudaStreamWaitEvent(s_out, ctx->ev_k[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
-    if (cudaMemcpy2DAsync(out + (size_t)r0 * w, plane * 4, dout, (size_t)hs * w * 4,
-                          (size_t)hs * w * 4, 3, cudaMemcpyDeviceToHost, s_out) != cudaSuccess)
+    if (out_fmt == kF32) {
+      if (cudaMemcpy2DAsync((float*)out + (size_t)r0 * w, plane * 4, dout, (size_t)hs * w * 4,
+                            (size_t)hs * w * 4, 3, cudaMemcpyDeviceToHost, s_out) != cudaSuccess)
+        return SVDLUT_ERR_CUDA;
+    } else if (cudaMemcpyAsync((char*)out + (size_t)3 * r0 * w * ob, dout, (size_t)3 * hs * w * ob,
+                               cudaMemcpyDeviceToHost, s_out) != cudaSuccess) {
       return SVDLUT_ERR_CUDA;
+    }
     if (trace) cudaEventRecord(tev[3 * s + 2], s_out);
   }
   if (trace) {
@@ -225,6 +249,24 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
   if (cudaStreamSynchronize(s_out) != cudaSuccess) return SVDLUT_ERR_CUDA;
   if (nonfinite) *nonfinite = fast ? *ctx->h_flag : 0;
   return SVDLUT_OK;
+}
+
+extern "C" {
+
+int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
+                        const float* lut_planes, const float* lw, const float* lb, int d_t,
+                        const float* grid_planes, const float* gw, const float* gb, int k,
+                        int d_s, float* out, int exact, int* nonfinite) {
+  return enhance_host_impl(ctx, rgb, kF32, h, w, lut_planes, lw, lb, d_t, grid_planes, gw, gb, k, d_s,
+                           out, kF32, exact, nonfinite);
+}
+
+int svdlut_enhance_host_io(svdlut_ctx* ctx, const void* in, int in_fmt, int h, int w,
+                           const float* lut_planes, const float* lw, const float* lb, int d_t,
+                           const float* grid_planes, const float* gw, const float* gb, int k, int d_s,
+                           void* out, int out_fmt, int* nonfinite) {
+  return enhance_host_impl(ctx, in, in_fmt, h, w, lut_planes, lw, lb, d_t, grid_planes, gw, gb, k, d_s,
+                           out, out_fmt, 0, nonfinite);
 }
 
 int svdlut_reconstruct_host(svdlut_ctx* ctx, const float* u, const float* s, const float* vt,

@@ -22,6 +22,14 @@ cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int
                              int* nonfinite, cudaStream_t st, long long pl_in = 0,
                              long long pl_out = 0);
 
+// Same with explicit sample formats (SampleFmt in svdlut_io.cuh: 0 f32 planar,
+// 1 u8 HWC, 2 big-endian u16 HWC); plane strides apply to f32 only.
+cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
+                                int w, int y0, int h_total, const float* tables, const TableLayout& L,
+                                int* nonfinite, cudaStream_t st, long long pl_in = 0,
+                                long long pl_out = 0);
+bool fused_fwd_formats_supported(int in_fmt, int out_fmt);
+
 cudaError_t launch_fused_exact(const float* rgb, float* out, int batch, int h, int w, int y0,
                                int h_total, const float* lp, const float* lw, const float* lb,
                                int dt, const float* gp, const float* gw, const float* gb, int k,

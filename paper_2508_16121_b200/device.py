@@ -23,6 +23,7 @@ from . import _lib
 from .errors import DimensionMismatch
 
 __all__ = [
+    "apply_io", "FMT_F32", "FMT_U8", "FMT_U16BE",
     "table_bytes", "fast_supported", "PackedTables", "reconstruct", "pack_tables",
     "pack_tables_factors", "apply",
     "apply_exact", "fused_forward", "indices", "fused_backward", "reconstruct_backward",
@@ -159,6 +160,56 @@ def apply(rgb, tables, out=None, y0=0, h_total=None, variant=-1, nonfinite=None)
     _lib.call("svdlut_fused_fwd_packed_ex", _p(rgb), b, h, w, y0, h_total, _p(tables.buf),
               tables.d_t, tables.d_s, _p(out), _p(None), 0, _p(nonfinite), variant,
               _stream(rgb))
+    return out
+
+
+FMT_F32, FMT_U8, FMT_U16BE = 0, 1, 2  # include/svdlut_b200.h SVDLUT_FMT_*
+_FMT_NAMES = {"f32": FMT_F32, "u8": FMT_U8, "u16be": FMT_U16BE}
+
+
+def _fmt(f):
+    return _FMT_NAMES[f] if isinstance(f, str) else int(f)
+
+
+def _io_image(t, fmt, batch):
+    """(B, H, W) of an image tensor in sample format fmt: f32 (B,3,H,W);
+    u8 (B,H,W,3) uint8; u16be (B,H,W,6) uint8 = 3 big-endian samples."""
+    if fmt == FMT_F32:
+        t = _image(t, batch)
+        return t, t.shape[0], t.shape[2], t.shape[3]
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.uint8 or not t.is_cuda:
+        raise DimensionMismatch("integer images must be CUDA uint8 tensors")
+    last = 3 if fmt == FMT_U8 else 6
+    if t.dim() == 3:
+        t = t.unsqueeze(0)
+    if t.dim() != 4 or t.shape[3] != last or not t.is_contiguous():
+        raise DimensionMismatch(f"expected a contiguous (B, H, W, {last}) uint8 image, got {tuple(t.shape)}")
+    if batch is not None and t.shape[0] != batch:
+        raise DimensionMismatch(f"{t.shape[0]} images but tables for {batch}")
+    return t, t.shape[0], t.shape[1], t.shape[2]
+
+
+def apply_io(x, tables, in_fmt="f32", out_fmt="f32", out=None, y0=0, h_total=None, nonfinite=None):
+    """Fused apply with PNM sample formats on either side: integer input is
+    decoded as pnm.load does (f32(f64(v) / maxval), pnm.py:79), integer
+    output quantized as pnm.save does (floor(clip(y,0,1)*maxval + 0.5),
+    pnm.py:83-86) — inside the kernel, so u8 in/out moves 6 B/pixel instead
+    of 24.  Formats: "f32" (B,3,H,W) float32, "u8" (B,H,W,3) uint8, "u16be"
+    (B,H,W,6) uint8 holding big-endian uint16 samples."""
+    fi, fo = _fmt(in_fmt), _fmt(out_fmt)
+    x, b, h, w = _io_image(x, fi, tables.batch)
+    h_total = h if h_total is None else h_total
+    if out is None:
+        if fo == FMT_F32:
+            out = torch.empty((b, 3, h, w), dtype=torch.float32, device=x.device)
+        else:
+            out = torch.empty((b, h, w, 3 if fo == FMT_U8 else 6), dtype=torch.uint8, device=x.device)
+    else:
+        out, bo, ho, wo = _io_image(out, fo, tables.batch)
+        if (bo, ho, wo) != (b, h, w):
+            raise DimensionMismatch("out does not match the input image size")
+    _lib.call("svdlut_fused_fwd_io", _p(x), fi, b, h, w, y0, h_total, _p(tables.buf), tables.d_t,
+              tables.d_s, _p(out), fo, _p(nonfinite), _stream(x))
     return out
 
 

@@ -24,7 +24,7 @@ from . import _lib
 from .core_types import Image as _Image
 from .errors import BadGridCount, CudaError, DegenerateImage, DimensionMismatch, NonFiniteValue
 
-__all__ = ["fused_enhance", "_alloc_raster"]
+__all__ = ["fused_enhance", "enhance_payload", "_alloc_raster"]
 
 # Test instrumentation: called with the shape of every raster this module
 # allocates (the reference's contract; transform.py:50-58).
@@ -35,6 +35,19 @@ def _alloc_raster(shape):
     if _raster_hook is not None:
         _raster_hook(shape)
     return _pinned_empty(shape)
+
+
+def _pinned_payload(shape, fmt):
+    """Page-locked output payload (uint8 or big-endian uint16) so the D2H
+    copies run at full PCIe rate; pageable memory if pinning is unavailable."""
+    try:
+        import torch
+
+        n = int(np.prod(shape)) * (1 if fmt == 1 else 2)
+        raw = torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy()
+        return raw.view(np.uint8 if fmt == 1 else np.dtype(">u2")).reshape(shape)
+    except Exception:  # noqa: BLE001 - pinning is an optimisation only
+        return np.empty(shape, np.uint8 if fmt == 1 else np.dtype(">u2"))
 
 
 def _pinned_empty(shape):
@@ -126,3 +139,53 @@ def fused_enhance(img, luts, lut_weights, grids, grid_weights, threads: int = 1,
             raise NonFiniteValue("image data contains a NaN or infinite entry")
         return cls._trusted(w, h, out)
     return cls(w, h, out)  # exact mode / foreign Image type: the constructor validates
+
+
+def enhance_payload(payload, luts, lut_weights, grids, grid_weights, out_bits=None):
+    """pnm.load -> fused_enhance -> pnm.save's payload, fused on the GPU.
+
+    ``payload``: a PNM P6 sample array (H, W, 3), uint8 (maxval 255) or
+    big-endian uint16 ``'>u2'`` (maxval 65535) — what reference pnm.py reads
+    and writes after the header.  Samples decode as f32(f64(v) / maxval)
+    (pnm.py:79), the fast fp32 apply runs, and the result is quantized as
+    floor(clip(y, 0, 1) * maxval + 0.5) (pnm.py:83-86) in the kernel epilogue;
+    only 6 (u8) or 12 (u16) bytes per pixel cross PCIe.  ``out_bits`` (8 or
+    16) defaults to the input's.  Against the reference chain the result
+    differs only where the fp32 output (within 1e-5 of the reference) falls on
+    the other side of a quantization boundary (±1).
+    """
+    pl = np.asarray(payload)
+    if pl.ndim != 3 or pl.shape[2] != 3:
+        raise DimensionMismatch(f"payload must be (H, W, 3), got {pl.shape}")
+    if pl.dtype == np.uint8:
+        fi, in_bits = 1, 8
+    elif pl.dtype in (np.dtype(">u2"), np.dtype("<u2")):
+        fi, in_bits = 2, 16
+        pl = pl.astype(">u2", copy=False)
+    else:
+        raise DimensionMismatch(f"payload dtype must be uint8 or >u2, got {pl.dtype}")
+    out_bits = in_bits if out_bits is None else out_bits
+    if out_bits not in (8, 16):
+        raise DimensionMismatch(f"out_bits must be 8 or 16, got {out_bits}")
+    if grids.k % 3 != 0:
+        raise BadGridCount(f"grid count {grids.k} is not a multiple of 3")
+    if grid_weights.k != grids.k:
+        raise DimensionMismatch(f"{grids.k} grids but {grid_weights.k} weight rows")
+    h, w = pl.shape[0], pl.shape[1]
+    if w < 2 or h < 2:
+        raise DegenerateImage("slicing needs at least 2 px in each direction")
+    pl = np.ascontiguousarray(pl)
+    fo = 1 if out_bits == 8 else 2
+    out = _pinned_payload((h, w, 3), fo)
+    planes = _c32(luts.planes)
+    lw, lb = _c32(lut_weights.w), _c32(lut_weights.b)
+    gp = _c32(grids.planes)
+    gw, gb = _c32(grid_weights.w), _c32(grid_weights.b)
+    flag = ctypes.c_int(0)
+    ctx = _host_ctx(_current_device())
+    _lib.call("svdlut_enhance_host_io", ctx, _ptr(pl), fi, h, w, _ptr(planes), _ptr(lw), _ptr(lb),
+              planes.shape[2], _ptr(gp), _ptr(gw), _ptr(gb), gp.shape[0], gp.shape[2], _ptr(out), fo,
+              ctypes.byref(flag))
+    if flag.value:
+        raise NonFiniteValue("enhanced image contains a NaN or infinite entry")
+    return out
