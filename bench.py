@@ -337,6 +337,33 @@ def main():
                "ms_per_step": round(ems, 4),
                "api": "svd.reconstruct_lut + transform.fused_enhance (pinned host arrays)"}
 
+    # ---- the same step on PNM payloads (u8 HWC in/out, decode + quantization fused) ----
+    e2e_u8 = None
+    if not a.no_e2e:
+        import torch as _t
+
+        pin8 = _t.empty((H, W, 3), dtype=_t.uint8, pin_memory=True)
+        pin8.copy_(_t.from_numpy(np.ascontiguousarray(
+            np.floor(np.clip(case.rgb.transpose(1, 2, 0), 0, 1) * 255 + 0.5).astype(np.uint8))))
+        payload = pin8.numpy()
+        for _ in range(3):  # same hold pattern as the timed loop (2 output buffers live)
+            q = transform.enhance_payload(payload, svd.reconstruct_lut(factors), lw, grids, gw)
+        barrier()
+        per8 = []
+        t0 = time.perf_counter()
+        for _ in range(esteps):
+            ta = time.perf_counter()
+            q = transform.enhance_payload(payload, svd.reconstruct_lut(factors), lw, grids, gw)
+            per8.append(time.perf_counter() - ta)
+        ums = max_over_ranks(1e3 * (time.perf_counter() - t0) / esteps)
+        print("e2e_pnm_u8 per-step ms: " + " ".join(f"{1e3 * v:.2f}" for v in per8), file=sys.stderr)
+        e2e_u8 = {"value": round(world * H * W / (ums * 1e-3) / 1e6, 3), "unit": UNIT,
+                  "h2d_bytes_per_step": int(payload.nbytes + table_h2d),
+                  "d2h_bytes_per_step": int(q.nbytes + 9 * 33 * 33 * 4),
+                  "ms_per_step": round(ums, 4),
+                  "api": "svd.reconstruct_lut + transform.enhance_payload (PNM u8 payload in/out, "
+                         "pinned; decode + pnm.save quantization fused in the kernel)"}
+
     cpu = None
     if rank == 0 and not a.no_cpu:
         mps, threads, med, _ = cpu_reference(case, 3)
@@ -353,7 +380,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded smooth field, SURVEY.md §8d recipe)",
             "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": 2 * a.steps, "clocks": sampler.summary(),
+            "e2e": e2e, "e2e_pnm_u8": e2e_u8, "gpu_launches": 2 * a.steps, "clocks": sampler.summary(),
             "launch": "cuda graphs of 4 steps" if step_graphs else "eager",
         }
         print(json.dumps(line), flush=True)

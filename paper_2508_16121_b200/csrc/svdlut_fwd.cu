@@ -109,11 +109,33 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+#ifndef FWD_TEXDEP
+#define FWD_TEXDEP 1  // next pixel's TLD index depends on this pixel's last LDS (see below)
+#endif
+#ifndef FWD_LDS_PLAIN
+#define FWD_LDS_PLAIN 1
+#endif
 __device__ __forceinline__ float4 lds4(uint32_t a) {
+#if FWD_LDS_PLAIN
+  // an ordinary shared load (the scheduler may move it; still ordered
+  // against the mbarrier waits, which clobber memory)
+  return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(a));
+#else
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(a));
+  return v;
+#endif
+}
+// Texture gather as volatile PTX: keeps the one-pixel-ahead issue order of the
+// source (the compiler otherwise hoists all of a chunk's TLDs to its top and
+// runs out of registers for the shared-memory gathers).
+__device__ __forceinline__ float4 texv4(cudaTextureObject_t t, int i) {
+  float4 v;
+  asm volatile("tex.1d.v4.f32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(t), "r"(i));
   return v;
 }
 __device__ __forceinline__ float2 lds2(uint32_t a) {
@@ -398,22 +420,14 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           const uint32_t bg = cbracket(__saturatef(cur.g[0]), tdm1, tdm2, tdg);
           const uint32_t bb = cbracket(__saturatef(cur.b[0]), tdm1, tdm2, tdb);
           const int ti = (int)(bg * cst3 + bb * 3u + texK);
-          tx0 = tex1Dfetch<float4>(p.tex, ti);
-          tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
-          tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
+          tx0 = texv4(p.tex, ti);
+          tx1 = texv4(p.tex, ti + 1);
+          tx2 = texv4(p.tex, ti + 2);
         }
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
           const float4 c0 = tx0, c1 = tx1, c2 = tx2;
           const float dg = tdg, db = tdb;
-          if (u + 1 < PX) {
-            const uint32_t bg1 = cbracket(__saturatef(cur.g[u + 1]), tdm1, tdm2, tdg);
-            const uint32_t bb1 = cbracket(__saturatef(cur.b[u + 1]), tdm1, tdm2, tdb);
-            const int ti = (int)(bg1 * cst3 + bb1 * 3u + texK);
-            tx0 = tex1Dfetch<float4>(p.tex, ti);
-            tx1 = tex1Dfetch<float4>(p.tex, ti + 1);
-            tx2 = tex1Dfetch<float4>(p.tex, ti + 2);
-          }
           const float qr = __saturatef(cur.r[u]), qg = __saturatef(cur.g[u]),
                       qb = __saturatef(cur.b[u]);
           float dr, dg_, db_;
@@ -435,6 +449,18 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           const float4 s0 = lds4(sa + sr * 16u);
           const float4 s1 = lds4(sa + chan_bytes + sg * 16u);
           const float4 s2 = lds4(sa + 2u * chan_bytes + sb * 16u);
+          if (u + 1 < PX) {
+            // next pixel's texture gathers, issued after this pixel's shared
+            // gathers: the index carries a (never taken) dependency on the
+            // last LDS so ptxas cannot hoist every TLD of the chunk to its top
+            // (which starves the LDS of registers)
+            const uint32_t bg1 = cbracket(__saturatef(cur.g[u + 1]), tdm1, tdm2, tdg);
+            const uint32_t bb1 = cbracket(__saturatef(cur.b[u + 1]), tdm1, tdm2, tdb);
+            const int ti = (int)(bg1 * cst3 + bb1 * 3u + texK) + (FWD_TEXDEP && s2.w != s2.w ? 1 : 0);
+            tx0 = texv4(p.tex, ti);
+            tx1 = texv4(p.tex, ti + 1);
+            tx2 = texv4(p.tex, ti + 2);
+          }
           float2 acc01;
           float acc2;
           cell_term<true>(rg0, rg1, rg2, dr, dg_, acc01, acc2);    // pair rg (shared memory)
