@@ -93,12 +93,19 @@ struct BwdParams {
 __device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+#ifndef BWD_LDS_PLAIN
+#define BWD_LDS_PLAIN 1  // plain shared loads: the scheduler may reorder them (faster)
+#endif
 __device__ __forceinline__ float4 blds4(uint32_t a) {
+#if BWD_LDS_PLAIN
+  return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(a));
+#else
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(a));
   return v;
+#endif
 }
 __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, float& delta) {
   const float t = fminf(__fmul_rz(q, dm1), dm2);
