@@ -19,6 +19,12 @@
  *                             decode of pnm.load (pnm.py:72-80) and the
  *                             quantization of pnm.save (pnm.py:83-108) fused
  *   svdlut_enhance_host_io    host-buffer entry with the same formats
+ *   svdlut_slice_grids        transform.slice_grid2d   (transform.py:152-178)
+ *   svdlut_apply_lut2d        transform.apply_lut2d    (transform.py:123-141)
+ *   svdlut_combine_slices     transform.combine_slices (transform.py:181-193)
+ *   svdlut_apply_lut3d        transform.apply_lut3d    (transform.py:93-120)
+ *                             (the multi-pass "original structure" and the 3D-LUT
+ *                             baseline, bitwise equal to the reference)
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  `stream` is a
@@ -183,6 +189,22 @@ int svdlut_enhance_host(svdlut_ctx* ctx, const float* rgb, int h, int w,
                         const float* lut_planes, const float* lw, const float* lb, int d_t,
                         const float* grid_planes, const float* gw, const float* gb, int k,
                         int d_s, float* out, int exact, int* nonfinite);
+
+/* ---- multi-pass "original structure" + 3D LUT (f64, bitwise equal to the
+ * reference's numpy stages; f32 rasters between stages) ------------------ */
+/* fs (B, K, H, W): per-grid slicing maps of rows y0.. of an h_total-row image. */
+int svdlut_slice_grids(const float* rgb, int batch, int h, int w, int y0, int h_total,
+                       const float* grid_planes, const float* gw, const float* gb, int k, int d_s,
+                       float* fs, void* stream);
+/* out (B, 3, H, W): weighted 2D-LUT transform + per-channel bias. */
+int svdlut_apply_lut2d(const float* rgb, int batch, int h, int w, const float* lut_planes,
+                       const float* lw, const float* lb, int d_t, float* out, void* stream);
+/* out = base + sum of maps j = c, c+3, ... (f32, map order). */
+int svdlut_combine_slices(const float* base, const float* fs, int batch, int h, int w, int k,
+                          float* out, void* stream);
+/* out (B, 3, H, W): trilinear 3D LUT, cubes (B, 3, d, d, d) [c][r][g][b]. */
+int svdlut_apply_lut3d(const float* rgb, int batch, int h, int w, const float* cubes, int d,
+                       float* out, void* stream);
 
 /* svdlut_enhance_host with sample formats (fast kernel only): e.g. a PNM
  * payload in, a PNM payload out — 6 B/pixel over PCIe instead of 24 (U8). */

@@ -48,6 +48,10 @@ _SIGS = {
     "svdlut_enhance_host": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i, _vp,
                                  _i, ctypes.POINTER(_i)]),
     "svdlut_reconstruct_host": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp]),
+    "svdlut_slice_grids": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "svdlut_apply_lut2d": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp]),
+    "svdlut_combine_slices": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+    "svdlut_apply_lut3d": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp]),
     "svdlut_fused_fwd_io": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _i, _vp, _vp]),
     "svdlut_enhance_host_io": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,
                                     _vp, _i, ctypes.POINTER(_i)]),

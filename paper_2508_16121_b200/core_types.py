@@ -17,7 +17,8 @@ import numpy as np
 
 from .errors import BadVertexCount, DimensionMismatch, NonFiniteValue
 
-__all__ = ["Image", "Lut2DSet", "LutWeights", "GridSet", "GridWeights", "SvdLut"]
+__all__ = ["Image", "Lut2DSet", "LutWeights", "GridSet", "GridWeights", "SvdLut", "Lut3D",
+           "SpatialFeatureMap"]
 
 
 def _ro_f32(a):
@@ -191,3 +192,42 @@ class SvdLut:
     @property
     def n_s(self) -> int:
         return self.u.shape[3]
+
+
+@dataclass(frozen=True)
+class Lut3D:
+    """tables[c][i_r][i_g][i_b] (3, d, d, d): one cube per output channel
+    (reference core_types.py:96-116)."""
+
+    tables: np.ndarray
+
+    def __post_init__(self):
+        t = np.asarray(self.tables, dtype=np.float32)
+        if t.ndim != 4 or t.shape[0] != 3 or not (t.shape[1] == t.shape[2] == t.shape[3]):
+            raise DimensionMismatch(f"expected (3, d, d, d) tables, got {t.shape}")
+        if t.shape[1] < 2:
+            raise BadVertexCount("3D LUT needs at least 2 vertices per axis")
+        _store(self, tables=_ro_f32(t))
+        _require_finite(self.tables, "3D LUT tables")
+
+    @property
+    def d_t(self) -> int:
+        return self.tables.shape[1]
+
+
+@dataclass(frozen=True)
+class SpatialFeatureMap:
+    """k per-grid slicing maps over the image plane, (k, h, w)
+    (reference transform.py:60-76)."""
+
+    data: np.ndarray
+
+    def __post_init__(self):
+        d = np.asarray(self.data, dtype=np.float32)
+        if d.ndim != 3:
+            raise DimensionMismatch(f"expected (k, h, w), got {d.shape}")
+        _store(self, data=_ro_f32(d))
+
+    @property
+    def k(self) -> int:
+        return self.data.shape[0]

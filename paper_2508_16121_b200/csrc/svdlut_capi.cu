@@ -300,6 +300,53 @@ int svdlut_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w,
   return SVDLUT_OK;
 }
 
+int svdlut_slice_grids(const float* rgb, int batch, int h, int w, int y0, int h_total,
+                       const float* grid_planes, const float* gw, const float* gb, int k, int d_s,
+                       float* fs, void* stream) {
+  int rc;
+  if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
+  if (k < 1) return fail(SVDLUT_ERR_DIMENSION_MISMATCH, "need at least one grid");
+  if (d_s < 2) return fail(SVDLUT_ERR_BAD_VERTEX_COUNT, "need at least 2 vertices per axis");
+  if ((long long)batch * h * w == 0) return SVDLUT_OK;
+  if (!rgb || !grid_planes || !gw || !gb || !fs) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  CUDA_TRY(launch_slice(rgb, fs, batch, h, w, y0, h_total, grid_planes, gw, gb, k, d_s,
+                        (cudaStream_t)stream),
+           "slice_grids");
+  return SVDLUT_OK;
+}
+
+int svdlut_apply_lut2d(const float* rgb, int batch, int h, int w, const float* lut_planes,
+                       const float* lw, const float* lb, int d_t, float* out, void* stream) {
+  if (batch < 0 || h < 0 || w < 0) return fail(SVDLUT_ERR_DIMENSION_MISMATCH, "negative size");
+  if (d_t < 2) return fail(SVDLUT_ERR_BAD_VERTEX_COUNT, "need at least 2 vertices per axis");
+  if ((long long)batch * h * w == 0) return SVDLUT_OK;
+  if (!rgb || !lut_planes || !lw || !lb || !out) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  CUDA_TRY(launch_lut2d(rgb, out, batch, h, w, lut_planes, lw, lb, d_t, (cudaStream_t)stream),
+           "apply_lut2d");
+  return SVDLUT_OK;
+}
+
+int svdlut_combine_slices(const float* base, const float* fs, int batch, int h, int w, int k,
+                          float* out, void* stream) {
+  int rc;
+  if ((rc = check_k(k)) != SVDLUT_OK) return rc;
+  if (batch < 0 || h < 0 || w < 0) return fail(SVDLUT_ERR_DIMENSION_MISMATCH, "negative size");
+  if ((long long)batch * h * w == 0) return SVDLUT_OK;
+  if (!base || !fs || !out) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  CUDA_TRY(launch_combine(base, fs, out, batch, h, w, k, (cudaStream_t)stream), "combine_slices");
+  return SVDLUT_OK;
+}
+
+int svdlut_apply_lut3d(const float* rgb, int batch, int h, int w, const float* cubes, int d,
+                       float* out, void* stream) {
+  if (batch < 0 || h < 0 || w < 0) return fail(SVDLUT_ERR_DIMENSION_MISMATCH, "negative size");
+  if (d < 2) return fail(SVDLUT_ERR_BAD_VERTEX_COUNT, "3D LUT needs at least 2 vertices per axis");
+  if ((long long)batch * h * w == 0) return SVDLUT_OK;
+  if (!rgb || !cubes || !out) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  CUDA_TRY(launch_lut3d(rgb, out, batch, h, w, cubes, d, (cudaStream_t)stream), "apply_lut3d");
+  return SVDLUT_OK;
+}
+
 int svdlut_reconstruct_bwd(const float* u, const float* s, const float* vt,
                            const float* dplanes, int batch, int d_t, int n_s, float* du,
                            float* ds, float* dvt, void* stream) {

@@ -35,6 +35,18 @@ cudaError_t launch_fused_exact(const float* rgb, float* out, int batch, int h, i
                                int dt, const float* gp, const float* gw, const float* gb, int k,
                                int ds, cudaStream_t st);
 
+// Multi-pass "original structure" (svdlut_naive.cu), f64, bitwise equal to the
+// reference's slice_grid2d / apply_lut2d / combine_slices / apply_lut3d.
+cudaError_t launch_slice(const float* rgb, float* fs, int batch, int h, int w, int y0, int h_total,
+                         const float* gp, const float* gw, const float* gb, int k, int ds,
+                         cudaStream_t st);
+cudaError_t launch_lut2d(const float* rgb, float* out, int batch, int h, int w, const float* lp,
+                         const float* lw, const float* lb, int dt, cudaStream_t st);
+cudaError_t launch_combine(const float* base, const float* fs, float* out, int batch, int h, int w,
+                           int k, cudaStream_t st);
+cudaError_t launch_lut3d(const float* rgb, float* out, int batch, int h, int w, const float* cubes,
+                         int d, cudaStream_t st);
+
 cudaError_t launch_indices(const float* rgb, int batch, int h, int w, int y0, int h_total,
                            int dt, int ds, int32_t* idx, cudaStream_t st);
 

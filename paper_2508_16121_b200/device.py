@@ -26,7 +26,8 @@ __all__ = [
     "apply_io", "FMT_F32", "FMT_U8", "FMT_U16BE",
     "table_bytes", "fast_supported", "PackedTables", "reconstruct", "pack_tables",
     "pack_tables_factors", "apply",
-    "apply_exact", "fused_forward", "indices", "fused_backward", "reconstruct_backward",
+    "apply_exact", "slice_grids", "apply_lut2d", "combine_slices", "apply_lut3d",
+    "fused_forward", "indices", "fused_backward", "reconstruct_backward",
 ]
 
 
@@ -210,6 +211,57 @@ def apply_io(x, tables, in_fmt="f32", out_fmt="f32", out=None, y0=0, h_total=Non
             raise DimensionMismatch("out does not match the input image size")
     _lib.call("svdlut_fused_fwd_io", _p(x), fi, b, h, w, y0, h_total, _p(tables.buf), tables.d_t,
               tables.d_s, _p(out), fo, _p(nonfinite), _stream(x))
+    return out
+
+
+# ---- multi-pass "original structure" and the 3D-LUT baseline (f64 stages,
+#      bitwise equal to the reference's numpy; svdlut_naive.cu) -------------------
+def slice_grids(rgb, grid_planes, gw, gb, y0=0, h_total=None):
+    """(B, K, H, W) slicing maps (reference transform.slice_grid2d)."""
+    gp, gw, gb = _f32(grid_planes, "grid_planes", 5), _f32(gw, "gw", 3), _f32(gb, "gb", 2)
+    rgb = _image(rgb, gp.shape[0])
+    b, _, h, w = rgb.shape
+    k, d_s = gp.shape[1], gp.shape[3]
+    if gw.shape[1] != k or gb.shape[1] != k:
+        raise DimensionMismatch(f"{k} grids but {gw.shape[1]} weight rows")
+    fs = torch.empty((b, k, h, w), dtype=torch.float32, device=rgb.device)
+    _lib.call("svdlut_slice_grids", _p(rgb), b, h, w, y0, h if h_total is None else h_total, _p(gp),
+              _p(gw), _p(gb), k, d_s, _p(fs), _stream(rgb))
+    return fs
+
+
+def apply_lut2d(rgb, lut_planes, lw, lb):
+    """(B, 3, H, W) weighted 2D-LUT transform (reference transform.apply_lut2d)."""
+    lp, lw, lb = _f32(lut_planes, "lut_planes", 5), _f32(lw, "lw", 3), _f32(lb, "lb", 2)
+    rgb = _image(rgb, lp.shape[0])
+    b, _, h, w = rgb.shape
+    out = torch.empty_like(rgb)
+    _lib.call("svdlut_apply_lut2d", _p(rgb), b, h, w, _p(lp), _p(lw), _p(lb), lp.shape[3], _p(out),
+              _stream(rgb))
+    return out
+
+
+def combine_slices(base, fs):
+    """base + channel-grouped slicing maps (reference transform.combine_slices)."""
+    base = _image(base, None)
+    fs = _f32(fs, "fs", 4)
+    if fs.shape[0] != base.shape[0] or fs.shape[2:] != base.shape[2:]:
+        raise DimensionMismatch("feature map size differs from image size")
+    b, _, h, w = base.shape
+    out = torch.empty_like(base)
+    _lib.call("svdlut_combine_slices", _p(base), _p(fs), b, h, w, fs.shape[1], _p(out),
+              _stream(base))
+    return out
+
+
+def apply_lut3d(rgb, cubes):
+    """(B, 3, H, W) trilinear 3D LUT, cubes (B, 3, d, d, d) (reference apply_lut3d)."""
+    cubes = _f32(cubes, "cubes", 5)
+    rgb = _image(rgb, cubes.shape[0])
+    b, _, h, w = rgb.shape
+    out = torch.empty_like(rgb)
+    _lib.call("svdlut_apply_lut3d", _p(rgb), b, h, w, _p(cubes), cubes.shape[2], _p(out),
+              _stream(rgb))
     return out
 
 

@@ -10,6 +10,9 @@ Patched names (the reference's own call sites):
   svdlut.transform.fused_enhance   transform.py:308   (tests import it by name)
   svdlut.network.fused_enhance     network.py:42      (bound at import by run_model)
   svdlut.svd.reconstruct_lut       svd.py:210         (called via module attribute)
+  svdlut.transform.naive_enhance   transform.py:196   (multi-stage twin, f64 stage kernels)
+  svdlut.network.naive_enhance     network.py:42      (run_model(fused=False))
+  svdlut.transform.apply_lut3d     transform.py:93    (3D-LUT baseline)
   svdlut.network.run_model         network.py:179     (only with generator=True: the
                                                       backbone and heads run on the
                                                       GPU too, network.py here)
@@ -72,6 +75,15 @@ def install(package="svdlut", exact=False, generator=False):
                                             alloc=ref_transform._alloc_raster)
 
     @_translate(ref_errors)
+    def naive_enhance(img, luts, lut_weights, grids, grid_weights):
+        return b200_transform.naive_enhance(img, luts, lut_weights, grids, grid_weights,
+                                            alloc=ref_transform._alloc_raster)
+
+    @_translate(ref_errors)
+    def apply_lut3d(img, lut):
+        return b200_transform.apply_lut3d(img, lut, alloc=ref_transform._alloc_raster)
+
+    @_translate(ref_errors)
     def reconstruct_lut(svdlut):
         return b200_svd.reconstruct_lut(svdlut)
 
@@ -83,6 +95,9 @@ def install(package="svdlut", exact=False, generator=False):
 
     patches = [(ref_transform, "fused_enhance", fused_enhance),
                (ref_network, "fused_enhance", fused_enhance),
+               (ref_transform, "naive_enhance", naive_enhance),
+               (ref_network, "naive_enhance", naive_enhance),
+               (ref_transform, "apply_lut3d", apply_lut3d),
                (ref_svd, "reconstruct_lut", reconstruct_lut)]
     if generator:
         patches.append((ref_network, "run_model", run_model))

@@ -24,7 +24,8 @@ from . import _lib
 from .core_types import Image as _Image
 from .errors import BadGridCount, CudaError, DegenerateImage, DimensionMismatch, NonFiniteValue
 
-__all__ = ["fused_enhance", "enhance_payload", "_alloc_raster"]
+__all__ = ["fused_enhance", "enhance_payload", "naive_enhance", "slice_grid2d", "apply_lut2d",
+           "combine_slices", "apply_lut3d", "_alloc_raster"]
 
 # Test instrumentation: called with the shape of every raster this module
 # allocates (the reference's contract; transform.py:50-58).
@@ -194,3 +195,91 @@ def enhance_payload(payload, luts, lut_weights, grids, grid_weights, out_bits=No
     if flag.value:
         raise NonFiniteValue("enhanced image contains a NaN or infinite entry")
     return out
+
+
+# ---- multi-pass "original structure" and the 3D-LUT baseline ---------------------
+# Reference transform.py:93-212 on the GPU (svdlut_naive.cu): every stage is an
+# f64 kernel with the reference's numpy operation order and f32 rasters
+# between stages, so results are bitwise equal to the reference.  They exist
+# for the multi-stage vs fused comparison; the product path is fused_enhance.
+
+def _to_dev(a):
+    import torch
+
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if not a.flags.writeable:  # frozen value types: torch wants a writable buffer
+        a = a.copy()
+    return torch.from_numpy(a).to(torch.device("cuda", _current_device()))
+
+
+def _to_host_raster(t, shape, alloc=None):
+    out = (alloc or _alloc_raster)(shape)
+    out[...] = t.cpu().numpy().reshape(shape)
+    return out
+
+
+def slice_grid2d(img, grids, weights, alloc=None):
+    """(K, H, W) slicing maps of every grid (transform.py:152-178)."""
+    from . import device
+    from .core_types import SpatialFeatureMap
+
+    if img.width < 2 or img.height < 2:
+        raise DegenerateImage("slicing needs at least 2 px in each direction")
+    if weights.k != grids.k:
+        raise DimensionMismatch(f"{grids.k} grids but {weights.k} weight rows")
+    fs = device.slice_grids(_to_dev(img.data)[None], _to_dev(grids.planes)[None],
+                            _to_dev(weights.w)[None], _to_dev(weights.b)[None])
+    return SpatialFeatureMap(_to_host_raster(fs[0], (grids.k, img.height, img.width), alloc))
+
+
+def apply_lut2d(img, luts, weights, alloc=None):
+    """Weighted 2D-LUT transform + channel bias (transform.py:123-141)."""
+    from . import device
+
+    y = device.apply_lut2d(_to_dev(img.data)[None], _to_dev(luts.planes)[None],
+                           _to_dev(weights.w)[None], _to_dev(weights.b)[None])
+    return _image_type(img)(img.width, img.height,
+                            _to_host_raster(y[0], (3, img.height, img.width), alloc))
+
+
+def combine_slices(base, fs, alloc=None):
+    """base + sum of the maps j = c, c+3, ... onto channel c (transform.py:181-193)."""
+    from . import device
+
+    if fs.k % 3 != 0:
+        raise BadGridCount(f"grid count {fs.k} is not a multiple of 3")
+    if tuple(fs.data.shape[1:]) != (base.height, base.width):
+        raise DimensionMismatch("feature map size differs from image size")
+    y = device.combine_slices(_to_dev(base.data)[None], _to_dev(fs.data)[None])
+    return _image_type(base)(base.width, base.height,
+                             _to_host_raster(y[0], (3, base.height, base.width), alloc))
+
+
+def naive_enhance(img, luts, lut_weights, grids, grid_weights, alloc=None):
+    """Slice, transform, then combine (transform.py:196-212): the multi-stage
+    composition with every intermediate raster materialized (on the device)."""
+    from . import device
+
+    if grids.k % 3 != 0:
+        raise BadGridCount(f"grid count {grids.k} is not a multiple of 3")
+    if img.width < 2 or img.height < 2:
+        raise DegenerateImage("slicing needs at least 2 px in each direction")
+    if grid_weights.k != grids.k:
+        raise DimensionMismatch(f"{grids.k} grids but {grid_weights.k} weight rows")
+    x = _to_dev(img.data)[None]
+    fs = device.slice_grids(x, _to_dev(grids.planes)[None], _to_dev(grid_weights.w)[None],
+                            _to_dev(grid_weights.b)[None])
+    base = device.apply_lut2d(x, _to_dev(luts.planes)[None], _to_dev(lut_weights.w)[None],
+                              _to_dev(lut_weights.b)[None])
+    y = device.combine_slices(base, fs)
+    return _image_type(img)(img.width, img.height,
+                            _to_host_raster(y[0], (3, img.height, img.width), alloc))
+
+
+def apply_lut3d(img, lut, alloc=None):
+    """Trilinear 3D LUT transform, one cube per output channel (transform.py:93-120)."""
+    from . import device
+
+    y = device.apply_lut3d(_to_dev(img.data)[None], _to_dev(lut.tables)[None])
+    return _image_type(img)(img.width, img.height,
+                            _to_host_raster(y[0], (3, img.height, img.width), alloc))

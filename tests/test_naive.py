@@ -1,0 +1,128 @@
+"""Multi-pass "original structure" (slice_grid2d, apply_lut2d, combine_slices,
+naive_enhance) and the 3D-LUT baseline (apply_lut3d): the numpy oracle and the
+GPU kernels (svdlut_naive.cu) against outputs of the reference itself
+(tests/golden/make_naive_golden.py).  All bit-exact."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, make_inputs
+
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+from make_naive_golden import LUT3D_CASES, NAIVE_CASES, lut3d_inputs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ngold():
+    return np.load(os.path.join(ROOT, "tests", "golden", "naive_golden.npz"))
+
+
+def _case(entry):
+    name, w, h, dt, ds, k, seed, lo, hi = entry
+    return name, make_inputs(w, h, d_t=dt, d_s=ds, k=k, seed=seed, low=lo, high=hi)
+
+
+@pytest.mark.parametrize("entry", NAIVE_CASES, ids=[c[0] for c in NAIVE_CASES])
+def test_oracle_naive_stages_match_reference(ngold, entry):
+    from oracle import naive
+
+    name, c = _case(entry)
+    fs = naive.slice_grids(c["rgb"], c["gp"], c["gw"], c["gb"])
+    base = naive.apply_lut2d(c["rgb"], c["lp"], c["lw"], c["lb"])
+    assert np.array_equal(fs, ngold[f"{name}_fs"])
+    assert np.array_equal(base, ngold[f"{name}_base"])
+    assert np.array_equal(naive.combine_slices(base, fs), ngold[f"{name}_out"])
+
+
+@pytest.mark.parametrize("entry", LUT3D_CASES, ids=[c[0] for c in LUT3D_CASES])
+def test_oracle_lut3d_matches_reference(ngold, entry):
+    from oracle import naive
+
+    name, w, h, d, seed, lo, hi = entry
+    rgb, cubes = lut3d_inputs(w, h, d, seed, lo, hi)
+    assert np.array_equal(naive.apply_lut3d(rgb, cubes), ngold[f"{name}_out"])
+
+
+def test_naive_errors_before_compute():
+    """The reference's validation order (transform.py:160-163, :185-188,
+    :206-207) — raised on the host, no GPU needed."""
+    from paper_2508_16121_b200 import transform
+    from paper_2508_16121_b200.core_types import (GridSet, GridWeights, Image, Lut2DSet,
+                                                  LutWeights, SpatialFeatureMap)
+    from paper_2508_16121_b200.errors import BadGridCount, DegenerateImage, DimensionMismatch
+
+    c = make_inputs(8, 6, k=6)
+    img = Image(8, 6, c["rgb"])
+    luts, lw = Lut2DSet(c["lp"]), LutWeights(c["lw"], c["lb"])
+    with pytest.raises(BadGridCount):
+        transform.naive_enhance(img, luts, lw, GridSet(c["gp"][:4]), GridWeights(c["gw"][:4], c["gb"][:4]))
+    with pytest.raises(DegenerateImage):
+        transform.slice_grid2d(Image(1, 6, c["rgb"][:, :, :1]), GridSet(c["gp"]),
+                               GridWeights(c["gw"], c["gb"]))
+    with pytest.raises(DimensionMismatch):
+        transform.slice_grid2d(img, GridSet(c["gp"]), GridWeights(c["gw"][:3], c["gb"][:3]))
+    with pytest.raises(BadGridCount):
+        transform.combine_slices(img, SpatialFeatureMap(np.zeros((4, 6, 8), np.float32)))
+    with pytest.raises(DimensionMismatch):
+        transform.combine_slices(img, SpatialFeatureMap(np.zeros((6, 5, 8), np.float32)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("entry", NAIVE_CASES, ids=[c[0] for c in NAIVE_CASES])
+def test_gpu_naive_stages_bit_exact(ngold, entry):
+    import __graft_entry__
+    from paper_2508_16121_b200 import transform
+    from paper_2508_16121_b200.core_types import GridSet, GridWeights, Image, Lut2DSet, LutWeights
+
+    __graft_entry__.build_library()
+    name, c = _case(entry)
+    h, w = c["rgb"].shape[1:]
+    img = Image(w, h, c["rgb"])
+    luts, lw = Lut2DSet(c["lp"]), LutWeights(c["lw"], c["lb"])
+    grids, gw = GridSet(c["gp"]), GridWeights(c["gw"], c["gb"])
+    fs = transform.slice_grid2d(img, grids, gw)
+    base = transform.apply_lut2d(img, luts, lw)
+    assert np.array_equal(fs.data, ngold[f"{name}_fs"])
+    assert np.array_equal(base.data, ngold[f"{name}_base"])
+    assert np.array_equal(transform.combine_slices(base, fs).data, ngold[f"{name}_out"])
+    assert np.array_equal(transform.naive_enhance(img, luts, lw, grids, gw).data, ngold[f"{name}_out"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("entry", LUT3D_CASES, ids=[c[0] for c in LUT3D_CASES])
+def test_gpu_lut3d_bit_exact(ngold, entry):
+    import __graft_entry__
+    from paper_2508_16121_b200 import transform
+    from paper_2508_16121_b200.core_types import Image, Lut3D
+
+    __graft_entry__.build_library()
+    name, w, h, d, seed, lo, hi = entry
+    rgb, cubes = lut3d_inputs(w, h, d, seed, lo, hi)
+    y = transform.apply_lut3d(Image(w, h, rgb), Lut3D(cubes))
+    assert np.array_equal(y.data, ngold[f"{name}_out"])
+
+
+@pytest.mark.gpu
+def test_gpu_naive_strip_and_batch_match_oracle():
+    """Row strips (y0, h_total) and batches through the device API."""
+    import torch
+
+    import __graft_entry__
+    from oracle import naive
+    from paper_2508_16121_b200 import device
+
+    __graft_entry__.build_library()
+    c = make_inputs(50, 40, d_t=17, d_s=9, k=6, seed=9)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    fs_full = naive.slice_grids(c["rgb"], c["gp"], c["gw"], c["gb"])
+    fs_strip = device.slice_grids(T(c["rgb"][:, 15:33])[None], T(c["gp"])[None], T(c["gw"])[None],
+                                  T(c["gb"])[None], y0=15, h_total=40)
+    assert np.array_equal(fs_strip[0].cpu().numpy(), fs_full[:, 15:33])
+    x2 = T(np.stack([c["rgb"], c["rgb"][:, ::-1].copy()]))
+    y = device.apply_lut2d(x2, T(np.stack([c["lp"]] * 2)), T(np.stack([c["lw"]] * 2)),
+                           T(np.stack([c["lb"]] * 2)))
+    assert np.array_equal(y[1].cpu().numpy(),
+                          naive.apply_lut2d(c["rgb"][:, ::-1].copy(), c["lp"], c["lw"], c["lb"]))
