@@ -25,6 +25,8 @@
  *   svdlut_apply_lut3d        transform.apply_lut3d    (transform.py:93-120)
  *                             (the multi-pass "original structure" and the 3D-LUT
  *                             baseline, bitwise equal to the reference)
+ *   svdlut_occurrence         analysis.occurrence_stats (analysis.py:109-122), the
+ *                             source of utilization_rate (analysis.py:74-106)
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  `stream` is a
@@ -205,6 +207,12 @@ int svdlut_combine_slices(const float* base, const float* fs, int batch, int h, 
 /* out (B, 3, H, W): trilinear 3D LUT, cubes (B, 3, d, d, d) [c][r][g][b]. */
 int svdlut_apply_lut3d(const float* rgb, int batch, int h, int w, const float* cubes, int d,
                        float* out, void* stream);
+
+/* cube (d, d, d) u64, zeroed then filled: how often each cube vertex is a
+ * corner of some pixel's bracketing cell, over a batch of (B, 3, H, W) images
+ * (exact counts). */
+int svdlut_occurrence(const float* rgb, int batch, int h, int w, int d, unsigned long long* cube,
+                      void* stream);
 
 /* svdlut_enhance_host with sample formats (fast kernel only): e.g. a PNM
  * payload in, a PNM payload out — 6 B/pixel over PCIe instead of 24 (U8). */

@@ -100,3 +100,14 @@ def _blend_rg(cube, ir, dr, ig, dg, ib):
     out = out + cube[ir + 1, ig, ib] * (dr * (1 - dg))
     out = out + cube[ir, ig + 1, ib] * ((1 - dr) * dg)
     return out + cube[ir + 1, ig + 1, ib] * (dr * dg)
+
+
+def occurrence(rgb, d):
+    """analysis.occurrence_stats (analysis.py:109-122) for one image: int64 cube
+    of bracketing-cell corner touches."""
+    ir, ig, ib = (bracket_array(rgb[c], d)[0].astype(np.int64) for c in range(3))
+    flat = np.zeros(d ** 3, np.int64)
+    base = ((ir * d + ig) * d + ib).ravel()
+    for corner in range(8):
+        np.add.at(flat, base + ((corner >> 2) * d + ((corner >> 1) & 1)) * d + (corner & 1), 1)
+    return flat.reshape(d, d, d)

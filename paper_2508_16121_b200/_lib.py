@@ -52,6 +52,7 @@ _SIGS = {
     "svdlut_apply_lut2d": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp]),
     "svdlut_combine_slices": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "svdlut_apply_lut3d": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp]),
+    "svdlut_occurrence": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "svdlut_fused_fwd_io": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _i, _vp, _vp]),
     "svdlut_enhance_host_io": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,
                                     _vp, _i, ctypes.POINTER(_i)]),

@@ -347,6 +347,16 @@ int svdlut_apply_lut3d(const float* rgb, int batch, int h, int w, const float* c
   return SVDLUT_OK;
 }
 
+int svdlut_occurrence(const float* rgb, int batch, int h, int w, int d, unsigned long long* cube,
+                      void* stream) {
+  if (batch < 0 || h < 0 || w < 0) return fail(SVDLUT_ERR_DIMENSION_MISMATCH, "negative size");
+  if (d < 2) return fail(SVDLUT_ERR_BAD_VERTEX_COUNT, "need at least 2 vertices, got %d", d);
+  if (d > 1024) return fail(SVDLUT_ERR_UNSUPPORTED, "cube too large (d=%d)", d);
+  if (!cube || (!rgb && (long long)batch * h * w > 0)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  CUDA_TRY(launch_occurrence(rgb, batch, h, w, d, cube, (cudaStream_t)stream), "occurrence");
+  return SVDLUT_OK;
+}
+
 int svdlut_reconstruct_bwd(const float* u, const float* s, const float* vt,
                            const float* dplanes, int batch, int d_t, int n_s, float* du,
                            float* ds, float* dvt, void* stream) {

@@ -47,6 +47,10 @@ cudaError_t launch_combine(const float* base, const float* fs, float* out, int b
 cudaError_t launch_lut3d(const float* rgb, float* out, int batch, int h, int w, const float* cubes,
                          int d, cudaStream_t st);
 
+// analysis.occurrence_stats: u64 corner-touch counts of a d^3 cube (zeroed first)
+cudaError_t launch_occurrence(const float* rgb, int batch, int h, int w, int d, unsigned long long* cube,
+                              cudaStream_t st);
+
 cudaError_t launch_indices(const float* rgb, int batch, int h, int w, int y0, int h_total,
                            int dt, int ds, int32_t* idx, cudaStream_t st);
 

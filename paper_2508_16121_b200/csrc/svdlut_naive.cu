@@ -204,4 +204,82 @@ cudaError_t launch_lut3d(const float* rgb, float* out, int batch, int h, int w, 
   return cudaGetLastError();
 }
 
+// ---- analysis.occurrence_stats (analysis.py:109-122): corner-touch histogram ----
+// Every pixel touches the 8 corners of its bracketing cell (left indices of
+// interp.bracket_array per channel).  Counts are exact integers: a per-CTA
+// shared-memory int32 histogram (d^3 <= kOccSmemMax entries), flushed once to
+// the global u64 cube; larger cubes count straight into global memory.  Lane l
+// of a warp walks pixels span + l*kOccRun + j (j < kOccRun), so the 32 lanes
+// of one atomic instruction sit kOccRun pixels apart and rarely hit the same
+// address (shared atomics serialize same-address lanes); a lane's consecutive
+// pixels share 32-byte sectors through L1.
+namespace svdlut {
+
+constexpr int kOccRun = 32;
+constexpr int kOccSmemMax = 48 * 1024;  // int32 entries (192 KB)
+
+__device__ __forceinline__ int left_index(float p, int d) {
+  p = fminf(fmaxf(p, 0.0f), 1.0f);
+  return (int)fminf(floorf(__fmul_rn(p, (float)(d - 1))), (float)(d - 2));
+}
+
+__global__ void occurrence_kernel(const float* __restrict__ rgb, int batch, long long plane, int d,
+                                  unsigned long long* __restrict__ cube, int use_smem) {
+  extern __shared__ int hist[];
+  const int n3 = d * d * d;
+  if (use_smem) {
+    for (int i = threadIdx.x; i < n3; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+  }
+  const long long total = (long long)batch * plane;
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long span = 32LL * kOccRun;
+  for (long long s = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * span; s < total;
+       s += warps * span) {
+    for (int j = 0; j < kOccRun; ++j) {
+      const long long e = s + (long long)lane * kOccRun + j;
+      if (e >= total) break;
+      const long long b = e / plane, o = e - b * plane;
+      const float* X = rgb + b * 3 * plane + o;
+      const int ir = left_index(__ldg(X), d), ig = left_index(__ldg(X + plane), d),
+                ib = left_index(__ldg(X + 2 * plane), d);
+      const int base = (ir * d + ig) * d + ib;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int idx = base + ((c >> 2) * d + ((c >> 1) & 1)) * d + (c & 1);
+        if (use_smem) atomicAdd(&hist[idx], 1);
+        else atomicAdd(&cube[idx], 1ull);
+      }
+    }
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < n3; i += blockDim.x)
+      if (hist[i]) atomicAdd(&cube[i], (unsigned long long)hist[i]);
+  }
+}
+
+cudaError_t launch_occurrence(const float* rgb, int batch, int h, int w, int d, unsigned long long* cube,
+                              cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(cube, 0, sizeof(unsigned long long) * d * d * d, st);
+  if (e != cudaSuccess) return e;
+  const long long total = (long long)batch * h * w;
+  if (total == 0) return cudaSuccess;
+  const int n3 = d * d * d;
+  const int use_smem = n3 <= kOccSmemMax;
+  const size_t smem = use_smem ? (size_t)n3 * 4 : 0;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(occurrence_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long spans = (total + 32LL * kOccRun * 16 - 1) / (32LL * kOccRun * 16);
+  const int grid = (int)(spans < sms ? (spans < 1 ? 1 : spans) : sms);
+  occurrence_kernel<<<grid, 512, smem, st>>>(rgb, batch, (long long)h * w, d, cube, use_smem);
+  return cudaGetLastError();
+}
+
 }  // namespace svdlut

@@ -126,3 +126,46 @@ def test_gpu_naive_strip_and_batch_match_oracle():
                            T(np.stack([c["lb"]] * 2)))
     assert np.array_equal(y[1].cpu().numpy(),
                           naive.apply_lut2d(c["rgb"][:, ::-1].copy(), c["lp"], c["lw"], c["lb"]))
+
+
+from make_naive_golden import ANALYSIS_CASES, analysis_image  # noqa: E402
+
+
+@pytest.mark.parametrize("entry", ANALYSIS_CASES, ids=[c[0] for c in ANALYSIS_CASES])
+def test_oracle_occurrence_matches_reference(ngold, entry):
+    from oracle import naive
+
+    name, w, h, seed, d, lo, hi, smooth = entry
+    cube = naive.occurrence(analysis_image(w, h, seed, lo, hi, smooth), d)
+    assert np.array_equal(cube, ngold[f"{name}_cube"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("entry", ANALYSIS_CASES, ids=[c[0] for c in ANALYSIS_CASES])
+def test_gpu_occurrence_and_utilization_exact(ngold, entry):
+    import __graft_entry__
+    from paper_2508_16121_b200 import analysis
+    from paper_2508_16121_b200.core_types import Image
+
+    __graft_entry__.build_library()
+    name, w, h, seed, d, lo, hi, smooth = entry
+    img = Image(w, h, analysis_image(w, h, seed, lo, hi, smooth))
+    occ = analysis.occurrence_stats([img, img], d)
+    assert np.array_equal(occ.cube, 2 * ngold[f"{name}_cube"])
+    assert occ.total == 2 * 8 * w * h
+    util = [analysis.utilization_rate(img, d, m) for m in ("1d", "2d", "3d")]
+    assert util == list(ngold[f"{name}_util"])
+
+
+@pytest.mark.gpu
+def test_gpu_image_metrics(ngold):
+    import __graft_entry__
+    from paper_2508_16121_b200 import analysis
+    from paper_2508_16121_b200.core_types import Image
+
+    __graft_entry__.build_library()
+    a = Image(40, 30, analysis_image(40, 30, 11, 0.0, 1.0, False))
+    b = Image(40, 30, analysis_image(40, 30, 12, -0.1, 1.1, False))
+    assert abs(analysis.psnr(a, b) - float(ngold["an_psnr"])) <= 1e-9 * abs(float(ngold["an_psnr"]))
+    assert abs(analysis.delta_e_ab(a, b) - float(ngold["an_delta_e"])) <= 1e-9 * float(ngold["an_delta_e"])
+    assert analysis.psnr(a, a) == float("inf")
