@@ -213,8 +213,6 @@ cudaError_t launch_lut3d(const float* rgb, float* out, int batch, int h, int w, 
 // of one atomic instruction sit kOccRun pixels apart and rarely hit the same
 // address (shared atomics serialize same-address lanes); a lane's consecutive
 // pixels share 32-byte sectors through L1.
-namespace svdlut {
-
 constexpr int kOccRun = 32;
 constexpr int kOccSmemMax = 48 * 1024;  // int32 entries (192 KB)
 
