@@ -406,7 +406,7 @@ def run_secondary(a):
     import __graft_entry__
 
     __graft_entry__.build_library()
-    from paper_2508_16121_b200 import device, parallel, synth
+    from paper_2508_16121_b200 import autograd, device, parallel, synth
 
     T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
     keys = ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")
@@ -429,7 +429,8 @@ def run_secondary(a):
         case = synth.make_batch(list(range(lo, hi)), h=1080, w=1920)
         h, w, units = 1080, 1920, (hi - lo)
         desc = (f"config5: training step on 8 x 3x1080x1920 (per-image shards, {hi - lo} per rank): "
-                f"forward + L2 loss vs X^0.8 + backward (gX, dU/dS/dVt, grids, weights)")
+                f"forward with the L2 loss vs X^0.8 fused in its epilogue + backward (gX, dU/dS/dVt, "
+                f"grids, weights; autograd.l2_step)")
     rgb = T(case.rgb)
     prm = {k: T(getattr(case, k)) for k in keys}
     y0_strip = parallel.strip_rows(4320, world, rank)[0] if a.config == 4 else 0
@@ -444,13 +445,9 @@ def run_secondary(a):
                                                 prm["grid_planes"], prm["gw"], prm["gb"])
             device.apply(rgb, tables, out=out, y0=y0_strip, h_total=h_total)
             return
-        planes = device.reconstruct(prm["u"], prm["s"], prm["vt"])
-        tables = device.pack_tables(planes, prm["lw"], prm["lb"], prm["grid_planes"], prm["gw"],
-                                    prm["gb"])
-        y = device.apply(rgb, tables, out=out)
-        gy = (y - target).mul_(2.0 / y.numel())
-        g = device.fused_backward(rgb, gy, planes, prm["lw"], prm["grid_planes"], prm["gw"])
-        device.reconstruct_backward(prm["u"], prm["s"], prm["vt"], g["dlut_planes"])
+        # fused training step: the L2 loss lives in the forward's epilogue
+        autograd.l2_step(rgb, target, prm["u"], prm["s"], prm["vt"], prm["lw"], prm["lb"],
+                         prm["grid_planes"], prm["gw"], prm["gb"])
 
     graph = None
     if not a.no_graph:

@@ -25,6 +25,8 @@
  *   svdlut_apply_lut3d        transform.apply_lut3d    (transform.py:93-120)
  *                             (the multi-pass "original structure" and the 3D-LUT
  *                             baseline, bitwise equal to the reference)
+ *   svdlut_fused_fwd_l2       forward + L2 loss epilogue (training step, config 5)
+ *   svdlut_fused_bwd_packed   svdlut_fused_bwd reusing the forward's tables / max|gY|
  *   svdlut_occurrence         analysis.occurrence_stats (analysis.py:109-122), the
  *                             source of utilization_rate (analysis.py:74-106)
  *
@@ -207,6 +209,25 @@ int svdlut_combine_slices(const float* base, const float* fs, int batch, int h, 
 /* out (B, 3, H, W): trilinear 3D LUT, cubes (B, 3, d, d, d) [c][r][g][b]. */
 int svdlut_apply_lut3d(const float* rgb, int batch, int h, int w, const float* cubes, int d,
                        float* out, void* stream);
+
+/* Training step, forward half: gy = (Y - target) * gscale (f32 planar, as
+ * rgb), loss_sum[b] = sum over image b of (Y - target)^2 (f64), gmax[b] =
+ * max |gy| of image b — the scale the backward's fixed-point scatter needs.
+ * With gscale = 2 / (B*3*H*W), gy is d mean((Y - T)^2) / dY. */
+int svdlut_fused_fwd_l2(const float* rgb, const float* target, int batch, int h, int w, int y0,
+                        int h_total, const void* tables, int d_t, int d_s, float* gy, double* loss_sum,
+                        float* gmax, float gscale, void* stream);
+
+/* svdlut_fused_bwd with optional packed `tables` (from svdlut_pack_tables*,
+ * biases are irrelevant to the backward) and optional per-image `gmax`
+ * (>= max |gy|, e.g. from svdlut_fused_fwd_l2); NULL recomputes either. */
+int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h, int w, int y0,
+                            int h_total, const void* tables, const float* gmax,
+                            const float* lut_planes, const float* lw, int d_t,
+                            const float* grid_planes, const float* gw, int k, int d_s, float* gx,
+                            float* dlut_planes, float* dlw, float* dlb, float* dgrid_planes,
+                            float* dgw, float* dgb, void* workspace, size_t workspace_bytes,
+                            void* stream);
 
 /* cube (d, d, d) u64, zeroed then filled: how often each cube vertex is a
  * corner of some pixel's bracketing cell, over a batch of (B, 3, H, W) images

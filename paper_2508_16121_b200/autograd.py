@@ -15,7 +15,7 @@ import torch
 
 from . import device
 
-__all__ = ["SvdLutApply", "svdlut_apply"]
+__all__ = ["SvdLutApply", "svdlut_apply", "l2_step"]
 
 
 class SvdLutApply(torch.autograd.Function):
@@ -50,3 +50,22 @@ class SvdLutApply(torch.autograd.Function):
 
 def svdlut_apply(rgb, u, s, vt, lw, lb, grid_planes, gw, gb, y0=0, h_total=None):
     return SvdLutApply.apply(rgb, u, s, vt, lw, lb, grid_planes, gw, gb, y0, h_total)
+
+
+def l2_step(rgb, target, u, s, vt, lw, lb, grid_planes, gw, gb, need_gx=True):
+    """One training step of mean((Y - target)^2) without autograd overhead
+    (BASELINE config 5): tables from the factors, the forward with the loss
+    fused into its epilogue (Y never hits HBM; gY and max|gY| come out of the
+    same kernel), the backward reusing the forward's tables and max|gY|, and
+    the factor gradients.  Returns a dict with the scalar ``loss`` (float64
+    tensor) and the gradients keyed like SvdLutApply's inputs.
+    """
+    planes = device.reconstruct(u, s, vt)
+    tables = device.pack_tables(planes, lw, lb, grid_planes, gw, gb)
+    gy, loss_sum, gmax = device.apply_l2(rgb, target, tables)
+    g = device.fused_backward(rgb, gy, planes, lw, grid_planes, gw, need_gx=need_gx, tables=tables,
+                              gmax=gmax)
+    du, ds, dvt = device.reconstruct_backward(u, s, vt, g["dlut_planes"])
+    return {"loss": loss_sum.sum() / rgb.numel(), "gx": g["gx"], "u": du, "s": ds, "vt": dvt,
+            "lw": g["dlw"], "lb": g["dlb"], "grid_planes": g["dgrid_planes"], "gw": g["dgw"],
+            "gb": g["dgb"]}

@@ -590,7 +590,8 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
                              int h_total, const float* lp, const float* lw, int dt,
                              const float* gp, const float* gw, int k, int ds, float* gx,
                              float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
-                             float* dgb, void* ws, size_t ws_bytes, cudaStream_t st) {
+                             float* dgb, void* ws, size_t ws_bytes, cudaStream_t st,
+                             const float* tables_in, const float* gmax_in) {
   (void)ws_bytes;
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
@@ -607,8 +608,10 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   float* gmax = (float*)wp;
   cudaError_t e;
   if ((e = cudaMemsetAsync(zb, 0, (size_t)batch * (3 + k) * 4, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(gmax, 0, (size_t)batch * 4, st)) != cudaSuccess) return e;
-  {
+  if (gmax_in) {
+    gmax = const_cast<float*>(gmax_in);  // caller-provided bound on max |gY| per image
+  } else {
+    if ((e = cudaMemsetAsync(gmax, 0, (size_t)batch * 4, st)) != cudaSuccess) return e;
     const long long per = 3LL * h * w;
     long long blocks = (per / 4 + 255) / 256;
     if (blocks > 512) blocks = 512;
@@ -618,9 +621,12 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if ((e = cudaMemsetAsync(E, 0, (size_t)batch * A.total * 4, st)) != cudaSuccess) return e;
-  if ((e = launch_pack(lp, nullptr, nullptr, nullptr, 0, lw, zb, gp, gw, zb + 3 * batch, k, L, batch,
-                       tables, st)) != cudaSuccess)
+  if (tables_in) {
+    tables = const_cast<float*>(tables_in);  // forward tables: biases do not enter the backward
+  } else if ((e = launch_pack(lp, nullptr, nullptr, nullptr, 0, lw, zb, gp, gw, zb + 3 * batch, k, L,
+                              batch, tables, st)) != cudaSuccess) {
     return e;
+  }
   BwdParams p;
   p.rgb = rgb;
   p.gy = gy;

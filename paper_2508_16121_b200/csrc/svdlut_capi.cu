@@ -357,6 +357,56 @@ int svdlut_occurrence(const float* rgb, int batch, int h, int w, int d, unsigned
   return SVDLUT_OK;
 }
 
+int svdlut_fused_fwd_l2(const float* rgb, const float* target, int batch, int h, int w, int y0,
+                        int h_total, const void* tables, int d_t, int d_s, float* gy, double* loss_sum,
+                        float* gmax, float gscale, void* stream) {
+  int rc;
+  if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
+  if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
+  if (!svdlut_fast_supported(d_t, d_s))
+    return fail(SVDLUT_ERR_UNSUPPORTED, "tables for d_t=%d d_s=%d exceed shared memory", d_t, d_s);
+  if (!loss_sum || !gmax) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(loss_sum, 0, sizeof(double) * (size_t)batch, st), "fused_fwd_l2");
+  CUDA_TRY(cudaMemsetAsync(gmax, 0, sizeof(float) * (size_t)batch, st), "fused_fwd_l2");
+  if ((long long)batch * h * w == 0) return SVDLUT_OK;
+  if (!rgb || !target || !tables || !gy) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
+  const TableLayout L = TableLayout::make(d_t, d_s);
+  CUDA_TRY(launch_fused_fwd_l2(rgb, target, gy, batch, h, w, y0, h_total, (const float*)tables, L,
+                               loss_sum, gmax, gscale, st),
+           "fused forward + L2 loss");
+  return SVDLUT_OK;
+}
+
+int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h, int w, int y0,
+                            int h_total, const void* tables, const float* gmax,
+                            const float* lut_planes, const float* lw, int d_t,
+                            const float* grid_planes, const float* gw, int k, int d_s, float* gx,
+                            float* dlut_planes, float* dlw, float* dlb, float* dgrid_planes,
+                            float* dgw, float* dgb, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  int rc;
+  if ((rc = check_k(k)) != SVDLUT_OK) return rc;
+  if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
+  if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
+  if (w > 32767)
+    return fail(SVDLUT_ERR_UNSUPPORTED, "backward rows are limited to 32767 pixels (got %d)", w);
+  if (batch == 0) return SVDLUT_OK;
+  if (!rgb || !gy || !lut_planes || !lw || !grid_planes || !gw || !dlut_planes || !dlw || !dlb ||
+      !dgrid_planes || !dgw || !dgb)
+    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (tables && !aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
+  const size_t need = bwd_workspace_bytes(batch, h, w, d_t, d_s, k);
+  if (!workspace || workspace_bytes < need)
+    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "workspace too small (%zu < %zu)", workspace_bytes, need);
+  CUDA_TRY(launch_fused_bwd(rgb, gy, batch, h, w, y0, h_total, lut_planes, lw, d_t, grid_planes, gw, k,
+                            d_s, gx, dlut_planes, dlw, dlb, dgrid_planes, dgw, dgb, workspace,
+                            workspace_bytes, (cudaStream_t)stream, (const float*)tables, gmax),
+           "fused backward");
+  return SVDLUT_OK;
+}
+
 int svdlut_reconstruct_bwd(const float* u, const float* s, const float* vt,
                            const float* dplanes, int batch, int d_t, int n_s, float* du,
                            float* ds, float* dvt, void* stream) {

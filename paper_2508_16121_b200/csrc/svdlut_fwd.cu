@@ -74,6 +74,13 @@ struct FwdParams {
   double rcp_w;             // RN64(1 / (W - 1)) for the exact column brackets
   double rcp_h;             // RN64(1 / (h_total - 1)) for the row brackets
   int* nonfinite;
+  // OUT == kL2Grad (fused L2 loss): target image (f32 planar, like the input),
+  // per-image sum of squared residuals (f64) and max |gY| (f32 bits), and the
+  // gradient scale 2 / N of mean((Y - T)^2)
+  const float* target;
+  double* loss;
+  float* gmax;
+  float gscale;
   int col_smem;             // 1: column brackets come from a per-CTA smem table of t values
 };
 
@@ -217,7 +224,11 @@ __host__ __device__ inline uint32_t smem_tables_bytes(const TableLayout& L) {
 
 template <int DT, int DS, bool CHECK, int PX, int NW, int IN, int OUT>
 __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
-  static_assert(PX == 4 || (IN == kF32 && OUT == kF32), "integer formats use 4-pixel lanes");
+  static_assert(PX == 4 || (IN == kF32 && (OUT == kF32 || OUT == kL2Grad)),
+                "integer formats use 4-pixel lanes");
+  constexpr bool LOSS = OUT == kL2Grad;
+  constexpr int OUTF = LOSS ? (int)kF32 : OUT;  // storage format of the output
+  float loss_acc = 0.f, gmax_acc = 0.f;         // LOSS: this thread's partials
   constexpr int CH = 32 * PX;  // pixels per warp chunk
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar_storage;
@@ -294,7 +305,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const long long pl = p.pl_in, opl = p.pl_out;  // plane strides (floats)
   const long long plane_len = (long long)p.h * p.w;
   const bool vec_in = ((p.w & 3) == 0) && Src<IN>::aligned(p.in, pl);
-  const bool vec_out = ((p.w & 3) == 0) && Dst<OUT>::aligned(p.out, opl);
+  const bool vec_out = ((p.w & 3) == 0) && Dst<OUTF>::aligned(p.out, opl) &&
+                       (!LOSS || Src<kF32>::aligned(p.target, pl));
   uint32_t phase = 0;
   uint32_t nrow = 0;  // CTA row ordinal (slot ring position)
   bool bad = false;
@@ -319,7 +331,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         bulk_g2s(sbase + lut_smem_bytes + off, gsrc + off, min(32768u, gbytes - off), bar);
     }
     const void* src = Src<IN>::image(p.in, b, pl);
-    void* dst = Dst<OUT>::image(p.out, b, opl);
+    void* dst = Dst<OUTF>::image(p.out, b, opl);
+    const void* tsrc = LOSS ? Src<kF32>::image(p.target, b, pl) : nullptr;
     // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
@@ -337,11 +350,15 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       }
     };
     // the first chunk's loads overlap the table copy
-    ChunkIn<PX> cur;
+    ChunkIn<PX> cur, tgt;
     int cur_y = y_first, cur_k = klo(y_first) + warp;
     settle(cur_y, cur_k);
-    if (cur_y <= y_last)
+    if (cur_y <= y_last) {
       Src<IN>::template load<PX>(src, pl, cur_y, cur_k * CH + PX * lane, p.w, vec_in, cur.r, cur.g, cur.b);
+      if (LOSS)
+        Src<kF32>::template load<PX>(tsrc, pl, cur_y, cur_k * CH + PX * lane, p.w, vec_out, tgt.r, tgt.g,
+                                     tgt.b);
+    }
     mbar_wait(bar, phase);
     phase ^= 1u;
     // This warp's share of the slots of row y (CTA row ordinal n) into ring
@@ -368,8 +385,14 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       const uint32_t n = n0 + (uint32_t)(y - y_first);
       if (FWD_L2PF > 0 && threadIdx.x == blockDim.x - 32) {
         if (y == y_first)
-          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) Src<IN>::prefetch_row(src, pl, plane_len, yy, p.w);
-        if (y + FWD_L2PF <= y_last) Src<IN>::prefetch_row(src, pl, plane_len, y + FWD_L2PF, p.w);
+          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) {
+            Src<IN>::prefetch_row(src, pl, plane_len, yy, p.w);
+            if (LOSS) Src<kF32>::prefetch_row(tsrc, pl, plane_len, yy, p.w);
+          }
+        if (y + FWD_L2PF <= y_last) {
+          Src<IN>::prefetch_row(src, pl, plane_len, y + FWD_L2PF, p.w);
+          if (LOSS) Src<kF32>::prefetch_row(tsrc, pl, plane_len, y + FWD_L2PF, p.w);
+        }
       }
       mbar_wait(full0 + 8u * (n % kRing), (n / kRing) & 1u);
       const uint32_t slotK = slotK0 + (n % kRing) * slot_row_bytes;
@@ -473,12 +496,30 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           o2[u] = acc2 + slot_term(s2, ex, eb);
           if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
         }
-        Dst<OUT>::template store<PX>(dst, opl, cur_y, xl, p.w, vec_out, o0, o1, o2);
+        if (LOSS) {  // gY = (Y - T) * 2/N, loss partial, max |gY| (pixels past the row end excluded)
+#pragma unroll
+          for (int u = 0; u < PX; ++u) {
+            const bool in_row = xl + u < p.w;
+            const float r0 = o0[u] - tgt.r[u], r1 = o1[u] - tgt.g[u], r2 = o2[u] - tgt.b[u];
+            o0[u] = r0 * p.gscale;
+            o1[u] = r1 * p.gscale;
+            o2[u] = r2 * p.gscale;
+            if (in_row) {
+              loss_acc = __fmaf_rn(r0, r0, __fmaf_rn(r1, r1, __fmaf_rn(r2, r2, loss_acc)));
+              gmax_acc = fmaxf(gmax_acc, fmaxf(fabsf(o0[u]), fmaxf(fabsf(o1[u]), fabsf(o2[u]))));
+            }
+          }
+        }
+        Dst<OUTF>::template store<PX>(dst, opl, cur_y, xl, p.w, vec_out, o0, o1, o2);
 #if FWD_REGPF
         cur = nxt;
 #else
-        if (nxt_y <= y_last)
+        if (nxt_y <= y_last) {
           Src<IN>::template load<PX>(src, pl, nxt_y, nxt_k * CH + PX * lane, p.w, vec_in, cur.r, cur.g, cur.b);
+          if (LOSS)
+            Src<kF32>::template load<PX>(tsrc, pl, nxt_y, nxt_k * CH + PX * lane, p.w, vec_out, tgt.r,
+                                         tgt.g, tgt.b);
+        }
 #endif
         cur_y = nxt_y;
         cur_k = nxt_k;
@@ -494,6 +535,19 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     }
     nrow = n0 + (uint32_t)cnt;
     r += y_last - y_first + 1;
+    if (LOSS) {  // this image's partials: warp reduction, one atomic per warp
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, off);
+        gmax_acc = fmaxf(gmax_acc, __shfl_xor_sync(0xffffffffu, gmax_acc, off));
+      }
+      if (lane == 0) {
+        atomicAdd(p.loss + b, (double)loss_acc);
+        atomicMax(reinterpret_cast<int*>(p.gmax) + b, __float_as_int(gmax_acc));  // gmax >= 0
+      }
+      loss_acc = 0.f;
+      gmax_acc = 0.f;
+    }
   }
   if (CHECK) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.nonfinite, 1);
@@ -687,10 +741,30 @@ cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int
                              st, pl_in, pl_out);
 }
 
+static cudaError_t launch_fwd_impl(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
+                                   int w, int y0, int h_total, const float* tables, const TableLayout& L,
+                                   int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out,
+                                   const float* target, double* loss, float* gmax, float gscale);
+
+cudaError_t launch_fused_fwd_l2(const float* rgb, const float* target, float* gy, int batch, int h, int w,
+                                int y0, int h_total, const float* tables, const TableLayout& L,
+                                double* loss, float* gmax, float gscale, cudaStream_t st) {
+  return launch_fwd_impl(rgb, kF32, gy, kL2Grad, batch, h, w, y0, h_total, tables, L, nullptr, st, 0, 0,
+                         target, loss, gmax, gscale);
+}
+
 cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
                                 int w, int y0, int h_total, const float* tables, const TableLayout& L,
                                 int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
   if (!fused_fwd_formats_supported(in_fmt, out_fmt)) return cudaErrorInvalidValue;
+  return launch_fwd_impl(in, in_fmt, out, out_fmt, batch, h, w, y0, h_total, tables, L, nonfinite, st,
+                         pl_in, pl_out, nullptr, nullptr, nullptr, 0.f);
+}
+
+static cudaError_t launch_fwd_impl(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
+                                   int w, int y0, int h_total, const float* tables, const TableLayout& L,
+                                   int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out,
+                                   const float* target, double* loss, float* gmax, float gscale) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (g_num_sms == 0) {
@@ -711,6 +785,10 @@ cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_f
   p.rcp_w = 1.0 / (double)(w - 1);
   p.rcp_h = 1.0 / (double)(h_total - 1);
   p.nonfinite = nonfinite;
+  p.target = target;
+  p.loss = loss;
+  p.gmax = gmax;
+  p.gscale = gscale;
   const long long rows = (long long)batch * h;
   if (rows == 0 || w == 0) return cudaSuccess;
   // texture over the whole batch of tables, base aligned down to textureAlignment
@@ -732,7 +810,9 @@ cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_f
   const bool chk = nonfinite != nullptr;
   const int g = (int)grid;
   const int fmt = in_fmt * 3 + out_fmt;
-  if (fmt == kF32 * 3 + kF32) {
+  if (out_fmt == kL2Grad) {
+    e = launch_fmt<kF32, kL2Grad>(p, L, chk, g, smem, st);
+  } else if (fmt == kF32 * 3 + kF32) {
     e = launch_fmt<kF32, kF32>(p, L, chk, g, smem, st);
   } else {
 #if FWD_PX == 4

@@ -29,6 +29,11 @@ cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_f
                                 int* nonfinite, cudaStream_t st, long long pl_in = 0,
                                 long long pl_out = 0);
 bool fused_fwd_formats_supported(int in_fmt, int out_fmt);
+// Fused forward + L2 loss epilogue: gy = (Y - target) * gscale (f32 planar),
+// loss[b] += sum (Y - T)^2 (f64), gmax[b] = max |gy| (both accumulated: zero them first).
+cudaError_t launch_fused_fwd_l2(const float* rgb, const float* target, float* gy, int batch, int h, int w,
+                                int y0, int h_total, const float* tables, const TableLayout& L,
+                                double* loss, float* gmax, float gscale, cudaStream_t st);
 
 cudaError_t launch_fused_exact(const float* rgb, float* out, int batch, int h, int w, int y0,
                                int h_total, const float* lp, const float* lw, const float* lb,
@@ -58,7 +63,8 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
                              int h_total, const float* lp, const float* lw, int dt,
                              const float* gp, const float* gw, int k, int ds, float* gx,
                              float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
-                             float* dgb, void* ws, size_t ws_bytes, cudaStream_t st);
+                             float* dgb, void* ws, size_t ws_bytes, cudaStream_t st,
+                             const float* tables_in = nullptr, const float* gmax_in = nullptr);
 size_t bwd_workspace_bytes(int batch, int h, int w, int dt, int ds, int k);
 
 cudaError_t launch_reconstruct_bwd(const float* u, const float* s, const float* vt,

@@ -26,7 +26,7 @@
 
 namespace svdlut {
 
-enum SampleFmt { kF32 = 0, kU8 = 1, kU16 = 2 };
+enum SampleFmt { kF32 = 0, kU8 = 1, kU16 = 2, kL2Grad = 3 /* f32 planar gY of a fused L2 loss */ };
 
 __host__ __device__ constexpr int fmt_bytes(int fmt) { return fmt == kF32 ? 4 : (fmt == kU8 ? 1 : 2); }
 

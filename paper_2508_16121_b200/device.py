@@ -23,7 +23,7 @@ from . import _lib
 from .errors import DimensionMismatch
 
 __all__ = [
-    "apply_io", "FMT_F32", "FMT_U8", "FMT_U16BE",
+    "apply_io", "FMT_F32", "FMT_U8", "FMT_U16BE", "apply_l2",
     "table_bytes", "fast_supported", "PackedTables", "reconstruct", "pack_tables",
     "pack_tables_factors", "apply",
     "apply_exact", "slice_grids", "apply_lut2d", "combine_slices", "apply_lut3d",
@@ -297,10 +297,37 @@ def indices(rgb, d_t, d_s, y0=0, h_total=None):
     return idx
 
 
-def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None, need_gx=True):
+def apply_l2(rgb, target, tables, gscale=None, y0=0, h_total=None):
+    """Training-step forward with the L2 loss fused into the epilogue.
+
+    Returns (gy, loss_sum, gmax): gy = (Y - target) * gscale (default 2/N,
+    i.e. d mean((Y-T)^2)/dY), loss_sum (B,) float64 = per-image sum of squared
+    residuals, gmax (B,) = per-image max |gy| (feeds fused_backward's
+    fixed-point scale).  Y itself is never written to HBM.
+    """
+    rgb = _image(rgb, tables.batch)
+    target = _image(target, tables.batch)
+    if target.shape != rgb.shape:
+        raise DimensionMismatch("target must be shaped like rgb")
+    b, _, h, w = rgb.shape
+    gscale = 2.0 / rgb.numel() if gscale is None else float(gscale)
+    gy = torch.empty_like(rgb)
+    loss = torch.empty(b, dtype=torch.float64, device=rgb.device)
+    gmax = torch.empty(b, dtype=torch.float32, device=rgb.device)
+    _lib.call("svdlut_fused_fwd_l2", _p(rgb), _p(target), b, h, w, y0, h if h_total is None else h_total,
+              _p(tables.buf), tables.d_t, tables.d_s, _p(gy), _p(loss), _p(gmax),
+              ctypes.c_float(gscale), _stream(rgb))
+    return gy, loss, gmax
+
+
+def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None, need_gx=True,
+                   tables=None, gmax=None):
     """Gradients of the fused apply w.r.t. the input and every table.
 
-    Returns dict(gx, dlut_planes, dlw, dlb, dgrid_planes, dgw, dgb).
+    ``tables`` (the forward's PackedTables) and ``gmax`` (per-image bound on
+    max |gy|, e.g. from apply_l2) skip the backward's own table packing and
+    max-reduction pass.  Returns dict(gx, dlut_planes, dlw, dlb, dgrid_planes,
+    dgw, dgb).
     """
     lp = _f32(lut_planes, "lut_planes", 5)
     lw = _f32(lw, "lw", 3)
@@ -326,7 +353,10 @@ def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None,
     )
     ws_bytes = int(_lib.load().svdlut_bwd_workspace_bytes(b, h, w, d_t, d_s, k))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    _lib.call("svdlut_fused_bwd", _p(rgb), _p(gy), b, h, w, y0, h_total, _p(lp), _p(lw), d_t,
+    if gmax is not None and (gmax.dtype != torch.float32 or gmax.numel() != b):
+        raise DimensionMismatch("gmax must be a float32 tensor with one entry per image")
+    _lib.call("svdlut_fused_bwd_packed", _p(rgb), _p(gy), b, h, w, y0, h_total,
+              _p(tables.buf if tables is not None else None), _p(gmax), _p(lp), _p(lw), d_t,
               _p(gp), _p(gw), k, d_s, _p(g["gx"]), _p(g["dlut_planes"]), _p(g["dlw"]),
               _p(g["dlb"]), _p(g["dgrid_planes"]), _p(g["dgw"]), _p(g["dgb"]), _p(ws), ws_bytes,
               _stream(rgb))

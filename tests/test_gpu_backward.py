@@ -149,3 +149,59 @@ def test_autograd_matches_oracle_and_trains(dev, oracle_mod):
         opt.step()
         losses.append(float(l))
     assert losses[-1] < losses[0]
+
+
+def test_fused_l2_forward_epilogue(dev):
+    """apply_l2: gy == (apply(x) - t) * 2/N (the epilogue's Y equals apply's up
+    to the compiler's FMA contraction of the two instantiations: within 1e-6
+    of max|gy|), gmax == max|gy| exactly, loss within 1e-6 relative of the
+    f64 sum; the backward fed with the forward's tables (biases folded in, so
+    float rounding of the biased grid vertices differs) and gmax matches the
+    standalone backward within the gradient tolerance."""
+    import torch
+
+    from paper_2508_16121_b200 import device, synth
+
+    cs = [synth.make_case(s, h=72, w=124) for s in (3, 4)]
+    st = lambda f: T(np.stack([getattr(c, f) for c in cs]), dev)  # noqa: E731
+    x = st("rgb")
+    tgt = x.clamp_min(0) ** 0.8
+    planes = device.reconstruct(st("u"), st("s"), st("vt"))
+    tables = device.pack_tables(planes, st("lw"), st("lb"), st("grid_planes"), st("gw"), st("gb"))
+    gy, loss, gmax = device.apply_l2(x, tgt, tables)
+    y = device.apply(x, tables)
+    scale = 2.0 / x.numel()
+    ref = (y - tgt) * scale
+    assert float((gy - ref).abs().max()) <= 1e-6 * float(ref.abs().max())
+    assert torch.equal(gmax, gy.abs().flatten(1).max(dim=1).values)
+    want = ((y.double() - tgt.double()) ** 2).flatten(1).sum(dim=1)
+    assert float(((loss - want).abs() / want).max()) <= 1e-6
+    g_ref = device.fused_backward(x, gy, planes, st("lw"), st("grid_planes"), st("gw"))
+    g_pk = device.fused_backward(x, gy, planes, st("lw"), st("grid_planes"), st("gw"), tables=tables,
+                                 gmax=gmax)
+    for k in g_ref:
+        close(g_pk[k].cpu().numpy(), g_ref[k].cpu().numpy(), k)
+
+
+def test_l2_step_matches_autograd(dev):
+    """autograd.l2_step (fused loss, no autograd graph) == SvdLutApply +
+    torch loss + backward, gradients within the 1e-4 relative tolerance."""
+    import torch
+
+    from paper_2508_16121_b200 import autograd, synth
+
+    c = synth.make_case(5, h=64, w=96)
+    leaves = {f: T(getattr(c, f), dev)[None].requires_grad_(True)
+              for f in ("rgb", "u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")}
+    tgt = leaves["rgb"].detach().clamp_min(0) ** 0.8
+    y = autograd.svdlut_apply(*leaves.values())
+    loss = ((y - tgt) ** 2).mean()
+    loss.backward()
+    params = [leaves[f].detach() for f in ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")]
+    step = autograd.l2_step(leaves["rgb"].detach(), tgt, *params)
+    assert abs(float(step["loss"]) - float(loss)) <= 1e-6 * float(loss)
+    names = {"rgb": "gx", "u": "u", "s": "s", "vt": "vt", "lw": "lw", "lb": "lb",
+             "grid_planes": "grid_planes", "gw": "gw", "gb": "gb"}
+    for leaf, key in names.items():
+        close(step[key].reshape(leaves[leaf].grad.shape).cpu().numpy(),
+              leaves[leaf].grad.cpu().numpy(), key)
