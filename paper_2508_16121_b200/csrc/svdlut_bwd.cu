@@ -30,7 +30,10 @@ constexpr int kBwdWarps = 15;
 constexpr int kBPx = 4;
 constexpr int kBChunk = 32 * kBPx;
 constexpr uint32_t kMagic = 0x4B000000u;
-constexpr int kBwdL2Rows = 2;  // rows of L2 prefetch distance (X and gY planes)
+constexpr int kBwdL2Rows = 2;
+#ifndef BWD_ROT
+#define BWD_ROT 2  // LUT scatter order per lane: 0 fixed, 1 rotated channels, 2 + rotated corners (best)
+#endif  // rows of L2 prefetch distance (X and gY planes)
 
 // Bulk L2 prefetch of row y of three planes (16-byte aligned cover, clipped
 // to each plane), no completion tracking.
@@ -48,7 +51,9 @@ __device__ __forceinline__ void bprefetch_row(const float* plane0, long long pl,
   }
 }
 
-// Global accumulator layout per image (floats): lut [p 3][i d_t][j d_t][c 3],
+// Global accumulator layout per image (floats): lut [p 3][i d_t][j d_t+1][c 3]
+// (row stride padded by one vertex so the four corners of a cell fall in
+// distinct shared-memory banks: offsets 0, 3, 3(d_t+1), 3(d_t+2) words),
 // grid [q 3 (xy|xc|yc)][c 3][a d_s][b d_s], then gsum [4].
 struct AccLayout {
   int dt, ds, lut_off, grid_off, gsum_off, total;
@@ -57,7 +62,7 @@ struct AccLayout {
     A.dt = dt;
     A.ds = ds;
     A.lut_off = 0;
-    A.grid_off = 3 * dt * dt * 3;
+    A.grid_off = 3 * dt * (dt + 1) * 3;
     A.gsum_off = A.grid_off + 9 * ds * ds;
     A.total = (A.gsum_off + 4 + 3) & ~3;
     return A;
@@ -202,6 +207,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const uint32_t sbase = bsmem_addr(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
+  const int rc0 = lane % 3, rc1 = (lane + 1) % 3, rc2 = (lane + 2) % 3;  // BWD_ROT channel order
+  const int rt = (lane / 3) & 3;                                           // BWD_ROT >= 2 corner order
 
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1) : "memory");
@@ -372,14 +379,46 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // ---- scatter: LUT pairs, one fixed-point atomic per value ----
           if (valid) {
             const int ir = (int)(br - kMagic), ig = (int)(bg - kMagic), ib = (int)(bb - kMagic);
+#if BWD_ROT >= 1
+            const float q0 = rc0 == 0 ? g0 : (rc0 == 1 ? g1 : g2);  // gY in this lane's channel order
+            const float q1 = rc1 == 0 ? g0 : (rc1 == 1 ? g1 : g2);
+            const float q2 = rc2 == 0 ? g0 : (rc2 == 1 ? g1 : g2);
+#endif
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
               const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
               const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
               const float w00 = (1.f - da) * (1.f - dbb), w10 = da * (1.f - dbb);
               const float w01 = (1.f - da) * dbb, w11 = da * dbb;
-              int* e = E_lut + (pr * dt * dt + ia * dt + ibb) * 3;
-              int* e10 = e + dt * 3;
+              int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
+              int* e10 = e + (dt + 1) * 3;
+#if BWD_ROT >= 2
+              // lane-rotated corner and channel order: lanes of one instruction
+              // that share a cell hit up to 12 different words (distinct banks,
+              // see AccLayout) instead of one address (ATOMS serializes them)
+              const float ea = 1.f - da, eb = 1.f - dbb;
+#pragma unroll
+              for (int jslot = 0; jslot < 4; ++jslot) {
+                const int kc = (jslot + rt) & 3;  // corner (a, b) = (kc & 1, kc >> 1)
+                const float wgt = ((kc & 1) ? da : ea) * ((kc & 2) ? dbb : eb);
+                int* ec = e + ((kc & 1) ? (dt + 1) * 3 : 0) + ((kc & 2) ? 3 : 0);
+                atomicAdd(ec + rc0, to_fixed(q0 * wgt, S));
+                atomicAdd(ec + rc1, to_fixed(q1 * wgt, S));
+                atomicAdd(ec + rc2, to_fixed(q2 * wgt, S));
+              }
+#elif BWD_ROT
+              // lane-rotated channel order: lanes of one instruction that share
+              // a cell hit three different words (banks) instead of one address
+              // (ATOMS serializes same-address lanes)
+              atomicAdd(e + rc0, to_fixed(q0 * w00, S)); atomicAdd(e + rc1, to_fixed(q1 * w00, S));
+              atomicAdd(e + rc2, to_fixed(q2 * w00, S));
+              atomicAdd(e10 + rc0, to_fixed(q0 * w10, S)); atomicAdd(e10 + rc1, to_fixed(q1 * w10, S));
+              atomicAdd(e10 + rc2, to_fixed(q2 * w10, S));
+              atomicAdd(e + 3 + rc0, to_fixed(q0 * w01, S)); atomicAdd(e + 3 + rc1, to_fixed(q1 * w01, S));
+              atomicAdd(e + 3 + rc2, to_fixed(q2 * w01, S));
+              atomicAdd(e10 + 3 + rc0, to_fixed(q0 * w11, S)); atomicAdd(e10 + 3 + rc1, to_fixed(q1 * w11, S));
+              atomicAdd(e10 + 3 + rc2, to_fixed(q2 * w11, S));
+#else
               atomicAdd(e, to_fixed(g0 * w00, S)); atomicAdd(e + 1, to_fixed(g1 * w00, S));
               atomicAdd(e + 2, to_fixed(g2 * w00, S));
               atomicAdd(e10, to_fixed(g0 * w10, S)); atomicAdd(e10 + 1, to_fixed(g1 * w10, S));
@@ -388,6 +427,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               atomicAdd(e + 5, to_fixed(g2 * w01, S));
               atomicAdd(e10 + 3, to_fixed(g0 * w11, S)); atomicAdd(e10 + 4, to_fixed(g1 * w11, S));
               atomicAdd(e10 + 5, to_fixed(g2 * w11, S));
+#endif
             }
           }
           // ---- grids: xc + yc runs per channel (key = guide cell; x-cell checked) ----
@@ -527,7 +567,8 @@ __global__ void finalize_kernel(const float* __restrict__ lp, const float* __res
     const float w = lw[b * 9 + task];
     float* D = dlp + (b * 9 + task) * (long long)dt * dt;
     for (int ij = threadIdx.x; ij < dt * dt; ij += blockDim.x) {
-      const float e = Eb[A.lut_off + (pr * dt * dt + ij) * 3 + c];
+      const int i = ij / dt, j = ij - i * dt;
+      const float e = Eb[A.lut_off + ((pr * dt + i) * (dt + 1) + j) * 3 + c];
       D[ij] = w * e;
       acc += (double)T[ij] * (double)e;
     }
