@@ -257,23 +257,14 @@ def combine_slices(base, fs, alloc=None):
 
 def naive_enhance(img, luts, lut_weights, grids, grid_weights, alloc=None):
     """Slice, transform, then combine (transform.py:196-212): the multi-stage
-    composition with every intermediate raster materialized (on the device)."""
-    from . import device
-
+    composition with every intermediate raster materialized — like the
+    reference, each stage allocates its raster through ``_alloc_raster``
+    ((K, H, W), then two (3, H, W)), so the raster hook sees the same pattern."""
     if grids.k % 3 != 0:
         raise BadGridCount(f"grid count {grids.k} is not a multiple of 3")
-    if img.width < 2 or img.height < 2:
-        raise DegenerateImage("slicing needs at least 2 px in each direction")
-    if grid_weights.k != grids.k:
-        raise DimensionMismatch(f"{grids.k} grids but {grid_weights.k} weight rows")
-    x = _to_dev(img.data)[None]
-    fs = device.slice_grids(x, _to_dev(grids.planes)[None], _to_dev(grid_weights.w)[None],
-                            _to_dev(grid_weights.b)[None])
-    base = device.apply_lut2d(x, _to_dev(luts.planes)[None], _to_dev(lut_weights.w)[None],
-                              _to_dev(lut_weights.b)[None])
-    y = device.combine_slices(base, fs)
-    return _image_type(img)(img.width, img.height,
-                            _to_host_raster(y[0], (3, img.height, img.width), alloc))
+    fs = slice_grid2d(img, grids, grid_weights, alloc=alloc)
+    base = apply_lut2d(img, luts, lut_weights, alloc=alloc)
+    return combine_slices(base, fs, alloc=alloc)
 
 
 def apply_lut3d(img, lut, alloc=None):

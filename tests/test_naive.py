@@ -169,3 +169,74 @@ def test_gpu_image_metrics(ngold):
     assert abs(analysis.psnr(a, b) - float(ngold["an_psnr"])) <= 1e-9 * abs(float(ngold["an_psnr"]))
     assert abs(analysis.delta_e_ab(a, b) - float(ngold["an_delta_e"])) <= 1e-9 * float(ngold["an_delta_e"])
     assert analysis.psnr(a, a) == float("inf")
+
+
+@pytest.mark.gpu
+def test_gpu_naive_raster_hook_pattern():
+    """naive_enhance allocates (K,H,W) then two (3,H,W) rasters through the
+    raster hook, like the reference (tests/test_transform.py:321-329 there)."""
+    import __graft_entry__
+    from paper_2508_16121_b200 import transform
+    from paper_2508_16121_b200.core_types import GridSet, GridWeights, Image, Lut2DSet, LutWeights
+
+    __graft_entry__.build_library()
+    c = make_inputs(20, 12, k=6, seed=2)
+    seen = []
+    transform._raster_hook = seen.append
+    try:
+        transform.naive_enhance(Image(20, 12, c["rgb"]), Lut2DSet(c["lp"]), LutWeights(c["lw"], c["lb"]),
+                                GridSet(c["gp"]), GridWeights(c["gw"], c["gb"]))
+    finally:
+        transform._raster_hook = None
+    assert seen == [(6, 12, 20), (3, 12, 20), (3, 12, 20)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("trial", range(10))
+def test_gpu_fused_vs_naive_random_models(trial):
+    """The reference's fused-vs-naive trials (d_t in [2,16], d_s in [2,8],
+    K in {3,6,9}; tests/test_transform.py:281-296 there): the fast fused
+    kernel within 1e-5 of the bit-exact naive stages, exact kernel within 1e-6."""
+    import torch
+
+    import __graft_entry__
+    from paper_2508_16121_b200 import device
+
+    __graft_entry__.build_library()
+    rng = np.random.default_rng(100 + trial)
+    d_t, d_s, k = int(rng.integers(2, 17)), int(rng.integers(2, 9)), int(rng.choice([3, 6, 9]))
+    w, h = int(rng.integers(2, 70)), int(rng.integers(2, 50))
+    c = make_inputs(w, h, d_t=d_t, d_s=d_s, k=k, seed=200 + trial)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()[None]  # noqa: E731
+    x, lp, lw, lb, gp, gw, gb = (T(c[f]) for f in ("rgb", "lp", "lw", "lb", "gp", "gw", "gb"))
+    naive = device.combine_slices(device.apply_lut2d(x, lp, lw, lb), device.slice_grids(x, gp, gw, gb))
+    fast = device.apply(x, device.pack_tables(lp, lw, lb, gp, gw, gb))
+    exact = device.apply_exact(x, lp, lw, lb, gp, gw, gb)
+    assert float((fast - naive).abs().max()) <= 1e-5
+    assert float((exact - naive).abs().max()) <= 1e-6
+
+
+@pytest.mark.gpu
+def test_gpu_bias_only_and_determinism():
+    """Zero planes and grids: the output is exactly lb[c] + sum gb[k % 3 == c]
+    (reference tests/test_transform.py:195-214 style); two launches are
+    bitwise identical (the thread-count determinism test's analog)."""
+    import torch
+
+    import __graft_entry__
+    from paper_2508_16121_b200 import device
+
+    __graft_entry__.build_library()
+    c = make_inputs(33, 17, d_t=9, d_s=5, k=6, seed=4)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()[None]  # noqa: E731
+    x = T(c["rgb"])
+    lb = torch.tensor([[0.25, -0.5, 0.125]], device="cuda")
+    gb = torch.tensor([[0.5, 0.25, -0.25, 0.125, 1.0, 0.0625]], device="cuda")
+    tables = device.pack_tables(T(np.zeros_like(c["lp"])), T(c["lw"]), lb, T(np.zeros_like(c["gp"])),
+                                T(c["gw"]), gb)
+    y = device.apply(x, tables)[0]
+    for ch in range(3):
+        want = float(lb[0, ch]) + float(gb[0, ch]) + float(gb[0, ch + 3])
+        assert bool((y[ch] == want).all())
+    tables = device.pack_tables(T(c["lp"]), T(c["lw"]), T(c["lb"]), T(c["gp"]), T(c["gw"]), T(c["gb"]))
+    assert torch.equal(device.apply(x, tables), device.apply(x, tables))
