@@ -53,7 +53,7 @@ namespace svdlut {
 #define FWD_REGPF 0  // next chunk's pixels prefetched into registers under this chunk's math
 #endif
 #ifndef FWD_CHUNKSPLIT
-#define FWD_CHUNKSPLIT 0  // 1: CTA ranges in 128-px chunks (measured slower); 0: whole rows
+#define FWD_CHUNKSPLIT 0  // 1: CTA ranges in 128-px chunks (balanced ends, but ~4% slower per CTA); 0: whole rows
 #endif
 constexpr int kPx = FWD_PX;
 constexpr int kFwdWarps = FWD_NW;
@@ -361,14 +361,32 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     }
     mbar_wait(bar, phase);
     phase ^= 1u;
+#ifdef FWD_DBG_TIMES
+    if (CHECK && threadIdx.x == 0 && r == r_begin) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      reinterpret_cast<unsigned long long*>(p.nonfinite + 2)[2 * blockIdx.x] = t;
+    }
+#endif
     // This warp's share of the slots of row y (CTA row ordinal n) into ring
     // buffer n % kRing.  Row n+2 is produced once row n is done, so warps may
     // drift apart by a row instead of meeting at a CTA barrier every row.
+    // x-cell of column x (the per-pixel rule: floor(min(t, d_s - 2)))
+    auto jx_of = [&](int x) -> int {
+      if (p.col_smem) return (int)floorf(fminf(col_t[x], sdm2));
+      float e;
+      return (int)(col_bracket(x, p.rcp_w, sdm1, sdm2, e) - kMagicBits);
+    };
     auto produce = [&](uint32_t n, int y) {
       float ey;
       const int jy = (int)(row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey) - kMagicBits);
       float4* S = slots + (n % kRing) * nent;
-      for (int e = warp * 32 + lane; e < nent; e += NW * 32) {
+      // only the x-cells this CTA's chunks of row y touch (all of them for a
+      // full row; a partial first / last row of a chunk range needs fewer)
+      const int x_lo = klo(y) * CH, x_hi = min(khi(y) * CH, p.w) - 1;
+      const int e_lo = x_hi >= x_lo ? jx_of(x_lo) * 3 * (ds - 1) : 0;
+      const int e_hi = x_hi >= x_lo ? (jx_of(x_hi) + 1) * 3 * (ds - 1) : 0;
+      for (int e = e_lo + warp * 32 + lane; e < e_hi; e += NW * 32) {
         const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
         const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
         S[e] = grid_entry(G, ds, ch, jx, jc, jy, ey);
@@ -552,6 +570,14 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   if (CHECK) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.nonfinite, 1);
   }
+#ifdef FWD_DBG_TIMES
+  __syncthreads();
+  if (CHECK && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    reinterpret_cast<unsigned long long*>(p.nonfinite + 2)[2 * blockIdx.x + 1] = t;
+  }
+#endif
 }
 
 size_t fwd_smem_bytes(int dt, int ds) {
