@@ -302,8 +302,19 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_fused_fwd.json")
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+    # the kernel's actual bound: the SM shared-memory (LSU) pipe, from the
+    # committed ncu capture of the same kernel
+    smem_pipe = None
+    if os.path.exists(prof):
+        try:
+            k0 = next(iter(json.load(open(prof))["kernels"].values()))
+            pct = float(k0["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"])
+            smem_pipe = {"bound": "shared-memory (LSU) pipe", "pct_of_peak_elapsed": round(pct, 1),
+                         "source": "profiles/ncu_fused_fwd.json (ncu --set full, one launch)"}
+        except (KeyError, StopIteration, ValueError):
+            smem_pipe = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "smem_pipe": smem_pipe,
                 "kernel": "svdlut::fused_fwd_kernel", "kernel_ms": round(kms, 5),
                 "algorithmic_bytes_per_launch": BYTES_PER_PX * H * W, "peak_source": peak_src}
 
