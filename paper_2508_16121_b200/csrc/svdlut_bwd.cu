@@ -31,6 +31,9 @@ constexpr int kBPx = 4;
 constexpr int kBChunk = 32 * kBPx;
 constexpr uint32_t kMagic = 0x4B000000u;
 constexpr int kBwdL2Rows = 2;
+#ifndef BWD_SPREAD
+#define BWD_SPREAD 1  // 1: a warp's lanes 60 px apart; 0: 32 consecutive 4-px groups
+#endif
 #ifndef BWD_ROT
 #define BWD_ROT 2  // LUT scatter order per lane: 0 fixed, 1 rotated channels, 2 + rotated corners (best)
 #endif  // rows of L2 prefetch distance (X and gY planes)
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // max lanes per bank, same-address lanes not merged).
       const int slots4 = (p.w + 3) >> 2;
       for (int s0 = 0; s0 < slots4; s0 += kBwdWarps * 32) {
-        const int xl = 4 * (s0 + lane * kBwdWarps + warp);
+        const int xl = BWD_SPREAD ? 4 * (s0 + lane * kBwdWarps + warp) : 4 * (s0 + warp * 32 + lane);
         if (xl >= p.w) continue;
         BChunk cur;
         bload_chunk(X, GY, pl, y, xl - 4 * lane, p.w, lane, vec, cur);
