@@ -188,7 +188,7 @@ int svdlut_fused_fwd_packed(const float* rgb, int batch, int h, int w, int y0, i
 }
 
 // Extended entry used by the Python layer: optional non-finite flag and
-// explicit kernel variant (0 = 128-bit lanes, 1 = interleaved lanes).
+// `variant` is reserved (ignored; kept for ABI stability).
 int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0, int h_total,
                                const void* tables, int d_t, int d_s, float* out, void* workspace,
                                size_t workspace_bytes, int* nonfinite, int variant, void* stream) {

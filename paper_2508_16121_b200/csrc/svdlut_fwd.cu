@@ -152,11 +152,6 @@ __device__ __forceinline__ float4 texv4(cudaTextureObject_t t, int i) {
                : "l"(t), "r"(i));
   return v;
 }
-__device__ __forceinline__ float2 lds2(uint32_t a) {
-  float2 v;
-  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
-  return v;
-}
 
 // Colour bracket returning the 2^23-biased index bits (see svdlut_common.cuh).
 __device__ __forceinline__ uint32_t cbracket(float q, float dm1, float dm2, float& delta) {

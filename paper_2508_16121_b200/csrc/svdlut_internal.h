@@ -12,8 +12,6 @@ cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const
                         const float* lw, const float* lb, const float* gp, const float* gw,
                         const float* gb, int k, const TableLayout& L, int batch, float* tables,
                         cudaStream_t st);
-cudaError_t launch_spatial(int w, int h, int y0, int h_total, int ds, SpatialBr* col,
-                           SpatialBr* row, cudaStream_t st);
 
 // Fast fused forward from packed tables; spatial brackets are computed in the
 // kernel (rows of a strip y0.. of an image with h_total rows).

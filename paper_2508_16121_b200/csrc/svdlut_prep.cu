@@ -1,6 +1,5 @@
 // svdlut_prep.cu — table prologue kernels (K1): LUT reconstruction from SVD
-// factors, weight folding / grid merging into coefficient cells, and the
-// spatial bracket tables.  All tiny (≈60 KB of tables per image); launched
+// factors and weight folding / grid merging into coefficient cells.  All tiny (≈60 KB of tables per image); launched
 // once per call on the caller's stream.
 #include "svdlut_common.cuh"
 #include "svdlut_internal.h"
@@ -179,14 +178,6 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
   }
 }
 
-// Column brackets for x in [0, w) and row brackets for rows y0..y0+h-1 of h_total.
-__global__ void spatial_kernel(int w, int h, int y0, int h_total, int ds, SpatialBr* __restrict__ col,
-                               SpatialBr* __restrict__ row) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < w) col[t] = spatial_bracket(t, w, ds);
-  if (t < h) row[t] = spatial_bracket(y0 + t, h_total, ds);
-}
-
 cudaError_t launch_reconstruct(const float* u, const float* s, const float* vt, int batch, int dt,
                                int ns, float* planes, cudaStream_t st) {
   dim3 grid(9, batch);
@@ -212,11 +203,5 @@ cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const
   return cudaGetLastError();
 }
 
-cudaError_t launch_spatial(int w, int h, int y0, int h_total, int ds, SpatialBr* col, SpatialBr* row,
-                           cudaStream_t st) {
-  const int n = w > h ? w : h;
-  spatial_kernel<<<(n + 255) / 256, 256, 0, st>>>(w, h, y0, h_total, ds, col, row);
-  return cudaGetLastError();
-}
 
 }  // namespace svdlut
