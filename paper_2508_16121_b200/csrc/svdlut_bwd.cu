@@ -31,6 +31,12 @@ constexpr int kBPx = 4;
 constexpr int kBChunk = 32 * kBPx;
 constexpr uint32_t kMagic = 0x4B000000u;
 constexpr int kBwdL2Rows = 2;
+#ifndef BWD_TEXLUT
+// 1: all three LUT pairs are gathered through the texture path (L1-resident:
+// only the grid block, slots and accumulators occupy shared memory, so ~160 KB
+// of L1 remains); 0: pairs rg / rb staged in shared memory like the forward
+#define BWD_TEXLUT 0  // 1 measured: smooth 880 -> 840 us, uniform noise 938 -> 1136 us (L1 misses)
+#endif
 #ifndef BWD_SPREAD
 #define BWD_SPREAD 1  // 1: a warp's lanes 60 px apart; 0: 32 consecutive 4-px groups
 #endif
@@ -217,7 +223,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t table_bytes = (uint32_t)L.staged_bytes();
+  // staged prefix: the LUT pairs rg / rb + the grid block, or just the grid block
+  const uint32_t stage_from = BWD_TEXLUT ? (uint32_t)L.xc_off * 4u : 0u;
+  const uint32_t table_bytes = (uint32_t)L.staged_bytes() - stage_from;
+  const float* gsm = smem - (BWD_TEXLUT ? L.xc_off : 0);  // + table offset -> smem
   const int nent = (ds - 1) * 3 * (ds - 1);
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
   float* Es = reinterpret_cast<float*>(slots + 2 * nent);  // A.total floats
@@ -261,7 +270,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 sbase + off),
-            "l"(reinterpret_cast<const char*>(tb) + off), "r"(n), "r"(bar)
+            "l"(reinterpret_cast<const char*>(tb) + stage_from + off), "r"(n), "r"(bar)
             : "memory");
       }
     }
@@ -276,6 +285,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     float* GX = p.gx ? p.gx + (long long)b * 3 * pl : nullptr;
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagic * (cst3 + 3u);
+    // texel of cell (a, b) of pair rg / rb: texKrg (+ pair offset) + bits_a*cst3 + bits_b*3
+    const uint32_t texKrg = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
+                            (uint32_t)(L.lut_off / 4) - kMagic * (cst3 + 3u);
+    const uint32_t texKrb = texKrg + (uint32_t)(L.pair_floats / 4);
     asm volatile(
         "{\n.reg .pred p;\nWAITB_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAITB_%=;\n}\n" ::"r"(bar),
         "r"(phase)
@@ -287,7 +300,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       for (int e = threadIdx.x; e < nent; e += blockDim.x) {
         const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
         const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-        slots[e] = bgrid_entry(smem, L, ch, jx, jc, jy, ey);
+        slots[e] = bgrid_entry(gsm, L, ch, jx, jc, jy, ey);
       }
     }
     __syncthreads();
@@ -349,15 +362,27 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // ---- input gradient from the coefficient cells ----
           float gar = 0.f, gag = 0.f, gab = 0.f;
           {
+#if BWD_TEXLUT
+            const int ti = (int)(br * cst3 + bg * 3u + texKrg);  // rg via the texture path
+            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
+                         c2 = tex1Dfetch<float4>(p.tex, ti + 2);
+#else
             const uint32_t a = br * cst48 + lutK + bg * 48u;  // rg
             const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
+#endif
             // cell_index: B c0.z c0.w c2.y  C c1.x c1.y c2.z  D c1.z c1.w c2.w
             gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.y);
             gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.z);
           }
           {
+#if BWD_TEXLUT
+            const int ti = (int)(br * cst3 + bb * 3u + texKrb);  // rb via the texture path
+            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
+                         c2 = tex1Dfetch<float4>(p.tex, ti + 2);
+#else
             const uint32_t a = br * cst48 + lutK + bb * 48u + pair_bytes;  // rb
             const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
+#endif
             gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.y);
             gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.z);
           }
@@ -515,7 +540,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         for (int e = threadIdx.x; e < nent; e += blockDim.x) {
           const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
           const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-          S[e] = bgrid_entry(smem, L, ch, jx, jc, jy1, ey1);
+          S[e] = bgrid_entry(gsm, L, ch, jx, jc, jy1, ey1);
         }
       }
       __syncthreads();
@@ -640,7 +665,8 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
-  const size_t smem = (size_t)L.staged_bytes() + 2 * (size_t)nent * 16 + (size_t)A.total * 4;
+  const size_t staged = (size_t)L.staged_bytes() - (BWD_TEXLUT ? (size_t)L.xc_off * 4 : 0);
+  const size_t smem = staged + 2 * (size_t)nent * 16 + (size_t)A.total * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
   float* tables = (float*)wp;
@@ -696,6 +722,12 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
     auto kern = (dt == 33 && ds == 17) ? fused_bwd_kernel<33, 17> : fused_bwd_kernel<0, 0>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
+      return e;
+    // smallest carve-out that fits: the rest of the 256 KB array is L1 for the
+    // texture-path LUT pairs
+    const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  pct > 100 ? 100 : pct)) != cudaSuccess)
       return e;
     kern<<<(int)grid, kBwdWarps * 32, smem, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
