@@ -58,7 +58,11 @@ namespace svdlut {
 constexpr int kPx = FWD_PX;
 constexpr int kFwdWarps = FWD_NW;
 constexpr int kChunk = 32 * kPx;
-constexpr int kRing = 3;  // per-row grid slot buffers
+#ifndef FWD_RING
+#define FWD_RING 4  // per-row grid slot buffers (warps may drift FWD_RING - 2 rows apart); 3: -2%, 5: +1% smooth but -1% noise
+#endif
+constexpr int kRing = FWD_RING;
+constexpr int kAhead = kRing - 1;  // rows of slots produced ahead of the one being consumed
 constexpr uint32_t kMagicBits = 0x4B000000u;  // bits of 2^23
 
 struct FwdParams {
@@ -374,8 +378,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     }
 #endif
     // This warp's share of the slots of row y (CTA row ordinal n) into ring
-    // buffer n % kRing.  Row n+2 is produced once row n is done, so warps may
-    // drift apart by a row instead of meeting at a CTA barrier every row.
+    // buffer n % kRing.  Row n+kAhead is produced once row n is done, so warps
+    // may drift apart instead of meeting at a CTA barrier every row.
     // x-cell of column x (the per-pixel rule: floor(min(t, d_s - 2)))
     auto jx_of = [&](int x) -> int {
       if (p.col_smem) return (int)floorf(fminf(col_t[x], sdm2));
@@ -401,8 +405,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     };
     const uint32_t n0 = nrow;
     const int cnt = y_last - y_first + 1;
-    produce(n0, y_first);
-    if (cnt > 1) produce(n0 + 1, y_first + 1);
+    for (int i = 0; i < kAhead && i < cnt; ++i) produce(n0 + i, y_first + i);
 
     for (int y = y_first; y <= y_last; ++y) {
       const uint32_t n = n0 + (uint32_t)(y - y_first);
@@ -549,11 +552,11 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8u * (n % kRing));
-      if (y + 2 <= y_last) {
-        // buffer (n+2) % kRing last held row n-1 (of this image segment when
-        // y > y_first; otherwise the segment-start barrier covers it)
+      if (y + kAhead <= y_last) {
+        // buffer (n+kAhead) % kRing last held row n-1 (of this image segment
+        // when y > y_first; otherwise the segment-start barrier covers it)
         if (y > y_first) mbar_wait(empty0 + 8u * ((n - 1) % kRing), ((n - 1) / kRing) & 1u);
-        produce(n + 2, y + 2);
+        produce(n + kAhead, y + kAhead);
       }
     }
     nrow = n0 + (uint32_t)cnt;
