@@ -26,7 +26,10 @@
 
 namespace svdlut {
 
-constexpr int kBwdWarps = 15;
+#ifndef BWD_NW
+#define BWD_NW 15
+#endif
+constexpr int kBwdWarps = BWD_NW;
 constexpr int kBPx = 4;
 constexpr int kBChunk = 32 * kBPx;
 constexpr uint32_t kMagic = 0x4B000000u;
