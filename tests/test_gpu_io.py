@@ -182,3 +182,30 @@ def test_enhance_payload_host_entry(dev):
     assert got16.dtype == np.dtype(">u2")
     d16 = np.abs(got16.astype(np.int64) - ref_quantize(ref.transpose(1, 2, 0), 65535).astype(np.int64))
     assert d16.max() <= 1
+
+
+@pytest.mark.parametrize("fmt", ["u8", "u16be"])
+@pytest.mark.parametrize("w,h", [(1001, 777), (3840, 2160)])
+def test_enhance_payload_many_strips_equals_device(dev, fmt, w, h):
+    """Large payloads travel as many strips through the streamed kernel; the
+    result is the device path's bit for bit (w=1001: unaligned rows)."""
+    import torch
+
+    from paper_2508_16121_b200 import device, synth, transform
+    from paper_2508_16121_b200.core_types import GridSet, GridWeights, Lut2DSet, LutWeights
+
+    c = synth.make_case(4, h=8, w=8)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)[None]  # noqa: E731
+    planes = device.reconstruct(T(c.u), T(c.s), T(c.vt))
+    tables = device.pack_tables(planes, T(c.lw), T(c.lb), T(c.grid_planes), T(c.gw), T(c.gb))
+    maxval = 255 if fmt == "u8" else 65535
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, maxval + 1, (h, w, 3)).astype(np.uint16)
+    payload = img.astype(np.uint8) if fmt == "u8" else img.astype(">u2")
+    got = transform.enhance_payload(payload, Lut2DSet(planes[0].cpu().numpy()), LutWeights(c.lw, c.lb),
+                                    GridSet(c.grid_planes), GridWeights(c.gw, c.gb))
+    raw = payload if fmt == "u8" else to_be_bytes(img)
+    dv = device.apply_io(torch.from_numpy(np.ascontiguousarray(raw)).to(dev), tables, in_fmt=fmt,
+                         out_fmt=fmt)[0].cpu().numpy()
+    dv = dv if fmt == "u8" else from_be_bytes(dv)
+    assert np.array_equal(np.asarray(got).astype(np.int64), dv.astype(np.int64))
