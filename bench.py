@@ -150,6 +150,29 @@ def cpu_reference(case, reps, min_seconds=0.0):
     return H * W * len(times) / sum(times) / 1e6, threads, med, times
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_single_thread(case, frames=2):
+    """Oracle port on one thread (SURVEY §8d asks for the 1-thread figure
+    beside the N-thread one, to show the parallel twin scales)."""
+    import oracle
+
+    planes = oracle.reconstruct(case.u, case.s, case.vt)
+    args = (case.rgb, planes, case.lw, case.lb, case.grid_planes, case.gw, case.gb)
+    t0 = time.perf_counter()
+    for _ in range(frames):
+        oracle.fused_fwd(*args, threads=1)
+    return H * W * frames / (time.perf_counter() - t0) / 1e6
+
+
 def run_reference_arm(a):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -385,7 +408,10 @@ def main():
     cpu = None
     if rank == 0 and not a.no_cpu:
         mps, threads, med, times = cpu_reference(case, 3, min_seconds=10.0)
+        one = cpu_single_thread(case)
         cpu = {"value": round(mps, 3), "unit": UNIT, "cores": threads, "kind": "port",
+               "cpu_model": cpu_model(), "single_thread_value": round(one, 3),
+               "thread_speedup": round(mps / one, 2),
                "sample": f"{len(times)} full 3x2160x3840 frames (reconstruct + fused apply, "
                          f"{sum(times):.1f} s of CPU work, median {med * 1e3:.1f} ms/frame), "
                          "oracle/svdlut_oracle.c (op-for-op restatement of the reference "

@@ -193,6 +193,12 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
   if (trace) {
     for (auto& e : tev) cudaEventCreate(&e);
     cudaEventRecord(tev[3 * kMaxStrips], s_k);
+    cudaPointerAttributes ai, ao;
+    const bool oki = cudaPointerGetAttributes(&ai, rgb) == cudaSuccess;
+    const bool oko = cudaPointerGetAttributes(&ao, out) == cudaSuccess;
+    cudaGetLastError();
+    fprintf(stderr, "host in %p type %d, out %p type %d (1 = page-locked), %d strips\n", rgb,
+            oki ? (int)ai.type : -1, out, oko ? (int)ao.type : -1, n_strips);
   }
   for (int s = 0; s < n_strips; ++s) {
     const int r0 = bounds[s], r1 = bounds[s + 1];

@@ -18,7 +18,10 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["shard_range", "strip_rows", "image_block", "forward_strip", "forward_images",
-           "gather_rows", "gather_images", "max_over_ranks"]
+           "gather_rows", "gather_images", "max_over_ranks", "data_parallel_l2_step", "PARAM_KEYS"]
+
+# parameter set of one SvdLut model, in autograd.l2_step's argument order
+PARAM_KEYS = ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")
 
 
 def shard_range(n, world, rank):
@@ -89,3 +92,48 @@ def max_over_ranks(value, device=None, group=None):
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def _device_l2_step(rgb, target, batched):
+    from . import autograd
+
+    return autograd.l2_step(rgb, target, *(batched[k] for k in PARAM_KEYS), need_gx=False)
+
+
+def data_parallel_l2_step(rgb, target, params, group=None, step_fn=None):
+    """One data-parallel training step of ONE shared parameter set.
+
+    The per-image path (configs 3 / 5) needs no exchange; when a single model
+    (unbatched ``params``: u, s, vt, lw, lb, grid_planes, gw, gb) is trained on
+    a batch sharded over ranks, the table gradients are the one real exchange
+    (SURVEY §8e).  Each rank runs the fused L2 step on its images with the
+    parameters broadcast per image, sums the per-image gradients, converts
+    them to the sum-of-squares form (x local pixel count) and issues ONE
+    all_reduce(SUM) over a single flat bucket (≈80 KB at d_t=33 / d_s=17,
+    latency-bound, so one bucket beats overlap) that also carries the loss
+    sum and the pixel count; dividing by the global count gives every rank
+    the gradient of the global mean((Y - target)^2).
+
+    Returns {"loss": float tensor, key: gradient shaped like params[key]}.
+    ``step_fn(rgb, target, batched_params)`` defaults to autograd.l2_step on
+    the sm_100a kernels; tests inject a CPU stand-in (gloo).
+    """
+    fn = step_fn or _device_l2_step
+    b = rgb.shape[0]
+    batched = {k: params[k].unsqueeze(0).expand(b, *params[k].shape).contiguous() for k in PARAM_KEYS}
+    g = fn(rgb, target, batched)
+    n_local = float(rgb.numel())
+    parts = [g[k].sum(0).reshape(-1).to(torch.float64) * n_local for k in PARAM_KEYS]
+    loss = torch.as_tensor(g["loss"], dtype=torch.float64, device=parts[0].device).reshape(1)
+    flat = torch.cat(parts + [loss * n_local, torch.tensor([n_local], dtype=torch.float64,
+                                                           device=parts[0].device)])
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    n_global = flat[-1]
+    out, off = {}, 0
+    for k in PARAM_KEYS:
+        n = params[k].numel()
+        out[k] = (flat[off:off + n] / n_global).reshape(params[k].shape).to(params[k].dtype)
+        off += n
+    out["loss"] = flat[off] / n_global
+    return out

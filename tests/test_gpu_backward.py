@@ -205,3 +205,27 @@ def test_l2_step_matches_autograd(dev):
     for leaf, key in names.items():
         close(step[key].reshape(leaves[leaf].grad.shape).cpu().numpy(),
               leaves[leaf].grad.cpu().numpy(), key)
+
+
+def test_shared_parameter_step_matches_autograd(dev):
+    """parallel.data_parallel_l2_step (single process: no exchange) on the
+    kernels == autograd through SvdLutApply with ONE parameter set shared by
+    a batch of 3 images."""
+    import torch
+
+    from paper_2508_16121_b200 import autograd, parallel, synth
+
+    c = synth.make_case(8, h=40, w=72)
+    rng = np.random.default_rng(8)
+    rgb = T(rng.random((3, 3, 40, 72), dtype=np.float32), dev)
+    tgt = rgb.clamp_min(0) ** 0.8
+    params = {k: T(getattr(c, k), dev) for k in parallel.PARAM_KEYS}
+    got = parallel.data_parallel_l2_step(rgb, tgt, params)
+    leaves = {k: v.clone().requires_grad_(True) for k, v in params.items()}
+    y = autograd.svdlut_apply(rgb, *(leaves[k].unsqueeze(0).expand(3, *leaves[k].shape).contiguous()
+                                     for k in parallel.PARAM_KEYS))
+    loss = ((y - tgt) ** 2).mean()
+    loss.backward()
+    assert abs(float(got["loss"]) - float(loss)) <= 1e-6 * float(loss)
+    for k in parallel.PARAM_KEYS:
+        close(got[k].cpu().numpy(), leaves[k].grad.cpu().numpy(), k)
