@@ -347,7 +347,11 @@ def main():
     e2e = None
     if not a.no_e2e:
         pin = torch.empty((3, H, W), dtype=torch.float32, pin_memory=True)
-        pin.copy_(torch.from_numpy(case.rgb))
+        # filled by one thread, like a frame arriving from a reader or decoder:
+        # a multi-threaded torch copy_ leaves the frame dirty in the cores'
+        # private caches, and every later DMA read of it snoops them (4K u8
+        # step 0.82 -> 1.6 ms measured, tools/u8_payload_probe.py)
+        pin.numpy()[...] = case.rgb
         img = Image(W, H, pin.numpy())
         factors = SvdLut(case.u, case.s, case.vt)
         lw = LutWeights(case.lw, case.lb)
@@ -379,8 +383,7 @@ def main():
         import torch as _t
 
         pin8 = _t.empty((H, W, 3), dtype=_t.uint8, pin_memory=True)
-        pin8.copy_(_t.from_numpy(np.ascontiguousarray(
-            np.floor(np.clip(case.rgb.transpose(1, 2, 0), 0, 1) * 255 + 0.5).astype(np.uint8))))
+        pin8.numpy()[...] = np.floor(np.clip(case.rgb.transpose(1, 2, 0), 0, 1) * 255 + 0.5).astype(np.uint8)
         payload = pin8.numpy()
         # a serving loop writes every frame into its own page-locked output
         # payload (enhance_payload's `out=`); a freshly allocated one per frame

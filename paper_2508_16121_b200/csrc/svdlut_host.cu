@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <mutex>
 
 #include "../../include/svdlut_b200.h"
@@ -115,6 +116,7 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
   if (w < 2 || h < 2) return SVDLUT_ERR_DEGENERATE_IMAGE;
   if (d_t < 2 || d_s < 2) return SVDLUT_ERR_BAD_VERTEX_COUNT;
   std::lock_guard<std::mutex> lock(ctx->mu);
+  const auto host_t0 = std::chrono::steady_clock::now();
   if (cudaSetDevice(ctx->device) != cudaSuccess) return SVDLUT_ERR_CUDA;
   const bool fast = !exact && svdlut_fast_supported(d_t, d_s);
 
@@ -241,7 +243,10 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     if (trace) cudaEventRecord(tev[3 * s + 2], s_out);
   }
   if (trace) {
+    const double enq_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
     cudaStreamSynchronize(s_out);
+    fprintf(stderr, "host enqueue %.3f ms\n", enq_ms);
     for (int s = 0; s < n_strips; ++s) {
       float t[3];
       for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], tev[3 * kMaxStrips], tev[3 * s + i]);
