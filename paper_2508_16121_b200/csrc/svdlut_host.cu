@@ -157,9 +157,9 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
 
   // ---- strip pipeline: H2D (s_in) -> kernel (s_k) -> D2H (s_out) ------------
   // ~12 MB strips at 4K: every copy has a fixed setup cost of several
-  // microseconds, so fewer, larger copies win; the first and the last strip
-  // are a quarter of that, because the pipeline fill (first H2D) and drain
-  // (last D2H) run one PCIe direction alone.
+  // microseconds, so fewer, larger copies win; the first strip is a quarter
+  // of that and the last ones halve (see below), because the pipeline fill
+  // (first H2D) and drain (last D2H) run one PCIe direction alone.
   const size_t plane = (size_t)h * w;
   const TableLayout L = TableLayout::make(d_t, d_s);
   static const size_t strip_env = [] {
@@ -176,16 +176,33 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     const size_t target =
         strip_env ? strip_env : std::min((size_t)12 << 20, std::max((size_t)2 << 20, row_b * h / 4));
     const int unit = (int)std::max<size_t>(1, target / row_b);  // rows per strip
-    const int edge = std::max(1, unit / 4);
+    // head: a quarter strip (the D2H engine idles until the first strip is
+    // through); tail: halving strips (unit/2, unit/4, ...), because the copy-out
+    // stream runs one strip behind, so the last full strip's D2H would
+    // otherwise be paid after the input has finished arriving
+    static const int tail_n = [] {
+      const char* e = getenv("SVDLUT_TAIL");  // development knob: number of halving tail strips
+      return e ? std::max(0, std::min(6, atoi(e))) : 3;
+    }();
+    const int head = std::max(1, unit / 4);
+    int tail[8], nt = 0, tail_sum = 0;
+    for (int k = 1; k <= tail_n; ++k) {
+      tail[nt] = std::max(1, unit >> k);
+      tail_sum += tail[nt++];
+    }
     bounds[0] = 0;
-    if (h <= 2 * edge + unit) {
+    if (h <= head + tail_sum + unit) {
       bounds[n_strips = 1] = h;
     } else {
-      const int mid = h - 2 * edge;
-      const int n_mid = std::min(kMaxStrips - 2, (mid + unit - 1) / unit);
-      bounds[++n_strips] = edge;
-      for (int i = 1; i <= n_mid; ++i) bounds[++n_strips] = edge + (int)((long long)mid * i / n_mid);
-      bounds[++n_strips] = h;
+      const int mid = h - head - tail_sum;
+      const int n_mid = std::min(kMaxStrips - 1 - nt, (mid + unit - 1) / unit);
+      bounds[++n_strips] = head;
+      for (int i = 1; i <= n_mid; ++i) bounds[++n_strips] = head + (int)((long long)mid * i / n_mid);
+      for (int k = 0; k < nt; ++k) {
+        bounds[n_strips + 1] = bounds[n_strips] + tail[k];
+        ++n_strips;
+      }
+      bounds[n_strips] = h;  // (already equal)
     }
   }
   // SVDLUT_TRACE=1 (development): per-strip H2D / kernel / D2H completion
