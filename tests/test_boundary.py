@@ -154,3 +154,29 @@ def test_product_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "svdlut_oracle" not in src, f
+
+
+def test_c_abi_widened_entries_validate_before_device_work(lib):
+    """The sample-format, multi-stage, 3D-LUT and histogram entry points map
+    bad arguments to the reference's error classes without touching a GPU."""
+    with pytest.raises(errors.InvalidArgument):  # unknown sample format
+        _lib.call("svdlut_fused_fwd_io", FAKE, 7, 1, 8, 8, 0, 8, FAKE, 33, 17, FAKE, 0, NULL, NULL)
+    with pytest.raises(errors.InvalidArgument):  # L2-gradient format is an internal output only
+        _lib.call("svdlut_fused_fwd_io", FAKE, 0, 1, 8, 8, 0, 8, FAKE, 33, 17, FAKE, 3, NULL, NULL)
+    with pytest.raises(errors.DegenerateImage):
+        _lib.call("svdlut_fused_fwd_io", FAKE, 1, 1, 1, 8, 0, 1, FAKE, 33, 17, FAKE, 1, NULL, NULL)
+    with pytest.raises(errors.BadVertexCount):
+        _lib.call("svdlut_slice_grids", FAKE, 1, 8, 8, 0, 8, FAKE, FAKE, FAKE, 6, 1, FAKE, NULL)
+    with pytest.raises(errors.DimensionMismatch):
+        _lib.call("svdlut_slice_grids", FAKE, 1, 8, 8, 0, 8, FAKE, FAKE, FAKE, 0, 5, FAKE, NULL)
+    with pytest.raises(errors.BadVertexCount):
+        _lib.call("svdlut_apply_lut3d", FAKE, 1, 8, 8, FAKE, 1, FAKE, NULL)
+    with pytest.raises(errors.InvalidArgument):
+        _lib.call("svdlut_apply_lut3d", NULL, 1, 8, 8, FAKE, 33, FAKE, NULL)
+    with pytest.raises(errors.Unsupported):
+        _lib.call("svdlut_occurrence", FAKE, 1, 8, 8, 2000, FAKE, NULL)
+    with pytest.raises(errors.InvalidArgument):
+        _lib.call("svdlut_occurrence", FAKE, 1, 8, 8, 33, NULL, NULL)
+    # empty inputs are no-ops that never dereference the pointers
+    _lib.call("svdlut_apply_lut3d", NULL, 0, 8, 8, NULL, 33, NULL, NULL)
+    _lib.call("svdlut_fused_fwd_io", NULL, 1, 0, 8, 8, 0, 8, NULL, 33, 17, NULL, 1, NULL, NULL)
