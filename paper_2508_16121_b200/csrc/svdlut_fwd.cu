@@ -127,6 +127,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 // ~92 KB of L1 for the texture-path LUT pair
 #define FWD_GRID_SMEM 1  // 0 measured slower (73.9 vs 70.1 us smooth, 153 vs 149 uniform)
 #endif
+#ifndef FWD_TGT_LATE
+// L2-loss epilogue: 1 loads the target chunk right before the epilogue (its
+// 12 registers are not live across the pixel math, but the load latency is
+// exposed: 8 x 1080p 214 vs 203 us, more spills); 0 loads it with the input
+// chunk
+#define FWD_TGT_LATE 0
+#endif
 #ifndef FWD_TEXDEP
 #define FWD_TEXDEP 1  // next pixel's TLD index depends on this pixel's last LDS (see below)
 #endif
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     settle(cur_y, cur_k);
     if (cur_y <= y_last) {
       Src<IN>::template load<PX>(src, pl, cur_y, cur_k * CH + PX * lane, p.w, vec_in, cur.r, cur.g, cur.b);
-      if (LOSS)
+      if (LOSS && !FWD_TGT_LATE)
         Src<kF32>::template load<PX>(tsrc, pl, cur_y, cur_k * CH + PX * lane, p.w, vec_out, tgt.r, tgt.g,
                                      tgt.b);
     }
@@ -523,6 +530,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
         }
         if (LOSS) {  // gY = (Y - T) * 2/N, loss partial, max |gY| (pixels past the row end excluded)
+          if (FWD_TGT_LATE)
+            Src<kF32>::template load<PX>(tsrc, pl, cur_y, xl, p.w, vec_out, tgt.r, tgt.g, tgt.b);
 #pragma unroll
           for (int u = 0; u < PX; ++u) {
             const bool in_row = xl + u < p.w;
@@ -542,7 +551,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
 #else
         if (nxt_y <= y_last) {
           Src<IN>::template load<PX>(src, pl, nxt_y, nxt_k * CH + PX * lane, p.w, vec_in, cur.r, cur.g, cur.b);
-          if (LOSS)
+          if (LOSS && !FWD_TGT_LATE)
             Src<kF32>::template load<PX>(tsrc, pl, nxt_y, nxt_k * CH + PX * lane, p.w, vec_out, tgt.r,
                                          tgt.g, tgt.b);
         }
