@@ -52,7 +52,22 @@ cudaError_t ensure(void** buf, size_t* have, size_t need) {
 
 size_t rup(size_t v) { return (v + 255) / 256 * 256; }
 
+// On a failed call, wait for whatever was already queued on the context's
+// streams before its lock is released, so the next call cannot reuse device or
+// staging buffers that copies or kernels of this one still touch.
+struct DrainOnFailure {
+  svdlut_ctx* ctx;
+  bool ok = false;
+  ~DrainOnFailure();
+};
+
 }  // namespace
+
+DrainOnFailure::~DrainOnFailure() {
+  if (ok) return;
+  for (cudaStream_t st : ctx->st)
+    if (st) cudaStreamSynchronize(st);
+}
 
 extern "C" {
 
@@ -116,6 +131,7 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
   if (w < 2 || h < 2) return SVDLUT_ERR_DEGENERATE_IMAGE;
   if (d_t < 2 || d_s < 2) return SVDLUT_ERR_BAD_VERTEX_COUNT;
   std::lock_guard<std::mutex> lock(ctx->mu);
+  DrainOnFailure drain{ctx};
   const auto host_t0 = std::chrono::steady_clock::now();
   if (cudaSetDevice(ctx->device) != cudaSuccess) return SVDLUT_ERR_CUDA;
   const bool fast = !exact && svdlut_fast_supported(d_t, d_s);
@@ -276,6 +292,7 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     return SVDLUT_ERR_CUDA;
   if (cudaStreamSynchronize(s_out) != cudaSuccess) return SVDLUT_ERR_CUDA;
   if (nonfinite) *nonfinite = fast ? *ctx->h_flag : 0;
+  drain.ok = true;
   return SVDLUT_OK;
 }
 
@@ -305,6 +322,7 @@ int svdlut_reconstruct_host(svdlut_ctx* ctx, const float* u, const float* s, con
   if (n_s < 1 || n_s > d_t) return SVDLUT_ERR_DIMENSION_MISMATCH;
   if (batch == 0) return SVDLUT_OK;
   std::lock_guard<std::mutex> lock(ctx->mu);
+  DrainOnFailure drain{ctx};
   if (cudaSetDevice(ctx->device) != cudaSuccess) return SVDLUT_ERR_CUDA;
   const size_t nu = (size_t)batch * 9 * d_t * n_s, ns = (size_t)batch * 9 * n_s;
   const size_t np = (size_t)batch * 9 * d_t * d_t;
@@ -334,6 +352,7 @@ int svdlut_reconstruct_host(svdlut_ctx* ctx, const float* u, const float* s, con
     return SVDLUT_ERR_CUDA;
   if (cudaStreamSynchronize(sk) != cudaSuccess) return SVDLUT_ERR_CUDA;
   memcpy(planes, st, np * 4);
+  drain.ok = true;
   return SVDLUT_OK;
 }
 
