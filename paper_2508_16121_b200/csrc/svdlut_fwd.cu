@@ -27,6 +27,7 @@
 //   * Streaming I/O: 24 B/pixel of HBM traffic (3 f32 in, 3 f32 out).  The
 //     kernel is bound by the shared-memory pipe (~87% of active cycles, 1.6
 //     wavefronts per pixel), not by HBM — DESIGN.md §3 has the budget.
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 #include <vector>
@@ -732,11 +733,15 @@ static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t 
                                cudaStream_t st) {
   auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps, IN, OUT>
                     : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps, IN, OUT>;
-  // function attributes are set once per (instantiation, smem size); setting
-  // them is not a stream operation, so graph capture does not see it
-  static size_t configured[2] = {0, 0};
+  // function attributes are set once per (instantiation, device, smem size);
+  // setting them is not a stream operation, so graph capture does not see it
+  constexpr int kMaxDev = 64;
+  static std::atomic<size_t> configured[kMaxDev][2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<size_t>* seen = dev < kMaxDev ? &configured[dev][check] : nullptr;
   cudaError_t e = cudaSuccess;
-  if (configured[check] != smem) {
+  if (!seen || seen->load(std::memory_order_relaxed) != smem) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // smallest shared-memory carve-out that fits: the rest of the 256 KB stays
@@ -744,7 +749,7 @@ static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t 
     const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
     if (e != cudaSuccess) return e;
-    configured[check] = smem;
+    if (seen) seen->store(smem, std::memory_order_relaxed);
   }
   // Programmatic dependent launch: the kernel's prologue (barriers, column
   // table) may overlap the tail of the table-packing kernel before it; every
