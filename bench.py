@@ -62,7 +62,20 @@ def dist_env():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # functional test of the multi-rank logic on a 1-GPU box (numbers
+    # meaningless): every rank on device 0, gloo for the host-side collectives
+    if os.environ.get("BENCH_SINGLE_DEVICE_TEST"):
+        local = 0
     return rank, world, local
+
+
+def init_dist(dev):
+    import torch.distributed as dist
+
+    if os.environ.get("BENCH_SINGLE_DEVICE_TEST"):
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
 
 
 def workload_config(world):
@@ -214,9 +227,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
 
     import __graft_entry__
 
@@ -451,7 +462,7 @@ def run_secondary(a):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     import __graft_entry__
 
     __graft_entry__.build_library()
