@@ -356,9 +356,13 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
 
     // chunk range [klo, khi) of row y of this segment; the warp takes
     // klo + warp, klo + warp + NW, ...
+    // in 32-bit: the only rows with a partial chunk range are the CTA's first
+    // (row yf of this segment, or none: -1) and last (yl, or beyond y_last)
     const long long rb0 = (long long)b * p.h;
-    auto klo = [&](int y) { return rb0 + y == r_begin ? k_first : 0; };
-    auto khi = [&](int y) { return rb0 + y == r_end - 1 ? k_last : cpr; };
+    const int yf = r_begin - rb0 < 0 ? -1 : (int)(r_begin - rb0);
+    const int yl = (int)min(r_end - 1 - rb0, (long long)p.h);
+    auto klo = [&](int y) { return y == yf ? k_first : 0; };
+    auto khi = [&](int y) { return y == yl ? k_last : cpr; };
     // move (y, k) forward to this warp's next chunk (y > y_last: none left)
     auto settle = [&](int& y, int& k) {
       while (y <= y_last && k >= khi(y)) {
@@ -400,9 +404,12 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       float4* S = slots + (n % kRing) * nent;
       // only the x-cells this CTA's chunks of row y touch (all of them for a
       // full row; a partial first / last row of a chunk range needs fewer)
-      const int x_lo = klo(y) * CH, x_hi = min(khi(y) * CH, p.w) - 1;
-      const int e_lo = x_hi >= x_lo ? jx_of(x_lo) * 3 * (ds - 1) : 0;
-      const int e_hi = x_hi >= x_lo ? (jx_of(x_hi) + 1) * 3 * (ds - 1) : 0;
+      int e_lo = 0, e_hi = nent;  // a full row touches every x-cell
+      if (y == yf || y == yl) {
+        const int x_lo = klo(y) * CH, x_hi = min(khi(y) * CH, p.w) - 1;
+        e_lo = x_hi >= x_lo ? jx_of(x_lo) * 3 * (ds - 1) : 0;
+        e_hi = x_hi >= x_lo ? (jx_of(x_hi) + 1) * 3 * (ds - 1) : 0;
+      }
       for (int e = e_lo + warp * 32 + lane; e < e_hi; e += NW * 32) {
         const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
         const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
