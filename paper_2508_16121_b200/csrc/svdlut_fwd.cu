@@ -128,6 +128,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 // ~92 KB of L1 for the texture-path LUT pair
 #define FWD_GRID_SMEM 1  // 0 measured slower (73.9 vs 70.1 us smooth, 153 vs 149 uniform)
 #endif
+#ifndef FWD_COLTAB_MAXW
+// column brackets from a per-CTA shared-memory table for rows narrower than
+// this, computed inline per pixel (one f64 multiply) for wider rows: the
+// table's LDS costs shared-pipe wavefronts, the inline path ALU work; measured
+// 4K smooth 67.6 -> 66.9 us inline, 8 x 1080p 155.1 -> 156.4 us inline
+#define FWD_COLTAB_MAXW 2560
+#endif
+#ifndef FWD_BREUSE
+// 1: the colour brackets of pair gb's axes (g, b), computed one pixel ahead
+// for the texture gathers, are reused for pairs rg / rb instead of being
+// recomputed (same cbracket, same values)
+#define FWD_BREUSE 1
+#endif
 #ifndef FWD_TGT_LATE
 // L2-loss epilogue: 1 loads the target chunk right before the epilogue (its
 // 12 registers are not live across the pixel math, but the load latency is
@@ -480,10 +493,11 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
         float o0[PX], o1[PX], o2[PX];
         float4 tx0, tx1, tx2;  // in-flight texture cells of the next pixel
         float tdg, tdb;        // its deltas
+        uint32_t nbg, nbb;     // and its colour brackets (g, b)
         {
-          const uint32_t bg = cbracket(__saturatef(cur.g[0]), tdm1, tdm2, tdg);
-          const uint32_t bb = cbracket(__saturatef(cur.b[0]), tdm1, tdm2, tdb);
-          const int ti = (int)(bg * cst3 + bb * 3u + texK);
+          nbg = cbracket(__saturatef(cur.g[0]), tdm1, tdm2, tdg);
+          nbb = cbracket(__saturatef(cur.b[0]), tdm1, tdm2, tdb);
+          const int ti = (int)(nbg * cst3 + nbb * 3u + texK);
           tx0 = texv4(p.tex, ti);
           tx1 = texv4(p.tex, ti + 1);
           tx2 = texv4(p.tex, ti + 2);
@@ -496,8 +510,14 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
                       qb = __saturatef(cur.b[u]);
           float dr, dg_, db_;
           const uint32_t br = cbracket(qr, tdm1, tdm2, dr);
+#if FWD_BREUSE
+          const uint32_t bg = nbg, bb = nbb;
+          dg_ = dg;
+          db_ = db;
+#else
           const uint32_t bg = cbracket(qg, tdm1, tdm2, dg_);
           const uint32_t bb = cbracket(qb, tdm1, tdm2, db_);
+#endif
           float er, eg, eb;
           const uint32_t sr = cbracket(qr, sdm1, sdm2, er);
           const uint32_t sg = cbracket(qg, sdm1, sdm2, eg);
@@ -518,9 +538,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
             // gathers: the index carries a (never taken) dependency on the
             // last LDS so ptxas cannot hoist every TLD of the chunk to its top
             // (which starves the LDS of registers)
-            const uint32_t bg1 = cbracket(__saturatef(cur.g[u + 1]), tdm1, tdm2, tdg);
-            const uint32_t bb1 = cbracket(__saturatef(cur.b[u + 1]), tdm1, tdm2, tdb);
-            const int ti = (int)(bg1 * cst3 + bb1 * 3u + texK) + (FWD_TEXDEP && s2.w != s2.w ? 1 : 0);
+            nbg = cbracket(__saturatef(cur.g[u + 1]), tdm1, tdm2, tdg);
+            nbb = cbracket(__saturatef(cur.b[u + 1]), tdm1, tdm2, tdb);
+            const int ti = (int)(nbg * cst3 + nbb * 3u + texK) + (FWD_TEXDEP && s2.w != s2.w ? 1 : 0);
             tx0 = texv4(p.tex, ti);
             tx1 = texv4(p.tex, ti + 1);
             tx2 = texv4(p.tex, ti + 2);
@@ -860,7 +880,7 @@ static cudaError_t launch_fwd_impl(const void* in, int in_fmt, void* out, int ou
   if (grid > chunks) grid = chunks;
   size_t smem = fwd_smem_bytes(L.dt, L.ds);
   const size_t col_bytes = (size_t)((w + 3) & ~3) * 4;
-  p.col_smem = smem + col_bytes <= kSmemForL1Tex ? 1 : 0;
+  p.col_smem = w < FWD_COLTAB_MAXW && smem + col_bytes <= kSmemForL1Tex ? 1 : 0;
   if (p.col_smem) smem += col_bytes;
   const bool chk = nonfinite != nullptr;
   const int g = (int)grid;
