@@ -43,6 +43,14 @@ constexpr int kBwdL2Rows = 2;
 #ifndef BWD_SPREAD
 #define BWD_SPREAD 1  // 1: a warp's lanes 60 px apart; 0: 32 consecutive 4-px groups
 #endif
+#ifndef BWD_RB
+// rows per CTA barrier: slot rows are produced BWD_RB at a time into a ring
+// of 2 * BWD_RB buffers, so the CTA meets at a barrier once per BWD_RB rows.
+// 2 measured slower (8 x 1080p smooth 882 -> 948 us): the extra 24 KB of
+// slots come out of the L1 that caches the texture-path LUT pair
+#define BWD_RB 1
+#endif
+constexpr int kBwdRb = BWD_RB;
 #ifndef BWD_ROT
 #define BWD_ROT 2  // LUT scatter order per lane: 0 fixed, 1 rotated channels, 2 + rotated corners (best)
 #endif  // rows of L2 prefetch distance (X and gY planes)
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const float* gsm = smem - (BWD_TEXLUT ? L.xc_off : 0);  // + table offset -> smem
   const int nent = (ds - 1) * 3 * (ds - 1);
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
-  float* Es = reinterpret_cast<float*>(slots + 2 * nent);  // A.total floats
+  float* Es = reinterpret_cast<float*>(slots + 2 * kBwdRb * nent);  // A.total floats
   const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
   const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
   const uint32_t cst48 = (uint32_t)L.cst * 48u;
@@ -297,20 +305,28 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         "r"(phase)
         : "memory");
     phase ^= 1u;
-    {
-      float ey;
-      const int jy = (int)(row_bracket(p.y0 + y_first, p.rcp_h, sdm1, sdm2, ey) - kMagic);
-      for (int e = threadIdx.x; e < nent; e += blockDim.x) {
-        const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
-        const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-        slots[e] = bgrid_entry(gsm, L, ch, jx, jc, jy, ey);
+    // rows per barrier: rb rows of at most kMaxFlushPx / 2 px each keep the
+    // fixed-point partials in range between the flush checks
+    const int rb = (kBwdRb > 1 && (long long)kBwdRb * p.w <= kMaxFlushPx) ? kBwdRb : 1;
+    // slot rows y0r .. y0r + rb - 1 (clipped to the segment) into ring buffers
+    auto produce_rows = [&](int y0r) {
+      for (int i = 0; i < rb && y0r + i <= y_last; ++i) {
+        float eyp;
+        const int jyp = (int)(row_bracket(p.y0 + y0r + i, p.rcp_h, sdm1, sdm2, eyp) - kMagic);
+        float4* S = slots + ((y0r + i - y_first) % (2 * rb)) * nent;
+        for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+          const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
+          const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
+          S[e] = bgrid_entry(gsm, L, ch, jx, jc, jyp, eyp);
+        }
       }
-    }
+    };
+    produce_rows(y_first);
     __syncthreads();
     float gsum0 = 0.f, gsum1 = 0.f, gsum2 = 0.f;
 
     for (int y = y_first; y <= y_last; ++y) {
-      const int buf = (y - y_first) & 1;
+      const int buf = (y - y_first) % (2 * rb);
       if (threadIdx.x == blockDim.x - 32) {
         for (int yy = (y == y_first ? y + 1 : y + kBwdL2Rows); yy <= y + kBwdL2Rows && yy <= y_last; ++yy) {
           bprefetch_row(X, pl, yy, p.w);
@@ -536,19 +552,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           }
         }
       }
-      if (y < y_last) {
-        float ey1;
-        const int jy1 = (int)(row_bracket(p.y0 + y + 1, p.rcp_h, sdm1, sdm2, ey1) - kMagic);
-        float4* S = slots + (buf ^ 1) * nent;
-        for (int e = threadIdx.x; e < nent; e += blockDim.x) {
-          const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
-          const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-          S[e] = bgrid_entry(gsm, L, ch, jx, jc, jy1, ey1);
-        }
-      }
-      __syncthreads();
       px_since_flush += p.w;
-      if (px_since_flush + p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
+      if ((y - y_first) % rb != rb - 1 && y < y_last) continue;  // barrier once per rb rows
+      if (y < y_last) produce_rows(y + 1);  // the other half of the ring
+      __syncthreads();
+      if (px_since_flush + rb * p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
         for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
           const int v = Ei[i];
           if (v != 0) {
@@ -669,7 +677,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
   const size_t staged = (size_t)L.staged_bytes() - (BWD_TEXLUT ? (size_t)L.xc_off * 4 : 0);
-  const size_t smem = staged + 2 * (size_t)nent * 16 + (size_t)A.total * 4;
+  const size_t smem = staged + 2 * kBwdRb * (size_t)nent * 16 + (size_t)A.total * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
   float* tables = (float*)wp;
