@@ -11,7 +11,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "../../include/svdlut_b200.h"
 #include "svdlut_common.cuh"
@@ -23,11 +27,82 @@ using namespace svdlut;
 
 constexpr int kMaxStrips = 32;
 
+// Host copy pool: a few threads that copy a strip between pageable user
+// memory and page-locked staging in parallel (one thread moves ~10 GB/s, the
+// PCIe link ~50 GB/s per direction).
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // runs f(0..n-1) on the pool and the calling thread; returns when all are done
+  void run(int n, const std::function<void(int)>& f) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &f;
+      n_ = n;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(m_);
+    done_cv_.wait(g, [this] { return done_ == n_; });
+    job_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      int i;
+      const std::function<void(int)>* f;
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (!job_ || next_ >= n_) return;
+        i = next_++;
+        f = job_;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> g(m_);
+      if (++done_ == n_) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, next_ = 0, done_ = 0;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+};
+
 struct svdlut_ctx {
   int device = 0;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // copy-in, compute, copy-out
   cudaEvent_t ev_in[kMaxStrips] = {};
   cudaEvent_t ev_k[kMaxStrips] = {};
+  cudaEvent_t ev_out[kMaxStrips] = {};
   void* d_img = nullptr;  // input strips followed by output strips
   size_t d_img_bytes = 0;
   void* d_par = nullptr;  // parameters + packed tables + workspaces
@@ -35,6 +110,10 @@ struct svdlut_ctx {
   int* h_flag = nullptr;  // pinned flag readback
   float* h_stage = nullptr;  // pinned staging for small host transfers
   size_t h_stage_bytes = 0;
+  // pageable images: two page-locked strip slots per direction + copy pool
+  char* h_strip = nullptr;
+  size_t h_strip_bytes = 0;
+  CopyPool* pool = nullptr;
   std::mutex mu;
 };
 
@@ -84,6 +163,7 @@ svdlut_ctx* svdlut_ctx_create(int device) {
   for (int i = 0; i < kMaxStrips; ++i) {
     ok &= cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming) == cudaSuccess;
+    ok &= cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming) == cudaSuccess;
   }
   ok &= cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault) == cudaSuccess;
   if (!ok) {
@@ -103,11 +183,14 @@ void svdlut_ctx_destroy(svdlut_ctx* c) {
   if (c->d_par) cudaFree(c->d_par);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->h_strip) cudaFreeHost(c->h_strip);
+  delete c->pool;
   for (int i = 0; i < 3; ++i)
     if (c->st[i]) cudaStreamDestroy(c->st[i]);
   for (int i = 0; i < kMaxStrips; ++i) {
     if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
     if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
+    if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
   }
   delete c;
 }
@@ -235,6 +318,77 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     fprintf(stderr, "host in %p type %d, out %p type %d (1 = page-locked), %d strips\n", rgb,
             oki ? (int)ai.type : -1, out, oko ? (int)ao.type : -1, n_strips);
   }
+  // Pageable user buffers (plain numpy arrays) go through two page-locked
+  // strip slots per direction, filled / drained by the copy pool, so the
+  // copy engines still see page-locked strips (a pageable cudaMemcpy is staged
+  // by the driver one piece at a time: 4K f32 8.9 ms instead of ~2.6).
+  auto page_locked = [](const void* ptr) {
+    cudaPointerAttributes a;
+    const bool ok = cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  const bool stage_in = !page_locked(rgb), stage_out = !page_locked(out);
+  char* slot_in[2] = {nullptr, nullptr};
+  char* slot_out[2] = {nullptr, nullptr};
+  if (stage_in || stage_out) {
+    size_t strip_max = 0;
+    for (int s = 0; s < n_strips; ++s)
+      strip_max = std::max(strip_max, (size_t)3 * (bounds[s + 1] - bounds[s]) * w * std::max(ib, ob));
+    const size_t slot = rup(strip_max);
+    if (ctx->h_strip_bytes < 4 * slot) {
+      if (ctx->h_strip) cudaFreeHost(ctx->h_strip);
+      ctx->h_strip = nullptr;
+      ctx->h_strip_bytes = 0;
+      if (cudaHostAlloc((void**)&ctx->h_strip, 4 * slot, cudaHostAllocDefault) != cudaSuccess)
+        return SVDLUT_ERR_CUDA;
+      ctx->h_strip_bytes = 4 * slot;
+    }
+    if (!ctx->pool) {
+      static const int n_threads = [] {
+        const char* e = getenv("SVDLUT_COPY_THREADS");  // pool size (the caller also copies)
+        if (e && atoi(e) > 0) return atoi(e);
+        // 4K f32 from pageable memory on a 16-core host: 3 threads 3.13 ms,
+        // 7 threads 3.10 ms, 11 threads 5.3 ms (contention with the driver)
+        const unsigned hc = std::thread::hardware_concurrency();
+        return (int)std::max(1u, std::min(5u, hc / 2));
+      }();
+      ctx->pool = new CopyPool(n_threads);
+    }
+    for (int i = 0; i < 2; ++i) {
+      slot_in[i] = ctx->h_strip + i * slot;
+      slot_out[i] = ctx->h_strip + (2 + i) * slot;
+    }
+  }
+  // copies strip rows [r0, r0 + hs) between the user image and a slot laid
+  // out like the device strip ((3, hs, w) for f32, rows for HWC), in ~1 MB pieces
+  auto strip_copy = [&](int r0, int hs, char* slotp, bool to_slot) {
+    struct Part { const char* src; char* dst; size_t n; };
+    Part parts[3];
+    int np_ = 0;
+    if ((to_slot ? in_fmt : out_fmt) == kF32) {
+      for (int c = 0; c < 3; ++c) {
+        const size_t user_off = ((size_t)c * plane + (size_t)r0 * w) * 4, slot_off = (size_t)c * hs * w * 4;
+        const size_t n = (size_t)hs * w * 4;
+        parts[np_++] = to_slot ? Part{(const char*)rgb + user_off, slotp + slot_off, n}
+                               : Part{slotp + slot_off, (char*)out + user_off, n};
+      }
+    } else {
+      const size_t eb = to_slot ? ib : ob;
+      const size_t user_off = (size_t)3 * r0 * w * eb, n = (size_t)3 * hs * w * eb;
+      parts[np_++] = to_slot ? Part{(const char*)rgb + user_off, slotp, n}
+                             : Part{slotp, (char*)out + user_off, n};
+    }
+    constexpr size_t kPiece = 1 << 20;
+    int pieces[3], total = 0;
+    for (int i = 0; i < np_; ++i) total += (pieces[i] = (int)((parts[i].n + kPiece - 1) / kPiece));
+    ctx->pool->run(total, [&](int t) {
+      int i = 0;
+      while (t >= pieces[i]) t -= pieces[i++];
+      const size_t off = (size_t)t * kPiece, n = std::min(kPiece, parts[i].n - off);
+      memcpy(parts[i].dst + off, parts[i].src + off, n);
+    });
+  };
   for (int s = 0; s < n_strips; ++s) {
     const int r0 = bounds[s], r1 = bounds[s + 1];
     const int hs = r1 - r0;
@@ -242,7 +396,13 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     // rows [r0, r1) contiguous, as on the host
     char* din = d_in + (size_t)3 * r0 * w * ib;
     char* dout = d_out + (size_t)3 * r0 * w * ob;
-    if (in_fmt == kF32) {  // the strip's 3 channel slabs: one 2D copy (host pitch = plane)
+    if (stage_in) {  // slot s % 2 is free once the H2D of strip s - 2 is done
+      if (s >= 2 && cudaEventSynchronize(ctx->ev_in[s - 2]) != cudaSuccess) return SVDLUT_ERR_CUDA;
+      strip_copy(r0, hs, slot_in[s & 1], true);
+      if (cudaMemcpyAsync(din, slot_in[s & 1], (size_t)3 * hs * w * ib, cudaMemcpyHostToDevice, s_in) !=
+          cudaSuccess)
+        return SVDLUT_ERR_CUDA;
+    } else if (in_fmt == kF32) {  // the strip's 3 channel slabs: one 2D copy (host pitch = plane)
       if (cudaMemcpy2DAsync(din, (size_t)hs * w * 4, (const float*)rgb + (size_t)r0 * w, plane * 4,
                             (size_t)hs * w * 4, 3, cudaMemcpyHostToDevice, s_in) != cudaSuccess)
         return SVDLUT_ERR_CUDA;
@@ -265,7 +425,16 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     if (trace) cudaEventRecord(tev[3 * s + 1], s_k);
     if (cudaEventRecord(ctx->ev_k[s], s_k) != cudaSuccess) return SVDLUT_ERR_CUDA;
     if (cudaStreamWaitEvent(s_out, ctx->ev_k[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
-    if (out_fmt == kF32) {
+    if (stage_out) {  // slot s % 2 still holds strip s - 2: drain it to the user buffer first
+      if (s >= 2) {
+        if (cudaEventSynchronize(ctx->ev_out[s - 2]) != cudaSuccess) return SVDLUT_ERR_CUDA;
+        strip_copy(bounds[s - 2], bounds[s - 1] - bounds[s - 2], slot_out[s & 1], false);
+      }
+      if (cudaMemcpyAsync(slot_out[s & 1], dout, (size_t)3 * hs * w * ob, cudaMemcpyDeviceToHost, s_out) !=
+              cudaSuccess ||
+          cudaEventRecord(ctx->ev_out[s], s_out) != cudaSuccess)
+        return SVDLUT_ERR_CUDA;
+    } else if (out_fmt == kF32) {
       if (cudaMemcpy2DAsync((float*)out + (size_t)r0 * w, plane * 4, dout, (size_t)hs * w * 4,
                             (size_t)hs * w * 4, 3, cudaMemcpyDeviceToHost, s_out) != cudaSuccess)
         return SVDLUT_ERR_CUDA;
@@ -286,6 +455,12 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
       fprintf(stderr, "strip %2d  h2d done %7.3f  kernel done %7.3f  d2h done %7.3f ms\n", s, t[0], t[1], t[2]);
     }
     for (auto& e : tev) cudaEventDestroy(e);
+  }
+  if (stage_out) {
+    for (int s = std::max(0, n_strips - 2); s < n_strips; ++s) {
+      if (cudaEventSynchronize(ctx->ev_out[s]) != cudaSuccess) return SVDLUT_ERR_CUDA;
+      strip_copy(bounds[s], bounds[s + 1] - bounds[s], slot_out[s & 1], false);
+    }
   }
   // the last kernel's event already orders every flag write before s_out
   if (cudaMemcpyAsync(ctx->h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s_out) != cudaSuccess)

@@ -209,3 +209,34 @@ def test_enhance_payload_many_strips_equals_device(dev, fmt, w, h):
                          out_fmt=fmt)[0].cpu().numpy()
     dv = dv if fmt == "u8" else from_be_bytes(dv)
     assert np.array_equal(np.asarray(got).astype(np.int64), dv.astype(np.int64))
+
+
+@pytest.mark.parametrize("pinned_in,pinned_out", [(False, False), (True, False), (False, True)])
+def test_enhance_payload_pageable_buffers(dev, pinned_in, pinned_out):
+    """Pageable payloads (plain numpy arrays) travel through the context's
+    page-locked strip slots; the result equals the page-locked path bit for bit."""
+    import torch
+
+    from paper_2508_16121_b200 import device, synth, transform
+    from paper_2508_16121_b200.core_types import GridSet, GridWeights, Lut2DSet, LutWeights
+
+    c = synth.make_case(6, h=8, w=8)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)[None]  # noqa: E731
+    planes = device.reconstruct(T(c.u), T(c.s), T(c.vt))
+    model = (Lut2DSet(planes[0].cpu().numpy()), LutWeights(c.lw, c.lb), GridSet(c.grid_planes),
+             GridWeights(c.gw, c.gb))
+    h, w = 1499, 2001
+    rng = np.random.default_rng(13)
+    img = rng.integers(0, 256, (h, w, 3)).astype(np.uint8)
+    src = img
+    if pinned_in:
+        src = torch.empty((h, w, 3), dtype=torch.uint8, pin_memory=True).numpy()
+        src[...] = img
+    out = (torch.empty((h, w, 3), dtype=torch.uint8, pin_memory=True).numpy() if pinned_out
+           else np.empty((h, w, 3), np.uint8))
+    got = transform.enhance_payload(src, *model, out=out)
+    assert got is out
+    ref_in = torch.empty((h, w, 3), dtype=torch.uint8, pin_memory=True).numpy()
+    ref_in[...] = img
+    want = transform.enhance_payload(ref_in, *model)
+    assert np.array_equal(got, want)
