@@ -387,6 +387,18 @@ def main():
                "d2h_bytes_per_step": int(y.data.nbytes + 9 * 33 * 33 * 4),
                "ms_per_step": round(ems, 4),
                "api": "svd.reconstruct_lut + transform.fused_enhance (pinned host arrays)"}
+        # the reference's usual caller hands in a plain (pageable) numpy array
+        img_pg = Image(W, H, np.array(case.rgb, copy=True))
+        for _ in range(2):
+            transform.fused_enhance(img_pg, svd.reconstruct_lut(factors), lw, grids, gw)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(esteps):
+            transform.fused_enhance(img_pg, svd.reconstruct_lut(factors), lw, grids, gw)
+        pms = max_over_ranks(1e3 * (time.perf_counter() - t0) / esteps)
+        e2e["pageable_input"] = {"value": round(world * H * W / (pms * 1e-3) / 1e6, 3), "unit": UNIT,
+                                 "ms_per_step": round(pms, 4),
+                                 "api": "same call, input Image over a pageable numpy array"}
 
     # ---- the same step on PNM payloads (u8 HWC in/out, decode + quantization fused) ----
     e2e_u8 = None
