@@ -31,7 +31,6 @@ namespace svdlut {
 #endif
 constexpr int kBwdWarps = BWD_NW;
 constexpr int kBPx = 4;
-constexpr int kBChunk = 32 * kBPx;
 constexpr uint32_t kMagic = 0x4B000000u;
 constexpr int kBwdL2Rows = 2;
 #ifndef BWD_TEXLUT
@@ -299,7 +298,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     // texel of cell (a, b) of pair rg / rb: texKrg (+ pair offset) + bits_a*cst3 + bits_b*3
     const uint32_t texKrg = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                             (uint32_t)(L.lut_off / 4) - kMagic * (cst3 + 3u);
-    const uint32_t texKrb = texKrg + (uint32_t)(L.pair_floats / 4);
+    [[maybe_unused]] const uint32_t texKrb = texKrg + (uint32_t)(L.pair_floats / 4);
     asm volatile(
         "{\n.reg .pred p;\nWAITB_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAITB_%=;\n}\n" ::"r"(bar),
         "r"(phase)
@@ -435,10 +434,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
             for (int pr = 0; pr < 3; ++pr) {
               const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
               const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
+              int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
+#if BWD_ROT < 2
               const float w00 = (1.f - da) * (1.f - dbb), w10 = da * (1.f - dbb);
               const float w01 = (1.f - da) * dbb, w11 = da * dbb;
-              int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
               int* e10 = e + (dt + 1) * 3;
+#endif
 #if BWD_ROT >= 2
               // lane-rotated corner and channel order: lanes of one instruction
               // that share a cell hit up to 12 different words (distinct banks,

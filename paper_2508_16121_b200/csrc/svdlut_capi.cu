@@ -64,7 +64,6 @@ int check_k(int k) {
   return SVDLUT_OK;
 }
 
-size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 
 }  // namespace

@@ -323,12 +323,12 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
   const uint32_t slotK0 = smem_addr(slots) - kMagicBits * 16u;
 
-  // contiguous range of global rows (image b, row y) for this CTA
   // contiguous range of global chunks g = (image b, row y) * cpr + k for this
-  // CTA: rows r_begin .. r_end-1, the first and last possibly partial
+  // CTA: rows r_begin .. r_end-1, the first and last possibly partial (whole
+  // rows unless FWD_CHUNKSPLIT)
   const int cpr = (p.w + CH - 1) / CH;
-  const long long chunks_total = (long long)p.batch * p.h * cpr;
 #if FWD_CHUNKSPLIT
+  const long long chunks_total = (long long)p.batch * p.h * cpr;
   const long long g_begin = (long long)blockIdx.x * chunks_total / gridDim.x;
   const long long g_end = (long long)(blockIdx.x + 1) * chunks_total / gridDim.x;
 #else
