@@ -68,8 +68,8 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
                             const float* __restrict__ lw,
                             const float* __restrict__ lb, const float* __restrict__ gp,
                             const float* __restrict__ gw, const float* __restrict__ gb, int k,
-                            TableLayout L, float* __restrict__ tables) {
-  extern __shared__ float Ts[];  // vertex rows of one LUT plane band
+                            TableLayout L, float* __restrict__ tables, int stage_factors) {
+  extern __shared__ float Ts[];  // vertex rows of one LUT plane band (+ staged factors)
   // let the fused kernel that follows launch and run its prologue (it waits
   // for this grid's completion before reading the tables)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -90,12 +90,30 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
     const int i0 = band * kPackBand, i1 = min(i0 + kPackBand, dt - 1);
     const long long cp = b * 9 + c * 3 + p;
     const int nv = (i1 - i0 + 1) * dt;
-    for (int e = threadIdx.x; e < nv; e += blockDim.x) {
-      const int i = i0 + e / dt, j = e - (e / dt) * dt;
-      if (lp) {
-        Ts[e] = lp[cp * dt * dt + i * dt + j];
-      } else {
-        Ts[e] = lut_entry(fu + cp * dt * ns, fs + cp * ns, fvt + cp * ns * dt, dt, ns, i, j);
+    if (!lp && stage_factors) {
+      // the band's U rows, S and all of Vt into shared memory first (one
+      // round of global latency instead of one per term of every dot product),
+      // then the same f64 sums in the same order
+      float* Us = Ts + (kPackBand + 1) * dt;
+      float* Ss = Us + (kPackBand + 1) * ns;
+      float* Vs = Ss + ns;
+      const float* U = fu + cp * dt * ns + (long long)i0 * ns;
+      for (int e = threadIdx.x; e < (i1 - i0 + 1) * ns; e += blockDim.x) Us[e] = U[e];
+      for (int e = threadIdx.x; e < ns; e += blockDim.x) Ss[e] = fs[cp * ns + e];
+      for (int e = threadIdx.x; e < ns * dt; e += blockDim.x) Vs[e] = fvt[cp * ns * dt + e];
+      __syncthreads();
+      for (int e = threadIdx.x; e < nv; e += blockDim.x) {
+        const int il = e / dt, j = e - il * dt;
+        Ts[e] = lut_entry(Us, Ss, Vs, dt, ns, il, j);
+      }
+    } else {
+      for (int e = threadIdx.x; e < nv; e += blockDim.x) {
+        const int i = i0 + e / dt, j = e - (e / dt) * dt;
+        if (lp) {
+          Ts[e] = lp[cp * dt * dt + i * dt + j];
+        } else {
+          Ts[e] = lut_entry(fu + cp * dt * ns, fs + cp * ns, fvt + cp * ns * dt, dt, ns, i, j);
+        }
       }
     }
     __syncthreads();
@@ -193,13 +211,17 @@ cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const
   const int grid_items = 3 * (L.ds - 1) * (L.ds - 1) + 4 * L.ds * L.ds + 64;
   const int nbands = (L.dt - 1 + kPackBand - 1) / kPackBand;
   dim3 grid(9 * nbands + (grid_items + 255) / 256, batch);
-  const size_t smem = (size_t)(kPackBand + 1) * L.dt * sizeof(float);
+  size_t smem = (size_t)(kPackBand + 1) * L.dt * sizeof(float);
+  // factors path: stage U band rows, S and Vt too when that stays small
+  const size_t fac = ((size_t)(kPackBand + 1) * ns + ns + (size_t)ns * L.dt) * sizeof(float);
+  const int stage = (!lp && smem + fac <= 32 * 1024) ? 1 : 0;
+  if (stage) smem += fac;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  pack_kernel<<<grid, 256, smem, st>>>(lp, fu, fs, fvt, ns, lw, lb, gp, gw, gb, k, L, tables);
+  pack_kernel<<<grid, 256, smem, st>>>(lp, fu, fs, fvt, ns, lw, lb, gp, gw, gb, k, L, tables, stage);
   return cudaGetLastError();
 }
 
