@@ -34,10 +34,23 @@ constexpr int kBPx = 4;
 constexpr uint32_t kMagic = 0x4B000000u;
 constexpr int kBwdL2Rows = 2;
 #ifndef BWD_TEXLUT
-// 1: all three LUT pairs are gathered through the texture path (L1-resident:
-// only the grid block, slots and accumulators occupy shared memory, so ~160 KB
-// of L1 remains); 0: pairs rg / rb staged in shared memory like the forward
-#define BWD_TEXLUT 0  // 1 measured: smooth 880 -> 840 us, uniform noise 938 -> 1136 us (L1 misses)
+// Which LUT pairs the backward gathers through the texture path (L1-cached)
+// instead of staging them in shared memory (pair gb always goes through it):
+//   0  rg and rb in shared memory, like the forward
+//   2  rg through the texture path too (default): 8 x 1080p smooth 883 ->
+//      859 us, uniform noise 940 -> 964 us
+//   1  all three: smooth 835 us but noise 1173 us (L1 misses)
+#define BWD_TEXLUT 2
+#endif
+#if BWD_TEXLUT == 2
+#define BWD_TEX_RG 1
+#define BWD_TEX_RB 0
+#elif BWD_TEXLUT
+#define BWD_TEX_RG 1
+#define BWD_TEX_RB 1
+#else
+#define BWD_TEX_RG 0
+#define BWD_TEX_RB 0
 #endif
 #ifndef BWD_SPREAD
 #define BWD_SPREAD 1  // 1: a warp's lanes 60 px apart; 0: 32 consecutive 4-px groups
@@ -234,9 +247,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // staged prefix: the LUT pairs rg / rb + the grid block, or just the grid block
-  const uint32_t stage_from = BWD_TEXLUT ? (uint32_t)L.xc_off * 4u : 0u;
+  // first staged byte: pairs read through the texture path are not staged
+  const uint32_t stage_from = BWD_TEX_RB ? (uint32_t)L.xc_off * 4u
+                              : BWD_TEX_RG ? (uint32_t)(L.lut_off + L.pair_floats) * 4u : 0u;
   const uint32_t table_bytes = (uint32_t)L.staged_bytes() - stage_from;
-  const float* gsm = smem - (BWD_TEXLUT ? L.xc_off : 0);  // + table offset -> smem
+  const float* gsm = smem - stage_from / 4u;  // + table offset -> smem
   const int nent = (ds - 1) * 3 * (ds - 1);
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
   float* Es = reinterpret_cast<float*>(slots + 2 * kBwdRb * nent);  // A.total floats
@@ -245,7 +260,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const uint32_t cst48 = (uint32_t)L.cst * 48u;
   const uint32_t pair_bytes = (uint32_t)(dt - 1) * cst48;
   const uint32_t cst3 = (uint32_t)L.cst * 3u;
-  const uint32_t lutK = sbase + (uint32_t)L.lut_off * 4u - kMagic * (cst48 + 48u);
+  // (the staged image starts at table byte stage_from)
+  const uint32_t lutK = sbase + (uint32_t)L.lut_off * 4u - stage_from - kMagic * (cst48 + 48u);
   const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;
   const uint32_t jx_bytes = 3u * chan_bytes;
   const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
@@ -380,7 +396,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // ---- input gradient from the coefficient cells ----
           float gar = 0.f, gag = 0.f, gab = 0.f;
           {
-#if BWD_TEXLUT
+#if BWD_TEX_RG
             const int ti = (int)(br * cst3 + bg * 3u + texKrg);  // rg via the texture path
             const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
                          c2 = tex1Dfetch<float4>(p.tex, ti + 2);
@@ -393,7 +409,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
             gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.z);
           }
           {
-#if BWD_TEXLUT
+#if BWD_TEX_RB
             const int ti = (int)(br * cst3 + bb * 3u + texKrb);  // rb via the texture path
             const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
                          c2 = tex1Dfetch<float4>(p.tex, ti + 2);
@@ -677,7 +693,8 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
-  const size_t staged = (size_t)L.staged_bytes() - (BWD_TEXLUT ? (size_t)L.xc_off * 4 : 0);
+  const size_t staged = (size_t)L.staged_bytes() - (BWD_TEX_RB ? (size_t)L.xc_off * 4
+                                                     : BWD_TEX_RG ? (size_t)(L.lut_off + L.pair_floats) * 4 : 0);
   const size_t smem = staged + 2 * kBwdRb * (size_t)nent * 16 + (size_t)A.total * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
