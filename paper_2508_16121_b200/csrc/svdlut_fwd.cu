@@ -248,10 +248,16 @@ __device__ __forceinline__ float4 grid_entry(const GridG& G, int ds, int c, int 
   return make_float4(x.x + q0 + r0, x.z + (q1 - q0), x.y + (r1 - r0), x.w);
 }
 
+#ifndef FWD_TEX_RB
+// 1: pair rb also through the texture path (not staged).  Measured 4K:
+// smooth 66.8 -> 73.0 us, uniform noise 140 -> 314 us (the texture pipe and
+// its L1 become the bound)
+#define FWD_TEX_RB 0
+#endif
 // Shared-memory image of the tables: LUT pairs rg, rb then the grid block
 // (xc, gxy, gyc); pair gb is read through the texture path.
 __host__ __device__ inline uint32_t smem_grid_off(const TableLayout& L) {
-  return 2u * (uint32_t)L.pair_floats * 4u;
+  return (FWD_TEX_RB ? 1u : 2u) * (uint32_t)L.pair_floats * 4u;
 }
 __host__ __device__ inline uint32_t smem_tables_bytes(const TableLayout& L) {
   return smem_grid_off(L) + (FWD_GRID_SMEM ? (uint32_t)(L.lut2_off - L.xc_off) * 4u : 0u);
@@ -372,6 +378,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
     const void* src = Src<IN>::image(p.in, b, pl);
     void* dst = Dst<OUTF>::image(p.out, b, opl);
     const void* tsrc = LOSS ? Src<kF32>::image(p.target, b, pl) : nullptr;
+    // texel index of pair rb's cell (ir, ib) (FWD_TEX_RB) = texKrb + bits_r*cst3 + bits_b*3
+    [[maybe_unused]] const uint32_t texKrb = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
+                                             (uint32_t)((L.lut_off + L.pair_floats) / 4) - kMagicBits * (cst3 + 3u);
     // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                           (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
@@ -561,7 +570,13 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
           // volatile, so program order is issue order): nine LDS.128 in
           // flight per warp instead of one cell's three at a time
           const float4 rg0 = lds4(ag), rg1 = lds4(ag + 16), rg2 = lds4(ag + 32);
+#if FWD_TEX_RB
+          const int tr = (int)(br * cst3 + bb * 3u + texKrb);
+          const float4 rb0 = texv4(p.tex, tr), rb1 = texv4(p.tex, tr + 1), rb2 = texv4(p.tex, tr + 2);
+          (void)ab;
+#else
           const float4 rb0 = lds4(ab), rb1 = lds4(ab + 16), rb2 = lds4(ab + 32);
+#endif
           const float4 s0 = lds4(sa + sr * 16u);
           const float4 s1 = lds4(sa + chan_bytes + sg * 16u);
           const float4 s2 = lds4(sa + 2u * chan_bytes + sb * 16u);
