@@ -32,7 +32,10 @@ namespace svdlut {
 constexpr int kBwdWarps = BWD_NW;
 constexpr int kBPx = 4;
 constexpr uint32_t kMagic = 0x4B000000u;
-constexpr int kBwdL2Rows = 2;
+#ifndef BWD_L2ROWS
+#define BWD_L2ROWS 2  // rows of L2 prefetch distance (X and gY planes)
+#endif
+constexpr int kBwdL2Rows = BWD_L2ROWS;
 #ifndef BWD_TEXLUT
 // Which LUT pairs the backward gathers through the texture path (L1-cached)
 // instead of staging them in shared memory (pair gb always goes through it):
