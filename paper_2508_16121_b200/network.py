@@ -245,6 +245,55 @@ class Generator:
 
         return device.apply(rgb, self.tables(rgb), out=out)
 
+    def graphed(self, shape):
+        """Enhance for a fixed (B, 3, H, W) as one CUDA-graph replay.
+
+        At batch 1 the pipeline is ~40 small launches (resize, five convs with
+        their norms, four heads, table packing, apply) and launch latency is
+        most of its time; the graph replays them back to back.  Returns
+        ``run(rgb) -> out``: ``rgb`` is copied into the graph's static input
+        and ``out`` is the graph's static output tensor (overwritten by the
+        next call).
+        """
+        import torch
+
+        shape = tuple(int(v) for v in shape)
+        x = torch.zeros(shape, dtype=torch.float32, device=self.device)
+        out = torch.empty_like(x)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            for _ in range(2):  # allocations, kernel attributes, texture objects
+                self.enhance(x, out=out)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        # relaxed: the apply may create a texture object over the graph pool's
+        # table buffer while capturing (not a stream operation)
+        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+            self.enhance(x, out=out)
+
+        def run(rgb):
+            if tuple(rgb.shape) != shape:
+                raise DimensionMismatch(f"graph was captured for {shape}, got {tuple(rgb.shape)}")
+            x.copy_(rgb, non_blocking=True)
+            graph.replay()
+            return out
+
+        run.graph = graph  # keeps the capture (and its memory pool) alive with the closure
+        return run
+
+    def enhance_replayed(self, rgb):
+        """``enhance`` through a CUDA graph captured on the first call for
+        each input shape (kept for the last four shapes).  The returned tensor
+        is the graph's static output: consume it before the next call."""
+        key = tuple(rgb.shape)
+        cache = self.__dict__.setdefault("_graphs", {})
+        if key not in cache:
+            if len(cache) >= 4:
+                cache.pop(next(iter(cache)))
+            cache[key] = self.graphed(key)
+        return cache[key](rgb)
+
 
 def backbone_forward(img, params, device="cuda"):
     """Context vector (32m,) of one reference-style Image (network.py:115-128)."""
@@ -274,7 +323,10 @@ def run_model(img, params, fused=True, threads=1, device="cuda"):
     del fused, threads
     from . import transform
 
-    gen = params if isinstance(params, Generator) else Generator(params, device)
+    reuse = isinstance(params, Generator)
+    gen = params if reuse else Generator(params, device)
     rgb = torch.from_numpy(np.array(img.data, np.float32))[None].to(gen.device)
-    y = gen.enhance(rgb)[0].cpu().numpy()
+    # a Generator that is reused across calls replays a per-shape CUDA graph
+    # (batch 1 is launch-bound); a one-off call runs eagerly
+    y = (gen.enhance_replayed(rgb) if reuse else gen.enhance(rgb))[0].cpu().numpy()
     return transform._image_type(img)(img.width, img.height, y)

@@ -128,3 +128,42 @@ def test_batched_enhance_equals_per_image():
     for i in range(3):
         yi = gen.enhance(x[i:i + 1].contiguous())[0]
         assert float((yb[i] - yi).abs().max()) <= OUT_TOL
+
+
+@pytest.mark.gpu
+def test_graphed_enhance_equals_eager():
+    """Generator.graphed (one CUDA-graph replay of backbone + heads + pack +
+    apply) returns the eager pipeline's output bit for bit, on fresh inputs."""
+    import torch
+
+    import __graft_entry__
+    from paper_2508_16121_b200 import network
+
+    __graft_entry__.build_library()
+    gen = network.Generator(network.random_init(0))
+    run = gen.graphed((1, 3, 96, 160))
+    rng = np.random.default_rng(4)
+    for _ in range(3):
+        x = torch.from_numpy(rng.random((1, 3, 96, 160), dtype=np.float32)).cuda()
+        got = run(x).clone()
+        assert torch.equal(got, gen.enhance(x))
+
+
+@pytest.mark.gpu
+def test_run_model_with_reused_generator_replays_graph():
+    """run_model with a Generator instance (reused across calls) replays a
+    per-shape CUDA graph and returns what the one-off eager call returns."""
+    import __graft_entry__
+    from paper_2508_16121_b200 import network
+    from paper_2508_16121_b200.core_types import Image
+
+    __graft_entry__.build_library()
+    params = network.random_init(0)
+    gen = network.Generator(params)
+    rng = np.random.default_rng(8)
+    for hw in ((64, 96), (64, 96), (48, 80)):
+        img = Image(hw[1], hw[0], rng.random((3, *hw), dtype=np.float32))
+        want = network.run_model(img, params)
+        got = network.run_model(img, gen)
+        assert np.array_equal(got.data, want.data)
+    assert len(gen._graphs) == 2
