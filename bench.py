@@ -48,7 +48,6 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["mine", "reference"], default="mine")
-    ap.add_argument("--variant", type=int, default=-1, help="fused kernel lane mapping (0/1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
@@ -250,7 +249,7 @@ def main():
         # reconstruct(U,S,Vt) fused into the table packing, then the apply
         tables = device.pack_tables_factors(p["u"], p["s"], p["vt"], p["lw"], p["lb"],
                                             p["grid_planes"], p["gw"], p["gb"])
-        device.apply(ins[i % N_ROT], tables, out=outs[i % N_ROT], variant=a.variant)
+        device.apply(ins[i % N_ROT], tables, out=outs[i % N_ROT])
         return tables
 
     # CUDA graphs: G_r holds r consecutive steps (factors->tables prologue +
@@ -272,7 +271,7 @@ def main():
         apply_graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(apply_graph, capture_error_mode="relaxed"):
             for i in range(N_ROT):
-                device.apply(ins[i], tables0, out=outs[i], variant=a.variant)
+                device.apply(ins[i], tables0, out=outs[i])
 
     def run_steps(n, start=0):
         """n consecutive steps (graph replays when graphs are on)."""
@@ -326,7 +325,7 @@ def main():
             apply_graph.replay()
         else:
             for j in range(N_ROT):
-                device.apply(ins[j], tables0, out=outs[j], variant=a.variant)
+                device.apply(ins[j], tables0, out=outs[j])
     k1.record(stream)
     torch.cuda.synchronize(dev)
     kms = k0.elapsed_time(k1) / kreps

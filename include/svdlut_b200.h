@@ -119,10 +119,10 @@ int svdlut_fused_fwd_packed(const float* rgb, int batch, int h, int w, int y0, i
 
 /* As svdlut_fused_fwd_packed, plus: `nonfinite` (device int, may be NULL) is
  * OR-ed with 1 if any output sample is NaN/Inf (the check core_types.py:55-59
- * does on the host).  `variant` is reserved (pass -1). */
+ * does on the host). */
 int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0, int h_total,
                                const void* tables, int d_t, int d_s, float* out, void* workspace,
-                               size_t workspace_bytes, int* nonfinite, int variant, void* stream);
+                               size_t workspace_bytes, int* nonfinite, void* stream);
 
 /* Reference-shaped entry: pack + apply.  `workspace` >= svdlut_workspace_bytes. */
 /* Sample formats of the _io entry points.  F32: planar float32 (B,3,H,W).

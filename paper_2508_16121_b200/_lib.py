@@ -33,7 +33,7 @@ _SIGS = {
                                         _vp, _vp]),
     "svdlut_fused_fwd_packed": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp, _sz, _vp]),
     "svdlut_fused_fwd_packed_ex": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp, _sz, _vp,
-                                        _i, _vp]),
+                                        _vp]),
     "svdlut_fused_fwd": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,
                               _vp, _vp, _sz, _vp]),
     "svdlut_fused_fwd_exact": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i,

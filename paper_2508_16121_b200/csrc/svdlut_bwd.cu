@@ -5,19 +5,22 @@
 //
 // fused_bwd_kernel mirrors the forward kernel's structure (svdlut_fwd.cu):
 // persistent CTA per SM over a contiguous row range, the same packed
-// coefficient tables staged by TMA (LUT pairs rg/rb + grids in shared memory,
-// pair gb through the texture path), the same per-row merged grid slots.
+// coefficient tables (LUT pair rb's chunk planes + the grid block staged in
+// shared memory by TMA, pairs rg and gb gathered through the texture path),
+// per-row merged grid slots.
 //   gX    from the coefficient form: d/da (A + B a + C b + D a b) = B + D b,
 //         d/db = C + D a; grid slot d/dec = M' + N' ex; the strict clamp of
 //         interp.py:37-40 zeroes the gradient outside [0, 1].
 //   E     UNWEIGHTED scatter sums  E_lut[p][i][j][c] = sum gY_c w_ij and
-//         E_grid[q][c][a][b], accumulated per CTA in shared memory.  Lanes
-//         holding the same cell are aggregated first (warp match + shuffle
-//         group sums), so each distinct cell costs one shared atomic per
-//         value per warp instruction; the xy plane (x-cell almost uniform per
-//         chunk, y-cell uniform per row) is summed in registers per chunk.
-//   flush at the end of each image phase: non-zero shared sums -> global E
-//         (one native f32 RED each).
+//         E_grid[q][c][a][b], accumulated per CTA in shared memory as 32-bit
+//         fixed point (native ATOMS.ADD; shared f32 atomics are CAS loops).
+//         A warp's lanes sit 60 px apart (unrelated cells on smooth images)
+//         and each lane issues its 36 LUT atomics in a lane-rotated corner /
+//         channel order, so lanes sharing a cell hit different banks; the xc
+//         / yc grid planes are summed in per-lane registers over runs of
+//         equal (x-cell, guide cell) and the xy plane per chunk.
+//   flush to the global f32 accumulators before any fixed-point partial can
+//         pass 2^31, and at the end of each image.
 // finalize_kernel: dlut = lw * E, dlw = <T, E>, dgrid[k,q] = gw[k,q] * E[q][k%3],
 // dgw = <G, E>, dlb / dgb from the per-image gY sums.
 #include <cstdint>
@@ -26,49 +29,10 @@
 
 namespace svdlut {
 
-#ifndef BWD_NW
-#define BWD_NW 15
-#endif
-constexpr int kBwdWarps = BWD_NW;
+constexpr int kBwdWarps = 15;
 constexpr int kBPx = 4;
 constexpr uint32_t kMagic = 0x4B000000u;
-#ifndef BWD_L2ROWS
-#define BWD_L2ROWS 2  // rows of L2 prefetch distance (X and gY planes)
-#endif
-constexpr int kBwdL2Rows = BWD_L2ROWS;
-#ifndef BWD_TEXLUT
-// Which LUT pairs the backward gathers through the texture path (L1-cached)
-// instead of staging them in shared memory (pair gb always goes through it):
-//   0  rg and rb in shared memory, like the forward
-//   2  rg through the texture path too (default): 8 x 1080p smooth 883 ->
-//      859 us, uniform noise 940 -> 964 us
-//   1  all three: smooth 835 us but noise 1173 us (L1 misses)
-#define BWD_TEXLUT 2
-#endif
-#if BWD_TEXLUT == 2
-#define BWD_TEX_RG 1
-#define BWD_TEX_RB 0
-#elif BWD_TEXLUT
-#define BWD_TEX_RG 1
-#define BWD_TEX_RB 1
-#else
-#define BWD_TEX_RG 0
-#define BWD_TEX_RB 0
-#endif
-#ifndef BWD_SPREAD
-#define BWD_SPREAD 1  // 1: a warp's lanes 60 px apart; 0: 32 consecutive 4-px groups
-#endif
-#ifndef BWD_RB
-// rows per CTA barrier: slot rows are produced BWD_RB at a time into a ring
-// of 2 * BWD_RB buffers, so the CTA meets at a barrier once per BWD_RB rows.
-// 2 measured slower (8 x 1080p smooth 882 -> 948 us): the extra 24 KB of
-// slots come out of the L1 that caches the texture-path LUT pair
-#define BWD_RB 1
-#endif
-constexpr int kBwdRb = BWD_RB;
-#ifndef BWD_ROT
-#define BWD_ROT 2  // LUT scatter order per lane: 0 fixed, 1 rotated channels, 2 + rotated corners (best)
-#endif  // rows of L2 prefetch distance (X and gY planes)
+constexpr int kBwdL2Rows = 2;  // rows of L2 prefetch distance (X and gY planes)
 
 // Bulk L2 prefetch of row y of three planes (16-byte aligned cover, clipped
 // to each plane), no completion tracking.
@@ -133,19 +97,8 @@ struct BwdParams {
 __device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-#ifndef BWD_LDS_PLAIN
-#define BWD_LDS_PLAIN 1  // plain shared loads: the scheduler may reorder them (faster)
-#endif
 __device__ __forceinline__ float4 blds4(uint32_t a) {
-#if BWD_LDS_PLAIN
   return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(a));
-#else
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(a));
-  return v;
-#endif
 }
 __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, float& delta) {
   const float t = fminf(__fmul_rz(q, dm1), dm2);
@@ -188,16 +141,17 @@ __device__ __forceinline__ void grid_flush(int key, const float (&v)[8], int c, 
   atomicAdd(yc + 1, to_fixed(v[6], S)); atomicAdd(yc + ds + 1, to_fixed(v[7], S));
 }
 
-// Merged grid coefficients of channel c at (row jy/ey, x-cell jx, guide cell jc).
-__device__ __forceinline__ float4 bgrid_entry(const float* sm, const TableLayout& L, int c, int jx,
+// Merged grid coefficients of channel c at (row jy/ey, x-cell jx, guide cell
+// jc) from the grid block `gsm` (xc first, svdlut_common.cuh).
+__device__ __forceinline__ float4 bgrid_entry(const float* gsm, const TableLayout& L, int c, int jx,
                                               int jc, int jy, float ey) {
   const int ds = L.ds;
-  const float4 x = reinterpret_cast<const float4*>(sm + L.xc_off)[(c * (ds - 1) + jx) * (ds - 1) + jc];
-  const float* Y = sm + L.gyc_off + c * ds * ds;
+  const float4 x = reinterpret_cast<const float4*>(gsm)[(c * (ds - 1) + jx) * (ds - 1) + jc];
+  const float* Y = gsm + (L.gyc_off - L.xc_off) + c * ds * ds;
   const float y00 = Y[jy * ds + jc], y01 = Y[jy * ds + jc + 1];
   const float y10 = Y[(jy + 1) * ds + jc], y11 = Y[(jy + 1) * ds + jc + 1];
   const float q0 = __fmaf_rn(ey, y10 - y00, y00), q1 = __fmaf_rn(ey, y11 - y01, y01);
-  const float* X = sm + L.gxy_off;
+  const float* X = gsm + (L.gxy_off - L.xc_off);
   const float v00 = X[(jx * ds + jy) * 3 + c], v01 = X[(jx * ds + jy + 1) * 3 + c];
   const float v10 = X[((jx + 1) * ds + jy) * 3 + c], v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
   const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
@@ -242,29 +196,27 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const uint32_t sbase = bsmem_addr(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
-  const int rc0 = lane % 3, rc1 = (lane + 1) % 3, rc2 = (lane + 2) % 3;  // BWD_ROT channel order
-  const int rt = (lane / 3) & 3;                                           // BWD_ROT >= 2 corner order
+  const int rc0 = lane % 3, rc1 = (lane + 1) % 3, rc2 = (lane + 2) % 3;  // lane's channel order
+  const int rt = (lane / 3) & 3;                                           // lane's corner order
 
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // staged prefix: the LUT pairs rg / rb + the grid block, or just the grid block
-  // first staged byte: pairs read through the texture path are not staged
-  const uint32_t stage_from = BWD_TEX_RB ? (uint32_t)L.xc_off * 4u
-                              : BWD_TEX_RG ? (uint32_t)(L.lut_off + L.pair_floats) * 4u : 0u;
-  const uint32_t table_bytes = (uint32_t)L.staged_bytes() - stage_from;
-  const float* gsm = smem - stage_from / 4u;  // + table offset -> smem
+  // staged: pair rb's three chunk planes, then the grid block
+  const uint32_t plane_bytes = (uint32_t)L.plane_floats * 4u;
+  const uint32_t grid_bytes = (uint32_t)L.grid_floats() * 4u;
+  const uint32_t table_bytes = 3u * plane_bytes + grid_bytes;
+  const float* gsm = smem + 3 * L.plane_floats;  // grid block
   const int nent = (ds - 1) * 3 * (ds - 1);
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
-  float* Es = reinterpret_cast<float*>(slots + 2 * kBwdRb * nent);  // A.total floats
+  float* Es = reinterpret_cast<float*>(slots + 2 * nent);  // A.total floats
   const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
   const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
-  const uint32_t cst48 = (uint32_t)L.cst * 48u;
-  const uint32_t pair_bytes = (uint32_t)(dt - 1) * cst48;
-  const uint32_t cst3 = (uint32_t)L.cst * 3u;
-  // (the staged image starts at table byte stage_from)
-  const uint32_t lutK = sbase + (uint32_t)L.lut_off * 4u - stage_from - kMagic * (cst48 + 48u);
+  const uint32_t cst = (uint32_t)L.cst, cst16 = cst * 16u;
+  const uint32_t ptex = (uint32_t)L.plane_floats / 4u;  // texels per plane
+  // smem address of pair rb's cell (bits_r, bits_b), chunk k: lutK + br*cst16 + bb*16 + k*plane_bytes
+  const uint32_t lutK = sbase - kMagic * (cst16 + 16u);
   const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;
   const uint32_t jx_bytes = 3u * chan_bytes;
   const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
@@ -294,14 +246,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(table_bytes)
                    : "memory");
-      for (uint32_t off = 0; off < table_bytes; off += 32768u) {
-        const uint32_t n = min(32768u, table_bytes - off);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                sbase + off),
-            "l"(reinterpret_cast<const char*>(tb) + stage_from + off), "r"(n), "r"(bar)
-            : "memory");
-      }
+      // pair rb's planes are contiguous in the table; the grid block follows them in smem
+      auto copy = [&](uint32_t dst, const char* from, uint32_t bytes) {
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dst + off),
+              "l"(from + off), "r"(min(32768u, bytes - off)), "r"(bar)
+              : "memory");
+      };
+      copy(sbase, reinterpret_cast<const char*>(tb + L.plane_off(1, 0)), 3u * plane_bytes);
+      copy(sbase + 3u * plane_bytes, reinterpret_cast<const char*>(tb + L.xc_off), grid_bytes);
     }
     for (int i = threadIdx.x; i < A.total; i += blockDim.x) Ei[i] = 0;
     const float gm = p.gmax[b];
@@ -312,31 +267,24 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     const float* X = p.rgb + (long long)b * 3 * pl;
     const float* GY = p.gy + (long long)b * 3 * pl;
     float* GX = p.gx ? p.gx + (long long)b * 3 * pl : nullptr;
-    const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
-                          (uint32_t)(L.lut2_off / 4) - kMagic * (cst3 + 3u);
-    // texel of cell (a, b) of pair rg / rb: texKrg (+ pair offset) + bits_a*cst3 + bits_b*3
+    // texel of cell (bits_a, bits_b), chunk k of pair rg / gb: tex* + bits_a*cst + bits_b + k*ptex
     const uint32_t texKrg = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
-                            (uint32_t)(L.lut_off / 4) - kMagic * (cst3 + 3u);
-    [[maybe_unused]] const uint32_t texKrb = texKrg + (uint32_t)(L.pair_floats / 4);
+                            (uint32_t)(L.plane_off(0, 0) / 4) - kMagic * (cst + 1u);
+    const uint32_t texK = texKrg + 6u * ptex;  // pair gb
     asm volatile(
         "{\n.reg .pred p;\nWAITB_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAITB_%=;\n}\n" ::"r"(bar),
         "r"(phase)
         : "memory");
     phase ^= 1u;
-    // rows per barrier: rb rows of at most kMaxFlushPx / 2 px each keep the
-    // fixed-point partials in range between the flush checks
-    const int rb = (kBwdRb > 1 && (long long)kBwdRb * p.w <= kMaxFlushPx) ? kBwdRb : 1;
-    // slot rows y0r .. y0r + rb - 1 (clipped to the segment) into ring buffers
-    auto produce_rows = [&](int y0r) {
-      for (int i = 0; i < rb && y0r + i <= y_last; ++i) {
-        float eyp;
-        const int jyp = (int)(row_bracket(p.y0 + y0r + i, p.rcp_h, sdm1, sdm2, eyp) - kMagic);
-        float4* S = slots + ((y0r + i - y_first) % (2 * rb)) * nent;
-        for (int e = threadIdx.x; e < nent; e += blockDim.x) {
-          const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
-          const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-          S[e] = bgrid_entry(gsm, L, ch, jx, jc, jyp, eyp);
-        }
+    // slot row yr into ring buffer (yr - y_first) % 2
+    auto produce_rows = [&](int yr) {
+      float eyp;
+      const int jyp = (int)(row_bracket(p.y0 + yr, p.rcp_h, sdm1, sdm2, eyp) - kMagic);
+      float4* S = slots + ((yr - y_first) & 1) * nent;
+      for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
+        const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
+        S[e] = bgrid_entry(gsm, L, ch, jx, jc, jyp, eyp);
       }
     };
     produce_rows(y_first);
@@ -344,7 +292,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     float gsum0 = 0.f, gsum1 = 0.f, gsum2 = 0.f;
 
     for (int y = y_first; y <= y_last; ++y) {
-      const int buf = (y - y_first) % (2 * rb);
+      const int buf = (y - y_first) & 1;
       if (threadIdx.x == blockDim.x - 32) {
         for (int yy = (y == y_first ? y + 1 : y + kBwdL2Rows); yy <= y + kBwdL2Rows && yy <= y_last; ++yy) {
           bprefetch_row(X, pl, yy, p.w);
@@ -363,7 +311,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // max lanes per bank, same-address lanes not merged).
       const int slots4 = (p.w + 3) >> 2;
       for (int s0 = 0; s0 < slots4; s0 += kBwdWarps * 32) {
-        const int xl = BWD_SPREAD ? 4 * (s0 + lane * kBwdWarps + warp) : 4 * (s0 + warp * 32 + lane);
+        const int xl = 4 * (s0 + lane * kBwdWarps + warp);
         if (xl >= p.w) continue;
         BChunk cur;
         bload_chunk(X, GY, pl, y, xl - 4 * lane, p.w, lane, vec, cur);
@@ -398,37 +346,27 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           const uint32_t sb = bbracket(qb, sdm1, sdm2, eb);
           // ---- input gradient from the coefficient cells ----
           float gar = 0.f, gag = 0.f, gab = 0.f;
+          // chunks {A0 A1 B0 B1} {C0 C1 D0 D1} {A2 C2 B2 D2} (svdlut_common.cuh):
+          // d/da = B + D b, d/db = C + D a per channel
           {
-#if BWD_TEX_RG
-            const int ti = (int)(br * cst3 + bg * 3u + texKrg);  // rg via the texture path
-            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
-                         c2 = tex1Dfetch<float4>(p.tex, ti + 2);
-#else
-            const uint32_t a = br * cst48 + lutK + bg * 48u;  // rg
-            const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
-#endif
-            // cell_index: B c0.z c0.w c2.y  C c1.x c1.y c2.z  D c1.z c1.w c2.w
-            gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.y);
-            gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.z);
+            const int ti = (int)(br * cst + bg + texKrg);  // rg via the texture path
+            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + (int)ptex),
+                         c2 = tex1Dfetch<float4>(p.tex, ti + 2 * (int)ptex);
+            gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.z);
+            gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-#if BWD_TEX_RB
-            const int ti = (int)(br * cst3 + bb * 3u + texKrb);  // rb via the texture path
-            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
-                         c2 = tex1Dfetch<float4>(p.tex, ti + 2);
-#else
-            const uint32_t a = br * cst48 + lutK + bb * 48u + pair_bytes;  // rb
-            const float4 c0 = blds4(a), c1 = blds4(a + 16), c2 = blds4(a + 32);
-#endif
-            gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.y);
-            gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.z);
+            const uint32_t a = br * cst16 + bb * 16u + lutK;  // rb (shared memory)
+            const float4 c0 = blds4(a), c1 = blds4(a + plane_bytes), c2 = blds4(a + 2u * plane_bytes);
+            gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
+            gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            const int ti = (int)(bg * cst3 + bb * 3u + texK);  // gb via the texture path
-            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + 1),
-                         c2 = tex1Dfetch<float4>(p.tex, ti + 2);
-            gag += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.y);
-            gab += g0 * __fmaf_rn(c1.z, dg, c1.x) + g1 * __fmaf_rn(c1.w, dg, c1.y) + g2 * __fmaf_rn(c2.w, dg, c2.z);
+            const int ti = (int)(bg * cst + bb + texK);  // gb via the texture path
+            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + (int)ptex),
+                         c2 = tex1Dfetch<float4>(p.tex, ti + 2 * (int)ptex);
+            gag += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
+            gab += g0 * __fmaf_rn(c1.z, dg, c1.x) + g1 * __fmaf_rn(c1.w, dg, c1.y) + g2 * __fmaf_rn(c2.w, dg, c2.y);
           }
           const uint32_t sa = slotK + (uint32_t)jx * jx_bytes;
           const float4 s0 = blds4(sa + sr * 16u);
@@ -444,22 +382,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // ---- scatter: LUT pairs, one fixed-point atomic per value ----
           if (valid) {
             const int ir = (int)(br - kMagic), ig = (int)(bg - kMagic), ib = (int)(bb - kMagic);
-#if BWD_ROT >= 1
             const float q0 = rc0 == 0 ? g0 : (rc0 == 1 ? g1 : g2);  // gY in this lane's channel order
             const float q1 = rc1 == 0 ? g0 : (rc1 == 1 ? g1 : g2);
             const float q2 = rc2 == 0 ? g0 : (rc2 == 1 ? g1 : g2);
-#endif
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
               const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
               const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
               int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
-#if BWD_ROT < 2
-              const float w00 = (1.f - da) * (1.f - dbb), w10 = da * (1.f - dbb);
-              const float w01 = (1.f - da) * dbb, w11 = da * dbb;
-              int* e10 = e + (dt + 1) * 3;
-#endif
-#if BWD_ROT >= 2
               // lane-rotated corner and channel order: lanes of one instruction
               // that share a cell hit up to 12 different words (distinct banks,
               // see AccLayout) instead of one address (ATOMS serializes them)
@@ -473,28 +403,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
                 atomicAdd(ec + rc1, to_fixed(q1 * wgt, S));
                 atomicAdd(ec + rc2, to_fixed(q2 * wgt, S));
               }
-#elif BWD_ROT
-              // lane-rotated channel order: lanes of one instruction that share
-              // a cell hit three different words (banks) instead of one address
-              // (ATOMS serializes same-address lanes)
-              atomicAdd(e + rc0, to_fixed(q0 * w00, S)); atomicAdd(e + rc1, to_fixed(q1 * w00, S));
-              atomicAdd(e + rc2, to_fixed(q2 * w00, S));
-              atomicAdd(e10 + rc0, to_fixed(q0 * w10, S)); atomicAdd(e10 + rc1, to_fixed(q1 * w10, S));
-              atomicAdd(e10 + rc2, to_fixed(q2 * w10, S));
-              atomicAdd(e + 3 + rc0, to_fixed(q0 * w01, S)); atomicAdd(e + 3 + rc1, to_fixed(q1 * w01, S));
-              atomicAdd(e + 3 + rc2, to_fixed(q2 * w01, S));
-              atomicAdd(e10 + 3 + rc0, to_fixed(q0 * w11, S)); atomicAdd(e10 + 3 + rc1, to_fixed(q1 * w11, S));
-              atomicAdd(e10 + 3 + rc2, to_fixed(q2 * w11, S));
-#else
-              atomicAdd(e, to_fixed(g0 * w00, S)); atomicAdd(e + 1, to_fixed(g1 * w00, S));
-              atomicAdd(e + 2, to_fixed(g2 * w00, S));
-              atomicAdd(e10, to_fixed(g0 * w10, S)); atomicAdd(e10 + 1, to_fixed(g1 * w10, S));
-              atomicAdd(e10 + 2, to_fixed(g2 * w10, S));
-              atomicAdd(e + 3, to_fixed(g0 * w01, S)); atomicAdd(e + 4, to_fixed(g1 * w01, S));
-              atomicAdd(e + 5, to_fixed(g2 * w01, S));
-              atomicAdd(e10 + 3, to_fixed(g0 * w11, S)); atomicAdd(e10 + 4, to_fixed(g1 * w11, S));
-              atomicAdd(e10 + 5, to_fixed(g2 * w11, S));
-#endif
             }
           }
           // ---- grids: xc + yc runs per channel (key = guide cell; x-cell checked) ----
@@ -573,10 +481,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         }
       }
       px_since_flush += p.w;
-      if ((y - y_first) % rb != rb - 1 && y < y_last) continue;  // barrier once per rb rows
       if (y < y_last) produce_rows(y + 1);  // the other half of the ring
       __syncthreads();
-      if (px_since_flush + rb * p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
+      if (px_since_flush + p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
         for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
           const int v = Ei[i];
           if (v != 0) {
@@ -682,10 +589,6 @@ __global__ void absmax_kernel(const float* __restrict__ gy, long long per_img, f
   if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(gmax + b), __float_as_int(m));
 }
 
-cudaError_t fwd_texture(const float* tables, int batch, const TableLayout& L, cudaStream_t st,
-                        cudaTextureObject_t* tex, int* tex_base);
-cudaError_t fwd_texture_used(cudaTextureObject_t tex, cudaStream_t st);
-
 cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w, int y0,
                              int h_total, const float* lp, const float* lw, int dt,
                              const float* gp, const float* gw, int k, int ds, float* gx,
@@ -696,9 +599,8 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
-  const size_t staged = (size_t)L.staged_bytes() - (BWD_TEX_RB ? (size_t)L.xc_off * 4
-                                                     : BWD_TEX_RG ? (size_t)(L.lut_off + L.pair_floats) * 4 : 0);
-  const size_t smem = staged + 2 * kBwdRb * (size_t)nent * 16 + (size_t)A.total * 4;
+  const size_t staged = (size_t)3 * L.plane_floats * 4 + (size_t)L.grid_floats() * 4;
+  const size_t smem = staged + 2 * (size_t)nent * 16 + (size_t)A.total * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
   float* tables = (float*)wp;
@@ -744,7 +646,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   p.rcp_h = 1.0 / (double)(h_total - 1);
   p.E = E;
   p.gmax = gmax;
-  if ((e = fwd_texture(tables, batch, L, st, &p.tex, &p.tex_base)) != cudaSuccess) return e;
+  if ((e = table_texture(tables, (size_t)batch * L.bytes(), st, &p.tex, &p.tex_base)) != cudaSuccess) return e;
   const long long rows = (long long)batch * h;
   if (rows > 0 && w > 0) {
     int dev = 0, sms = 148;
@@ -763,7 +665,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
       return e;
     kern<<<(int)grid, kBwdWarps * 32, smem, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if ((e = fwd_texture_used(p.tex, st)) != cudaSuccess) return e;
+    if ((e = table_texture_used(p.tex, st)) != cudaSuccess) return e;
   }
   dim3 fg(9 + 3 * k, batch);
   finalize_kernel<<<fg, 256, 0, st>>>(lp, lw, gp, gw, k, A, E, dlp, dlw, dlb, dgp, dgw, dgb);

@@ -160,10 +160,9 @@ int svdlut_pack_tables_factors(const float* u, const float* s, const float* vt, 
 
 static int fused_fwd_packed_impl(const float* rgb, int batch, int h, int w, int y0, int h_total,
                                  const void* tables, int d_t, int d_s, float* out, void* ws,
-                                 size_t ws_bytes, int* nonfinite, int variant, cudaStream_t st) {
+                                 size_t ws_bytes, int* nonfinite, cudaStream_t st) {
   (void)ws;
   (void)ws_bytes;
-  (void)variant;
   int rc;
   if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
   if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
@@ -183,16 +182,15 @@ int svdlut_fused_fwd_packed(const float* rgb, int batch, int h, int w, int y0, i
                             const void* tables, int d_t, int d_s, float* out, void* workspace,
                             size_t workspace_bytes, void* stream) {
   return fused_fwd_packed_impl(rgb, batch, h, w, y0, h_total, tables, d_t, d_s, out, workspace,
-                               workspace_bytes, nullptr, -1, (cudaStream_t)stream);
+                               workspace_bytes, nullptr, (cudaStream_t)stream);
 }
 
-// Extended entry used by the Python layer: optional non-finite flag and
-// `variant` is reserved (ignored; kept for ABI stability).
+// Extended entry used by the Python layer: optional device non-finite flag.
 int svdlut_fused_fwd_packed_ex(const float* rgb, int batch, int h, int w, int y0, int h_total,
                                const void* tables, int d_t, int d_s, float* out, void* workspace,
-                               size_t workspace_bytes, int* nonfinite, int variant, void* stream) {
+                               size_t workspace_bytes, int* nonfinite, void* stream) {
   return fused_fwd_packed_impl(rgb, batch, h, w, y0, h_total, tables, d_t, d_s, out, workspace,
-                               workspace_bytes, nonfinite, variant, (cudaStream_t)stream);
+                               workspace_bytes, nonfinite, (cudaStream_t)stream);
 }
 
 int svdlut_fused_fwd_io(const void* in, int in_fmt, int batch, int h, int w, int y0, int h_total,
@@ -236,7 +234,7 @@ int svdlut_fused_fwd(const float* rgb, int batch, int h, int w, int y0, int h_to
     return rc;
   (void)tb;
   return fused_fwd_packed_impl(rgb, batch, h, w, y0, h_total, workspace, d_t, d_s, out, nullptr, 0,
-                               nullptr, -1, (cudaStream_t)stream);
+                               nullptr, (cudaStream_t)stream);
 }
 
 int svdlut_fused_fwd_exact(const float* rgb, int batch, int h, int w, int y0, int h_total,

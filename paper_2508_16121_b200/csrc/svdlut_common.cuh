@@ -23,58 +23,63 @@ constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 
 // ---- packed per-image table layout (floats; every block 16 B aligned) ------
 //
-//   lut01 [pair rg|rb][i d_t-1][j cst][12]  LUT coefficient cells, 3 channels
-//         packed {A0 A1 B0 B1 | C0 C1 D0 D1 | A2 B2 C2 D2} (cell_index):
-//         channels 0/1 as float2 pairs for the packed FP32x2 pipe,
-//         v_c(a,b) = A_c + B_c*da + C_c*db + D_c*da*db   (weights lw folded in)
-//   xc    [c 3][jx d_s-1][jc d_s-1][4]   merged xc grid of output channel c,
-//         {A,B,C,D} over (ex, ec)        (sum over k%3==c of gw[k,1]*G[k,1])
-//   gxy   [a d_s][b d_s][3]              merged xy grid vertices, channels packed
-//   gyc   [c 3][a d_s][b d_s]            merged yc grid vertices + the channel's
-//                                        total bias lb[c] + sum gb[k]
-//   lut2  [i d_t-1][j cst][12]           pair gb, same cell format
+// LUT pairs rg, rb, gb (pair p = 0, 1, 2; first cell axis = first named
+// channel) as coefficient cells v_c(a, b) = A_c + B_c a + C_c b + D_c a b with
+// the mixing weights lw folded in, stored as nine float4 PLANES [p][k]
+// (structure of arrays), plane k of pair p holding chunk k of every cell:
+//     k = 0  {A0 A1 B0 B1}     channels 0/1 as float2 pairs for FFMA2
+//     k = 1  {C0 C1 D0 D1}
+//     k = 2  {A2 C2 B2 D2}     so {A2 + B2 a, C2 + D2 a} is one FFMA2
+// Each plane is (dt-1) cell rows x cst cell columns, cst >= dt-1 (cst % 8 ==
+// 3): cell (i, j) at index i*cst + j.  With cst % 8 == 3 the 3x3 cell
+// neighbourhood a run of pixels touches maps to distinct 16-byte bank groups
+// except the two opposite diagonals.
 //
-// The fused kernel stages everything before lut2 in shared memory (one TMA
-// bulk copy of a contiguous prefix) and gathers lut2 through the texture
-// path, which runs beside the shared-memory pipe.
-// gxy / gyc are vertex planes: the fused kernel interpolates them along y once
-// per row (per warp) into per-(row, x-cell) coefficient slots.
-// The LUT cell row stride cst is the smallest value >= d_t-1 with
-// cst % 8 == 3: a 16-byte chunk of cell n sits in bank group (3n + k) % 8, so
-// the 3x3 cell neighbourhood a noisy pixel run touches maps to distinct bank
-// groups (offsets {0, +-1, +-cst, +-cst+-1} mod 8 collide only for the two
-// opposite diagonals).
-// Position of coefficient k (0 A, 1 B, 2 C, 3 D) of output channel c in a cell.
-__host__ __device__ constexpr int cell_index(int c, int k) { return c < 2 ? 2 * k + c : 8 + k; }
+// Grid block (K grids merged per output channel c: grid k feeds output and
+// guide channel k%3, transform.py:269-297):
+//   xc   [c 3][jx ds-1][jc ds-1] float4 {A,B,C,D} over (ex, ec) (sum over
+//        k%3==c of gw[k,1]*G[k,1])
+//   gxy  [a ds][b ds][3]   merged xy vertices, channels packed
+//   gyc  [c 3][a ds][b ds] merged yc vertices + the channel's total bias
+//        lb[c] + sum gb[k]
+// The fused kernel interpolates xy / yc along y once per row into merged
+// per-(row, jx, c, jc) slots {M, M', N, N'} (term M + N ex + (M' + N' ex) ec).
+__host__ __device__ constexpr int cst_for(int dt) { return (dt - 1) + ((3 - (dt - 1)) & 7); }
 
 struct TableLayout {
   int dt, ds, cst;
-  int pair_floats;                               // one LUT pair
-  int lut_off, xc_off, gxy_off, gyc_off, lut2_off;  // in floats
-  int total_floats;                              // rounded up to 32 floats (128 B)
+  int plane_floats;                  // one LUT float4 plane: (dt-1) * cst * 4
+  int lut_off;                       // 9 planes [pair][chunk]
+  int xc_off, gxy_off, gyc_off;      // grid block
+  int total_floats;                  // rounded up to 32 floats (128 B)
   __host__ __device__ static TableLayout make(int dt, int ds) {
     TableLayout L;
     L.dt = dt;
     L.ds = ds;
-    L.cst = (dt - 1) + ((3 - (dt - 1)) & 7);
-    L.pair_floats = (dt - 1) * L.cst * 12;
+    L.cst = cst_for(dt);
+    L.plane_floats = (dt - 1) * L.cst * 4;
     L.lut_off = 0;
-    L.xc_off = L.lut_off + 2 * L.pair_floats;
+    L.xc_off = L.lut_off + 9 * L.plane_floats;
     L.gxy_off = L.xc_off + 3 * (ds - 1) * (ds - 1) * 4;
     L.gyc_off = L.gxy_off + ((ds * ds * 3 + 3) & ~3);
-    L.lut2_off = (L.gyc_off + 3 * ds * ds + 31) & ~31;
-    L.total_floats = (L.lut2_off + L.pair_floats + 31) & ~31;
+    L.total_floats = (L.gyc_off + 3 * ds * ds + 31) & ~31;
     return L;
   }
-  __host__ __device__ int pair_off(int p) const { return p < 2 ? lut_off + p * pair_floats : lut2_off; }
+  __host__ __device__ int plane_off(int p, int k) const { return lut_off + (3 * p + k) * plane_floats; }
   __host__ __device__ size_t bytes() const { return (size_t)total_floats * 4; }
-  // bytes of the shared-memory prefix (everything but lut2)
-  __host__ __device__ int staged_bytes() const { return lut2_off * 4; }
-  // one per-warp grid slot of the fused kernel: for a (row y, x-cell jx) the
-  // merged xy + xc + yc grid term of channel c over guide cell jc is
-  //   M + N*ex + (M' + N'*ex)*ec   stored as float4 [c 3][jc d_s-1]
-  __host__ __device__ int slot_bytes() const { return 3 * (ds - 1) * 16; }
+  __host__ __device__ int grid_floats() const { return total_floats - xc_off; }
+  // merged grid slots of one row: [jx ds-1][c 3][jc ds] float4, the last jc
+  // being the padding slot for a guide value of exactly 1.0
+  __host__ __device__ int slot_entries() const { return (ds - 1) * 3 * ds; }
 };
+
+// Position of coefficient q (0 A, 1 B, 2 C, 3 D) of output channel c within
+// the 12 floats {chunk0, chunk1, chunk2} of a cell: slot / 4 = plane (chunk),
+// slot % 4 = float in the float4.
+__host__ __device__ constexpr int coef_slot(int c, int q) {
+  return c < 2 ? (q == 0 ? c : q == 1 ? 2 + c : q == 2 ? 4 + c : 6 + c)
+               : (q == 0 ? 8 : q == 1 ? 10 : q == 2 ? 9 : 11);
+}
 
 // Spatial bracket entry (per column / per row): cell index and f32 delta.
 struct SpatialBr {
@@ -129,6 +134,10 @@ __device__ __forceinline__ uint32_t col_bracket(int x, double rcp, float sdm1, f
 __device__ __forceinline__ uint32_t row_bracket(int y, double rcp, float sdm1, float sdm2,
                                                 float& e) {
   return col_bracket(y, rcp, sdm1, sdm2, e);
+}
+// t = RN32(RN32(x / (W-1)) * (d_s-1)) of a column (uncapped), as col_bracket.
+__device__ __forceinline__ float col_t_value(int x, double rcp, float sdm1) {
+  return __fmul_rn(__double2float_rn(__dmul_rn((double)x, rcp)), sdm1);
 }
 
 }  // namespace svdlut

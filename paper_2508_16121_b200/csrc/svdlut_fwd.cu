@@ -3,34 +3,26 @@
 // Replaces transform._fused_impl (reference transform.py:215-300).
 //
 // Design:
-//   * One persistent CTA per SM (15 warps); LUT pairs rg, rb and the grid
-//     block of one image (≈180 KB at d_t=33 / d_s=17) live in shared memory,
-//     staged by TMA bulk copies (`cp.async.bulk`, mbarrier completion); pair
-//     gb is gathered through the texture path, which runs beside the
-//     shared-memory pipe.  A CTA owns a contiguous range of rows over
-//     (image, row) and re-stages only when the range crosses an image.
-//   * Warps take 128-pixel chunks of a row (lane = 4 consecutive pixels,
-//     128-bit streaming loads/stores).  One thread per CTA bulk-prefetches
-//     the input rows two rows ahead into L2 (`cp.async.bulk.prefetch.L2`), so
-//     the chunk loads issued at the top of each chunk hit L2 and no registers
-//     are spent on a register-level prefetch (measured: 73 -> 67.6 µs).
-//   * Per pixel, all nine shared-memory gathers (rg, rb cells: 3 × LDS.128
-//     each; one merged grid slot per channel) are issued back to back, the
-//     three texture gathers of pair gb one pixel ahead.  LUT cells hold
-//     channel-packed coefficients with the weights folded in:
-//     v = A + B·a + C·b + D·a·b (channels 0/1 on the FP32x2 pipe).
+//   * One persistent CTA per SM.  The LUT chunk planes named by kSmemPlanes
+//     and the grid block of one image are staged into shared memory by TMA
+//     bulk copies (`cp.async.bulk`, mbarrier completion); the remaining LUT
+//     chunk planes are gathered through the texture path, a second pipe beside
+//     the shared-memory (LSU) pipe: an LDS.128 delivers 128 B of lane data
+//     per clock, a TLD.128 64 B (tools/microbench/{ldsclean,texphase}.cu), so
+//     the split balances the two.
+//   * A CTA owns a contiguous range of 128-pixel chunks over (image, row,
+//     chunk) — balanced to one chunk — and its warps take the range's chunks
+//     round robin (lane = 4 consecutive pixels, 128-bit streaming loads and
+//     stores).  One thread bulk-prefetches input rows two rows ahead into L2.
+//   * Brackets are evaluated for two pixels at a time on the FP32x2 pipe
+//     (__fmul2_rz / __fadd2_rz / __ffma2_rn); the merged grid slots carry a
+//     padding guide cell so a guide of exactly 1.0 needs no min().
 //   * Grid terms: per row, the CTA interpolates xy + xc + yc along y into
 //     merged slots {M, M', N, N'} per (x-cell, channel, guide cell) in a ring
-//     of three row buffers (mbarrier handshakes, warps may drift by a row).
-//   * Integer work stays on 32-bit shared addresses; the colour floor is an
-//     add of 2^23 (svdlut_common.cuh), so the index bits feed IMADs directly.
-//   * Streaming I/O: 24 B/pixel of HBM traffic (3 f32 in, 3 f32 out).  The
-//     kernel is bound by the shared-memory pipe (~87% of active cycles, 1.6
-//     wavefronts per pixel), not by HBM — DESIGN.md §3 has the budget.
+//     of kRing row buffers (mbarrier handshakes, warps may drift kRing-2 rows).
+//   * Streaming I/O: 24 B/pixel of HBM traffic (3 f32 in, 3 f32 out).
 #include <atomic>
 #include <cstdint>
-#include <mutex>
-#include <vector>
 
 #include "svdlut_common.cuh"
 #include "svdlut_io.cuh"
@@ -38,33 +30,34 @@
 
 namespace svdlut {
 
-// Kernel shape (pixels per lane PX, warps per CTA NW) is a template choice;
-// the default below is what launch_fused_fwd uses (FWD_PX / FWD_NW override
-// it at build time for experiments).
-#ifndef FWD_PX
-#define FWD_PX 4
-#endif
 #ifndef FWD_NW
-#define FWD_NW 15  // 15 x 128 px = 1920: divides 1080p / 4K / 8K rows exactly
+#define FWD_NW 16
 #endif
-#ifndef FWD_L2PF
-#define FWD_L2PF 2  // rows of L2 prefetch distance for the input planes (0: off)
+#ifndef FWD_PLANES
+// LUT chunk planes staged in shared memory (bit 3*pair + chunk; pairs rg, rb,
+// gb); the others go through the texture path
+#define FWD_PLANES 0x3F
 #endif
-#ifndef FWD_REGPF
-#define FWD_REGPF 0  // next chunk's pixels prefetched into registers under this chunk's math
-#endif
-#ifndef FWD_CHUNKSPLIT
-#define FWD_CHUNKSPLIT 0  // 1: CTA ranges in 128-px chunks (balanced ends, but ~4% slower per CTA); 0: whole rows
-#endif
-constexpr int kPx = FWD_PX;
 constexpr int kFwdWarps = FWD_NW;
-constexpr int kChunk = 32 * kPx;
-#ifndef FWD_RING
-#define FWD_RING 4  // per-row grid slot buffers (warps may drift FWD_RING - 2 rows apart); 3: -2%, 5: +1% smooth but -1% noise
+constexpr int kPx = 4;                 // consecutive pixels per lane
+constexpr int kChunk = 32 * kPx;       // pixels per warp chunk
+constexpr int kRing = 3;               // per-row grid slot buffers (4: the smem carve-out steps up)
+constexpr int kAhead = kRing - 1;      // rows of slots produced ahead of the one consumed
+#ifndef FWD_L2ROWS
+#define FWD_L2ROWS 2
 #endif
-constexpr int kRing = FWD_RING;
-constexpr int kAhead = kRing - 1;  // rows of slots produced ahead of the one being consumed
+constexpr int kL2Rows = FWD_L2ROWS;    // rows of L2 prefetch distance for the input
+constexpr uint32_t kSmemPlanes = FWD_PLANES;
 constexpr uint32_t kMagicBits = 0x4B000000u;  // bits of 2^23
+constexpr float kMagic = 8388608.0f;
+
+__host__ __device__ constexpr int popcount9(uint32_t m) {
+  return (int)((m & 1u) + ((m >> 1) & 1u) + ((m >> 2) & 1u) + ((m >> 3) & 1u) + ((m >> 4) & 1u) +
+               ((m >> 5) & 1u) + ((m >> 6) & 1u) + ((m >> 7) & 1u) + ((m >> 8) & 1u));
+}
+__host__ __device__ constexpr bool plane_in_smem(int idx) { return (kSmemPlanes >> idx) & 1u; }
+__host__ __device__ constexpr int smem_plane_slot(int idx) { return popcount9(kSmemPlanes & ((1u << idx) - 1u)); }
+constexpr int kSmemPlaneCount = popcount9(kSmemPlanes);
 
 struct FwdParams {
   const void* in;           // input samples (format IN of the kernel)
@@ -74,7 +67,7 @@ struct FwdParams {
   int y0;                   // first row of this strip in an image of h_total rows
   const float* tables;
   TableLayout L;
-  cudaTextureObject_t tex;  // float4 texels over the packed tables (pair gb reads)
+  cudaTextureObject_t tex;  // float4 texels over the packed tables
   int tex_base;             // texel index of image 0's table start
   double rcp_w;             // RN64(1 / (W - 1)) for the exact column brackets
   double rcp_h;             // RN64(1 / (h_total - 1)) for the row brackets
@@ -86,7 +79,6 @@ struct FwdParams {
   double* loss;
   float* gmax;
   float gscale;
-  int col_smem;             // 1: column brackets come from a per-CTA smem table of t values
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -96,14 +88,11 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          dst),
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
@@ -121,63 +110,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-#ifndef FWD_GRID_SMEM
-// 1: the grid block (xc, gxy, gyc; ~19 KB) is staged in shared memory with
-// the LUT pairs; 0: the once-per-row slot production reads it from global
-// memory through L1, which lowers the smem carve-out to 164 KB and leaves
-// ~92 KB of L1 for the texture-path LUT pair
-#define FWD_GRID_SMEM 1  // 0 measured slower (73.9 vs 70.1 us smooth, 153 vs 149 uniform)
-#endif
-#ifndef FWD_ILV
-// 1 (f32 in/out): a lane's four pixels are x0 + lane + 32u (u = 0..3) instead
-// of four consecutive ones, so the eight lanes of an LDS.128 phase hold eight
-// neighbouring pixels (fewer distinct LUT cells per phase, fewer bank
-// conflicts); loads / stores become coalesced 32-bit accesses.  Measured 4K:
-// smooth 66.8 -> 73.2 us (32 B of spills), uniform noise 140.4 -> 128.9 us
-#define FWD_ILV 0
-#endif
-#ifndef FWD_COLTAB_MAXW
-// column brackets from a per-CTA shared-memory table for rows narrower than
-// this, computed inline per pixel (one f64 multiply) for wider rows: the
-// table's LDS costs shared-pipe wavefronts, the inline path ALU work; measured
-// 4K smooth 67.6 -> 66.9 us inline, 8 x 1080p 155.1 -> 156.4 us inline
-#define FWD_COLTAB_MAXW 2560
-#endif
-#ifndef FWD_BREUSE
-// 1: the colour brackets of pair gb's axes (g, b), computed one pixel ahead
-// for the texture gathers, are reused for pairs rg / rb instead of being
-// recomputed (same cbracket, same values)
-#define FWD_BREUSE 1
-#endif
-#ifndef FWD_TGT_LATE
-// L2-loss epilogue: 1 loads the target chunk right before the epilogue (its
-// 12 registers are not live across the pixel math, but the load latency is
-// exposed: 8 x 1080p 214 vs 203 us, more spills); 0 loads it with the input
-// chunk
-#define FWD_TGT_LATE 0
-#endif
-#ifndef FWD_TEXDEP
-#define FWD_TEXDEP 1  // next pixel's TLD index depends on this pixel's last LDS (see below)
-#endif
-#ifndef FWD_LDS_PLAIN
-#define FWD_LDS_PLAIN 1
-#endif
 __device__ __forceinline__ float4 lds4(uint32_t a) {
-#if FWD_LDS_PLAIN
-  // an ordinary shared load (the scheduler may move it; still ordered
-  // against the mbarrier waits, which clobber memory)
   return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(a));
-#else
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(a));
-  return v;
-#endif
 }
-// Texture gather as volatile PTX: keeps the one-pixel-ahead issue order of the
-// source (the compiler otherwise hoists all of a chunk's TLDs to its top and
-// runs out of registers for the shared-memory gathers).
+// Texture gather as volatile PTX: keeps the one-pixel-ahead issue order (the
+// compiler otherwise hoists a chunk's texture gathers to its top and runs
+// out of registers for the shared-memory gathers).
 __device__ __forceinline__ float4 texv4(cudaTextureObject_t t, int i) {
   float4 v;
   asm volatile("tex.1d.v4.f32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
@@ -186,94 +124,65 @@ __device__ __forceinline__ float4 texv4(cudaTextureObject_t t, int i) {
   return v;
 }
 
-// Colour bracket returning the 2^23-biased index bits (see svdlut_common.cuh).
-__device__ __forceinline__ uint32_t cbracket(float q, float dm1, float dm2, float& delta) {
-  const float t = fminf(__fmul_rz(q, dm1), dm2);
-  const float m = __fadd_rz(t, 8388608.0f);
-  delta = __fmaf_rn(q, dm1, -(m - 8388608.0f));
-  return __float_as_uint(m);
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// Colour / guide brackets of two pixels (interp.py:35-45, exact floor; see
+// svdlut_common.cuh): biased index bits m (2^23 + i as float) and delta.
+// CAP: i = min(floor(t), d-2); without it a value of exactly 1.0 lands on
+// index d-1 (the padding guide slot stands for (d-2, delta 1)).
+template <bool CAP>
+__device__ __forceinline__ void bracket2(float2 q, float dm1, float2& m, float2& delta) {
+  float2 t = __fmul2_rz(q, f2(dm1));
+  if (CAP) t = f2(fminf(t.x, dm1 - 1.0f), fminf(t.y, dm1 - 1.0f));
+  m = __fadd2_rz(t, f2(kMagic));
+  const float2 nf = __ffma2_rn(m, f2(-1.0f), f2(kMagic));  // -floor(t), exact
+  delta = __ffma2_rn(q, f2(dm1), nf);
 }
 
-// One LUT pair's contribution A + B a + (C + D a) b for the three channels;
-// cell = {A0 A1 B0 B1 | C0 C1 D0 D1 | A2 B2 C2 D2} (cell_index in
-// svdlut_common.cuh): channels 0/1 on the FP32x2 pipe.
-template <bool FIRST>
-__device__ __forceinline__ void cell_term(const float4& c0, const float4& c1, const float4& c2,
-                                          float da, float db, float2& acc01, float& acc2) {
-  const float2 a2 = make_float2(da, da);
-  const float2 t = __ffma2_rn(make_float2(c0.z, c0.w), a2, make_float2(c0.x, c0.y));
-  const float2 s = __ffma2_rn(make_float2(c1.z, c1.w), a2, make_float2(c1.x, c1.y));
-  const float v2 = __fmaf_rn(db, __fmaf_rn(c2.w, da, c2.z), __fmaf_rn(c2.y, da, c2.x));
-  if (FIRST) {
-    acc01 = __ffma2_rn(s, make_float2(db, db), t);
-    acc2 = v2;
-  } else {
-    acc01 = __ffma2_rn(s, make_float2(db, db), __fadd2_rn(t, acc01));
-    acc2 += v2;
+// Merged grid coefficients of channel c at (row bracket jy/ey, x-cell jx, guide cell jc):
+//   {M, M', N, N'} with term = M + N*ex + (M' + N'*ex)*ec  (biases included);
+// jc == ds-1 is the padding slot: cell ds-2 at ec = 1.  `gb` is the image's
+// grid block (shared-memory copy).
+__device__ __forceinline__ float4 grid_slot(const float* gb, const TableLayout& L, int ds, int c,
+                                            int jx, int jc, int jy, float ey) {
+  const int jcc = min(jc, ds - 2);
+  const float4 x = reinterpret_cast<const float4*>(gb)[(c * (ds - 1) + jx) * (ds - 1) + jcc];
+  const float* Y = gb + (L.gyc_off - L.xc_off) + c * ds * ds;
+  const float y00 = Y[jy * ds + jcc], y01 = Y[jy * ds + jcc + 1];
+  const float y10 = Y[(jy + 1) * ds + jcc], y11 = Y[(jy + 1) * ds + jcc + 1];
+  const float q0 = __fmaf_rn(ey, y10 - y00, y00), q1 = __fmaf_rn(ey, y11 - y01, y01);
+  const float* X = gb + (L.gxy_off - L.xc_off);
+  const float v00 = X[(jx * ds + jy) * 3 + c], v01 = X[(jx * ds + jy + 1) * 3 + c];
+  const float v10 = X[((jx + 1) * ds + jy) * 3 + c], v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
+  const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
+  float4 s = make_float4(x.x + q0 + r0, x.z + (q1 - q0), x.y + (r1 - r0), x.w);
+  if (jc != jcc) {  // at ec = 1: {M + M', M', N + N', N'}
+    s.x += s.y;
+    s.z += s.w;
   }
-}
-
-// Merged grid slot {M, M', N, N'}: M + N ex + (M' + N' ex) ec.
-__device__ __forceinline__ float slot_term(const float4& g, float ex, float ec) {
-  const float2 pq = __ffma2_rn(make_float2(g.z, g.w), make_float2(ex, ex), make_float2(g.x, g.y));
-  return __fmaf_rn(ec, pq.y, pq.x);
+  return s;
 }
 
 template <int PX>
 struct ChunkIn {
-  float r[PX], g[PX], b[PX];  // PX consecutive pixels per lane
+  float r[PX], g[PX], b[PX];
 };
 
-// Grid part of one image's tables (shared memory copy; slot builds / wide path).
-struct GridG {
-  const float4* xc;   // [c][jx][jc] {A,B,C,D}
-  const float* gxy;   // [a][b][3]
-  const float* gyc;   // [c][a][b]
-};
-
-// Merged grid coefficients of channel c at (row bracket jy/ey, x-cell jx, guide cell jc):
-//   {M, M', N, N'} with term = M + N*ex + (M' + N'*ex)*ec  (biases included)
-__device__ __forceinline__ float4 grid_entry(const GridG& G, int ds, int c, int jx, int jc, int jy,
-                                             float ey) {
-  const float4 x = G.xc[(c * (ds - 1) + jx) * (ds - 1) + jc];
-  const float* Y = G.gyc + c * ds * ds;
-  const float y00 = Y[jy * ds + jc], y01 = Y[jy * ds + jc + 1];
-  const float y10 = Y[(jy + 1) * ds + jc], y11 = Y[(jy + 1) * ds + jc + 1];
-  const float q0 = __fmaf_rn(ey, y10 - y00, y00), q1 = __fmaf_rn(ey, y11 - y01, y01);
-  const float* X = G.gxy;
-  const float v00 = X[(jx * ds + jy) * 3 + c], v01 = X[(jx * ds + jy + 1) * 3 + c];
-  const float v10 = X[((jx + 1) * ds + jy) * 3 + c];
-  const float v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
-  const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
-  return make_float4(x.x + q0 + r0, x.z + (q1 - q0), x.y + (r1 - r0), x.w);
+// Shared-memory bytes of the staged tables (LUT chunk planes + grid block).
+__host__ __device__ inline uint32_t staged_bytes(const TableLayout& L) {
+  return (uint32_t)kSmemPlaneCount * (uint32_t)L.plane_floats * 4u + (uint32_t)L.grid_floats() * 4u;
 }
 
-#ifndef FWD_TEX_RB
-// 1: pair rb also through the texture path (not staged).  Measured 4K:
-// smooth 66.8 -> 73.0 us, uniform noise 140 -> 314 us (the texture pipe and
-// its L1 become the bound)
-#define FWD_TEX_RB 0
-#endif
-// Shared-memory image of the tables: LUT pairs rg, rb then the grid block
-// (xc, gxy, gyc); pair gb is read through the texture path.
-__host__ __device__ inline uint32_t smem_grid_off(const TableLayout& L) {
-  return (FWD_TEX_RB ? 1u : 2u) * (uint32_t)L.pair_floats * 4u;
-}
-__host__ __device__ inline uint32_t smem_tables_bytes(const TableLayout& L) {
-  return smem_grid_off(L) + (FWD_GRID_SMEM ? (uint32_t)(L.lut2_off - L.xc_off) * 4u : 0u);
-}
-
-template <int DT, int DS, bool CHECK, int PX, int NW, int IN, int OUT>
-__global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
-  static_assert(PX == 4 || (IN == kF32 && (OUT == kF32 || OUT == kL2Grad)),
-                "integer formats use 4-pixel lanes");
+template <int DT, int DS, bool CHECK, int IN, int OUT>
+__global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams p) {
+  constexpr int NW = kFwdWarps;
   constexpr bool LOSS = OUT == kL2Grad;
   constexpr int OUTF = LOSS ? (int)kF32 : OUT;  // storage format of the output
   float loss_acc = 0.f, gmax_acc = 0.f;         // LOSS: this thread's partials
-  constexpr int CH = 32 * PX;  // pixels per warp chunk
-  constexpr bool ILV = FWD_ILV && PX == 4 && IN == kF32 && (OUT == kF32 || OUT == kL2Grad);
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar_storage;
+  __shared__ __align__(8) uint64_t ring_bar[2 * kRing];
   const int dt = DT ? DT : p.L.dt;
   const int ds = DS ? DS : p.L.ds;
   const TableLayout L = TableLayout::make(dt, ds);
@@ -282,70 +191,38 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
 
-  // slot ring: full[i] completes when every warp wrote its share of the row in
-  // buffer i, empty[i] when every warp finished reading it
-  __shared__ __align__(8) uint64_t ring_bar[2 * kRing];
+  // slot ring: full[i] completes when every warp wrote its share of the row
+  // in buffer i, empty[i] when every warp finished reading it
   const uint32_t full0 = smem_addr(&ring_bar[0]), empty0 = smem_addr(&ring_bar[kRing]);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     for (int i = 0; i < 2 * kRing; ++i) mbar_init(smem_addr(&ring_bar[i]), NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t lut_smem_bytes = smem_grid_off(L);
-  const uint32_t table_bytes = smem_tables_bytes(L);
-  const int nent = (ds - 1) * 3 * (ds - 1);                  // slot entries per row
-  float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
-  // column table: t(x) = RN32(RN32(x/(W-1)) * (d_s-1)) for every column, built once
-  float* col_t = reinterpret_cast<float*>(slots + kRing * nent);
-  const uint32_t col_addr = smem_addr(col_t);
-  if (p.col_smem) {
-    const int wpad = (p.w + 3) & ~3;
-    for (int x = threadIdx.x; x < wpad; x += blockDim.x) {
-      const int xc = min(x, p.w - 1);
-      col_t[x] = __fmul_rn(__double2float_rn(__dmul_rn((double)xc, p.rcp_w)), (float)(ds - 1));
-    }
-  }
-
+  const uint32_t plane_bytes = (uint32_t)L.plane_floats * 4u;
+  const uint32_t tables_bytes = staged_bytes(L);
+  const int nent = L.slot_entries();
+  float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + tables_bytes);
+  const float tdm1 = (float)(dt - 1);
+  const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
   // inputs and tables may come from the previous kernel in the stream (PDL)
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  GridG G;
-  auto set_grid = [&](const float* gsm) {  // gsm + table offset = grid block
-    G.xc = reinterpret_cast<const float4*>(gsm + L.xc_off);
-    G.gxy = gsm + L.gxy_off;
-    G.gyc = gsm + L.gyc_off;
-  };
-  if (FWD_GRID_SMEM) set_grid(smem + lut_smem_bytes / 4 - L.xc_off);  // global offset -> smem
-
-  const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
-  const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
-  const uint32_t cst48 = (uint32_t)L.cst * 48u;
-  const uint32_t pair_bytes = (uint32_t)(dt - 1) * cst48;
-  const uint32_t cst3 = (uint32_t)L.cst * 3u;
-  // address = base + bits_a*cst48 + bits_b*48 with the 2^23 bias folded in
-  const uint32_t lutK = sbase + (uint32_t)L.lut_off * 4u - kMagicBits * (cst48 + 48u);
-  const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;  // one channel of a slot row
-  const uint32_t jx_bytes = 3u * chan_bytes;             // one x-cell of a slot row
+  const uint32_t cst = (uint32_t)L.cst;
+  const uint32_t cst16 = cst * 16u;
+  // smem address of cell (bits_a, bits_b) of a staged plane of pair p:
+  //   lutK + bits_a*cst16 + bits_b*16 + (plane slot)*plane_bytes
+  const uint32_t lutK = sbase - kMagicBits * (cst16 + 16u);
+  const uint32_t chan_bytes = (uint32_t)ds * 16u;      // one channel of a slot row
+  const uint32_t jx_bytes = 3u * chan_bytes;          // one x-cell of a slot row
   const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
-  const uint32_t slotK0 = smem_addr(slots) - kMagicBits * 16u;
+  const uint32_t slotK0 = smem_addr(slots) - kMagicBits * (jx_bytes + 16u);
 
-  // contiguous range of global chunks g = (image b, row y) * cpr + k for this
-  // CTA: rows r_begin .. r_end-1, the first and last possibly partial (whole
-  // rows unless FWD_CHUNKSPLIT)
-  const int cpr = (p.w + CH - 1) / CH;
-#if FWD_CHUNKSPLIT
+  // contiguous range of global chunks g = ((image b) * h + row y) * cpr + k
+  const int cpr = (p.w + kChunk - 1) / kChunk;
   const long long chunks_total = (long long)p.batch * p.h * cpr;
   const long long g_begin = (long long)blockIdx.x * chunks_total / gridDim.x;
   const long long g_end = (long long)(blockIdx.x + 1) * chunks_total / gridDim.x;
-#else
-  const long long rows_total = (long long)p.batch * p.h;
-  const long long g_begin = (long long)blockIdx.x * rows_total / gridDim.x * cpr;
-  const long long g_end = (long long)(blockIdx.x + 1) * rows_total / gridDim.x * cpr;
-#endif
-  const long long r_begin = g_begin / cpr;
-  const long long r_end = (g_end + cpr - 1) / cpr;
-  const int k_first = (int)(g_begin - r_begin * cpr);
-  const int k_last = (int)(g_end - (r_end - 1) * cpr);  // exclusive, in the last row
   const long long pl = p.pl_in, opl = p.pl_out;  // plane strides (floats)
   const long long plane_len = (long long)p.h * p.w;
   const bool vec_in = ((p.w & 3) == 0) && Src<IN>::aligned(p.in, pl);
@@ -355,114 +232,72 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   uint32_t nrow = 0;  // CTA row ordinal (slot ring position)
   bool bad = false;
 
-  long long r = r_begin;
-  while (r < r_end) {
-    const int b = (int)(r / p.h);
-    const int y_first = (int)(r - (long long)b * p.h);
-    const int y_last = (int)(min(r_end, (long long)(b + 1) * p.h) - 1 - (long long)b * p.h);
+  long long g_seg = g_begin;
+  while (g_seg < g_end) {
+    const long long r_seg = g_seg / cpr;              // global row of the segment's first chunk
+    const int b = (int)(r_seg / p.h);
+    const long long g_img_end = min(g_end, (long long)(b + 1) * p.h * cpr);
+    const int y_first = (int)(r_seg - (long long)b * p.h);
+    const int y_last = (int)((g_img_end - 1) / cpr - (long long)b * p.h);
     const float* tb = p.tables + (long long)b * L.total_floats;
-    if (!FWD_GRID_SMEM) set_grid(tb);
-    // ---- stage image b's tables into shared memory (TMA bulk copy) ----
+    // the image's grid block (shared-memory copy, read by the slot production)
+    const float* gsm = reinterpret_cast<const float*>(reinterpret_cast<const char*>(smem) +
+                                                      kSmemPlaneCount * plane_bytes);
+    // ---- stage image b's tables into shared memory (TMA bulk copies) ----
     __syncthreads();  // every warp is done reading the previous image's tables
     if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(bar, table_bytes);
-      const char* src = reinterpret_cast<const char*>(tb);
-      for (uint32_t off = 0; off < lut_smem_bytes; off += 32768u)  // LUT pairs kept in smem
-        bulk_g2s(sbase + off, src + off, min(32768u, lut_smem_bytes - off), bar);
-      const char* gsrc = src + (size_t)L.xc_off * 4;
-      const uint32_t gbytes = table_bytes - lut_smem_bytes;
-      for (uint32_t off = 0; off < gbytes; off += 32768u)       // grid block
-        bulk_g2s(sbase + lut_smem_bytes + off, gsrc + off, min(32768u, gbytes - off), bar);
+      mbar_arrive_expect_tx(bar, tables_bytes);
+#pragma unroll
+      for (int idx = 0; idx < 9; ++idx)
+        if (plane_in_smem(idx)) {
+          const char* src = reinterpret_cast<const char*>(tb + L.plane_off(idx / 3, idx % 3));
+          for (uint32_t off = 0; off < plane_bytes; off += 32768u)
+            bulk_g2s(sbase + smem_plane_slot(idx) * plane_bytes + off, src + off, min(32768u, plane_bytes - off),
+                     bar);
+        }
+      const char* gsrc = reinterpret_cast<const char*>(tb + L.xc_off);
+      const uint32_t gbytes = (uint32_t)L.grid_floats() * 4u;
+      for (uint32_t off = 0; off < gbytes; off += 32768u)
+        bulk_g2s(sbase + kSmemPlaneCount * plane_bytes + off, gsrc + off, min(32768u, gbytes - off), bar);
+
     }
     const void* src = Src<IN>::image(p.in, b, pl);
     void* dst = Dst<OUTF>::image(p.out, b, opl);
     const void* tsrc = LOSS ? Src<kF32>::image(p.target, b, pl) : nullptr;
-    // texel index of pair rb's cell (ir, ib) (FWD_TEX_RB) = texKrb + bits_r*cst3 + bits_b*3
-    [[maybe_unused]] const uint32_t texKrb = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
-                                             (uint32_t)((L.lut_off + L.pair_floats) / 4) - kMagicBits * (cst3 + 3u);
-    // texel index of pair gb's cell (ig, ib) = texK + bits_g*cst3 + bits_b*3
-    const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
-                          (uint32_t)(L.lut2_off / 4) - kMagicBits * (cst3 + 3u);
+    // texel of cell (bits_a, bits_b) of plane idx: texK + bits_a*cst + bits_b + plane_off/4
+    const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) -
+                          kMagicBits * (cst + 1u);
+    const uint32_t ptex = (uint32_t)L.plane_floats / 4u;  // texels per plane
 
-    // chunk range [klo, khi) of row y of this segment; the warp takes
-    // klo + warp, klo + warp + NW, ...
-    // in 32-bit: the only rows with a partial chunk range are the CTA's first
-    // (row yf of this segment, or none: -1) and last (yl, or beyond y_last)
-    const long long rb0 = (long long)b * p.h;
-    const int yf = r_begin - rb0 < 0 ? -1 : (int)(r_begin - rb0);
-    const int yl = (int)min(r_end - 1 - rb0, (long long)p.h);
-    auto klo = [&](int y) { return y == yf ? k_first : 0; };
-    auto khi = [&](int y) { return y == yl ? k_last : cpr; };
-    // move (y, k) forward to this warp's next chunk (y > y_last: none left)
-    auto settle = [&](int& y, int& k) {
-      while (y <= y_last && k >= khi(y)) {
-        ++y;
-        k = y <= y_last ? klo(y) + warp : 0;
-      }
-    };
-    // the first chunk's loads overlap the table copy
-    // chunk k of row y: the input, and the f32 target of the loss epilogue
-    auto load_ilv = [&](const void* img, int y, int k, ChunkIn<PX>& c) {
-      const float* pp = static_cast<const float*>(img) + (long long)y * p.w;
-#pragma unroll
-      for (int u = 0; u < PX; ++u) {
-        const int xx = min(k * CH + lane + 32 * u, p.w - 1);
-        c.r[u] = io_ld_f(pp + xx);
-        c.g[u] = io_ld_f(pp + pl + xx);
-        c.b[u] = io_ld_f(pp + 2 * pl + xx);
-      }
-    };
-    auto load_chunk = [&](const void* img, int y, int k, bool vec, ChunkIn<PX>& c) {
-      if constexpr (ILV) load_ilv(img, y, k, c);
-      else Src<IN>::template load<PX>(img, pl, y, k * CH + PX * lane, p.w, vec, c.r, c.g, c.b);
-    };
-    auto load_target = [&](const void* img, int y, int k, bool vec, ChunkIn<PX>& c) {
-      if constexpr (ILV) load_ilv(img, y, k, c);
-      else Src<kF32>::template load<PX>(img, pl, y, k * CH + PX * lane, p.w, vec, c.r, c.g, c.b);
-    };
-    ChunkIn<PX> cur, tgt;
-    int cur_y = y_first, cur_k = klo(y_first) + warp;
-    settle(cur_y, cur_k);
-    if (cur_y <= y_last) {
-      load_chunk(src, cur_y, cur_k, vec_in, cur);
-      if (LOSS && !FWD_TGT_LATE)
-        load_target(tsrc, cur_y, cur_k, vec_out, tgt);
+    // this warp's chunks: global chunk g_seg + warp + NW*i (< g_img_end), as
+    // (row cy, chunk ck) advanced in 32-bit
+    int cy, ck;
+    {
+      const long long g0 = g_seg + warp;
+      cy = (int)(g0 / cpr - (long long)b * p.h);
+      ck = (int)(g0 % cpr);
     }
+    const int k_end = (int)((g_img_end - 1) % cpr) + 1;  // chunks of row y_last in the segment
+    auto in_seg = [&](int y, int k) { return y < y_last || (y == y_last && k < k_end); };
+    ChunkIn<kPx> cur, tgt;
+    auto load = [&](int y, int k) {
+      Src<IN>::template load<kPx>(src, pl, y, k * kChunk + kPx * lane, p.w, vec_in, cur.r, cur.g, cur.b);
+      if (LOSS) Src<kF32>::template load<kPx>(tsrc, pl, y, k * kChunk + kPx * lane, p.w, vec_out, tgt.r, tgt.g, tgt.b);
+    };
+    if (in_seg(cy, ck)) load(cy, ck);  // the first chunk's loads overlap the table copy
     mbar_wait(bar, phase);
     phase ^= 1u;
-#ifdef FWD_DBG_TIMES
-    if (CHECK && threadIdx.x == 0 && r == r_begin) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      reinterpret_cast<unsigned long long*>(p.nonfinite + 2)[2 * blockIdx.x] = t;
-    }
-#endif
-    // This warp's share of the slots of row y (CTA row ordinal n) into ring
-    // buffer n % kRing.  Row n+kAhead is produced once row n is done, so warps
-    // may drift apart instead of meeting at a CTA barrier every row.
-    // x-cell of column x (the per-pixel rule: floor(min(t, d_s - 2)))
-    auto jx_of = [&](int x) -> int {
-      if (p.col_smem) return (int)floorf(fminf(col_t[x], sdm2));
-      float e;
-      return (int)(col_bracket(x, p.rcp_w, sdm1, sdm2, e) - kMagicBits);
-    };
+
+    // this warp's share of the slots of row y (CTA row ordinal n) into ring buffer n % kRing
     auto produce = [&](uint32_t n, int y) {
       float ey;
       const int jy = (int)(row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey) - kMagicBits);
       float4* S = slots + (n % kRing) * nent;
-      // only the x-cells this CTA's chunks of row y touch (all of them for a
-      // full row; a partial first / last row of a chunk range needs fewer)
-      int e_lo = 0, e_hi = nent;  // a full row touches every x-cell
-      if (y == yf || y == yl) {
-        const int x_lo = klo(y) * CH, x_hi = min(khi(y) * CH, p.w) - 1;
-        e_lo = x_hi >= x_lo ? jx_of(x_lo) * 3 * (ds - 1) : 0;
-        e_hi = x_hi >= x_lo ? (jx_of(x_hi) + 1) * 3 * (ds - 1) : 0;
-      }
-      for (int e = e_lo + warp * 32 + lane; e < e_hi; e += NW * 32) {
-        const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
-        const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
-        S[e] = grid_entry(G, ds, ch, jx, jc, jy, ey);
+      for (int e = warp * 32 + lane; e < nent; e += NW * 32) {
+        const int jx = e / (3 * ds), rem = e - jx * 3 * ds;
+        const int ch = rem / ds, jc = rem - ch * ds;
+        S[e] = grid_slot(gsm, L, ds, ch, jx, jc, jy, ey);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(full0 + 8u * (n % kRing));
@@ -473,143 +308,132 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
 
     for (int y = y_first; y <= y_last; ++y) {
       const uint32_t n = n0 + (uint32_t)(y - y_first);
-      if (FWD_L2PF > 0 && threadIdx.x == blockDim.x - 32) {
-        if (y == y_first)
-          for (int yy = y + 1; yy < y + FWD_L2PF && yy <= y_last; ++yy) {
-            Src<IN>::prefetch_row(src, pl, plane_len, yy, p.w);
-            if (LOSS) Src<kF32>::prefetch_row(tsrc, pl, plane_len, yy, p.w);
-          }
-        if (y + FWD_L2PF <= y_last) {
-          Src<IN>::prefetch_row(src, pl, plane_len, y + FWD_L2PF, p.w);
-          if (LOSS) Src<kF32>::prefetch_row(tsrc, pl, plane_len, y + FWD_L2PF, p.w);
+      if (threadIdx.x == blockDim.x - 32) {  // L2 prefetch of the input rows ahead
+        for (int yy = (y == y_first ? y + 1 : y + kL2Rows); yy <= y + kL2Rows && yy <= y_last; ++yy) {
+          Src<IN>::prefetch_row(src, pl, plane_len, yy, p.w);
+          if (LOSS) Src<kF32>::prefetch_row(tsrc, pl, plane_len, yy, p.w);
         }
       }
       mbar_wait(full0 + 8u * (n % kRing), (n / kRing) & 1u);
       const uint32_t slotK = slotK0 + (n % kRing) * slot_row_bytes;
-      // ---- this warp's chunks of row y: k = warp, warp + W, ... ----
-      for (; cur_y == y;) {
-        ChunkIn<PX> nxt;
-        int nxt_y = cur_y, nxt_k = cur_k + NW;
-        settle(nxt_y, nxt_k);
-#if FWD_REGPF
-        if (nxt_y <= y_last)
-          load_chunk(src, nxt_y, nxt_k, vec_in, nxt);
-#endif
-
-        const int xl = cur_k * CH + PX * lane;
-        // x of this lane's pixel u
-        auto xof = [&](int u) { return ILV ? cur_k * CH + lane + 32 * u : xl + u; };
-        int jxs[PX];
-        float exs[PX];
-        if (p.col_smem) {
-          float ts[PX];
-          if (ILV) {
-#pragma unroll
-            for (int u = 0; u < PX; ++u) ts[u] = col_t[min(xof(u), p.w - 1)];
-          } else if (PX == 4) {
-            // lanes past the row end read the last (in-bounds) group; their
-            // pixels are never stored
-            const int xt = min(xl, ((p.w + 3) & ~3) - 4);
-            const float4 t4 = lds4(col_addr + (uint32_t)xt * 4u);
-            ts[0] = t4.x; ts[PX > 1 ? 1 : 0] = t4.y; ts[PX > 2 ? 2 : 0] = t4.z; ts[PX > 3 ? 3 : 0] = t4.w;
-          } else {
-#pragma unroll
-            for (int u = 0; u < PX; ++u) ts[u] = col_t[min(xl + u, p.w - 1)];
-          }
-#pragma unroll
-          for (int u = 0; u < PX; ++u) {
-            const float m = __fadd_rz(fminf(ts[u], sdm2), 8388608.0f);
-            exs[u] = ts[u] - (m - 8388608.0f);
-            jxs[u] = (int)(__float_as_uint(m) - kMagicBits);
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < PX; ++u)
-            jxs[u] = (int)(col_bracket(min(xof(u), p.w - 1), p.rcp_w, sdm1, sdm2, exs[u]) - kMagicBits);
+      // ---- this warp's chunks of row y ----
+      while (cy == y && in_seg(cy, ck)) {
+        const int xl = ck * kChunk + kPx * lane;
+        int ny = cy, nk = ck + NW;  // this warp's next chunk
+        while (nk >= cpr) {
+          nk -= cpr;
+          ++ny;
         }
+        const bool has_next = in_seg(ny, nk);
 
-        // Pair gb is gathered through the texture path one pixel ahead of its
-        // use (software pipeline depth 1), hiding the texture latency behind
-        // the shared-memory work of the previous pixel.
-        float o0[PX], o1[PX], o2[PX];
-        float4 tx0, tx1, tx2;  // in-flight texture cells of the next pixel
-        float tdg, tdb;        // its deltas
-        uint32_t nbg, nbb;     // and its colour brackets (g, b)
-        {
-          nbg = cbracket(__saturatef(cur.g[0]), tdm1, tdm2, tdg);
-          nbb = cbracket(__saturatef(cur.b[0]), tdm1, tdm2, tdb);
-          const int ti = (int)(nbg * cst3 + nbb * 3u + texK);
-          tx0 = texv4(p.tex, ti);
-          tx1 = texv4(p.tex, ti + 1);
-          tx2 = texv4(p.tex, ti + 2);
-        }
+        // column brackets (x-cell bits, ex) of the lane's 4 pixels: exact t(x)
+        // (lanes past the row end use the last column; never stored)
+        const float2 tx01 = f2(col_t_value(min(xl, p.w - 1), p.rcp_w, sdm1),
+                               col_t_value(min(xl + 1, p.w - 1), p.rcp_w, sdm1));
+        const float2 tx23 = f2(col_t_value(min(xl + 2, p.w - 1), p.rcp_w, sdm1),
+                               col_t_value(min(xl + 3, p.w - 1), p.rcp_w, sdm1));
+        // brackets of pixel pair h2 (two pixels at a time on the FP32x2 pipe):
+        // x-cell bits / ex, colour bits / deltas vs d_t (mc*, d*) and guide
+        // bits / deltas vs d_s (ms*, e*).  Pair 1's colour brackets are computed
+        // while pixel 1 runs (its texture gathers are issued there).
+        float2 mx[2], ex[2], mcr[2], mcg[2], mcb[2], dr[2], dg[2], db[2];
+        float2 msr[2], msg[2], msb[2], er[2], eg[2], eb[2];
+        auto q2 = [&](const float* v, int h2) { return f2(__saturatef(v[2 * h2]), __saturatef(v[2 * h2 + 1])); };
+        auto colour_brackets = [&](int h2) {
+          bracket2<true>(q2(cur.r, h2), tdm1, mcr[h2], dr[h2]);
+          bracket2<true>(q2(cur.g, h2), tdm1, mcg[h2], dg[h2]);
+          bracket2<true>(q2(cur.b, h2), tdm1, mcb[h2], db[h2]);
+        };
+        auto grid_brackets = [&](int h2) {
+          const float2 t = h2 ? tx23 : tx01;
+          mx[h2] = __fadd2_rz(f2(fminf(t.x, sdm2), fminf(t.y, sdm2)), f2(kMagic));
+          ex[h2] = __fadd2_rn(t, __ffma2_rn(mx[h2], f2(-1.0f), f2(kMagic)));  // t - floor(min(t, ds-2)): exact
+          bracket2<false>(q2(cur.r, h2), sdm1, msr[h2], er[h2]);
+          bracket2<false>(q2(cur.g, h2), sdm1, msg[h2], eg[h2]);
+          bracket2<false>(q2(cur.b, h2), sdm1, msb[h2], eb[h2]);
+        };
+        colour_brackets(0);
+        auto lo = [](const float2& v, int u) { return (u & 1) ? v.y : v.x; };
+        auto bits = [](const float2& v, int u) { return __float_as_uint((u & 1) ? v.y : v.x); };
+
+        // texture-path planes of pixel u: issued one pixel ahead
+        float4 tq[9];
+        auto tex_issue = [&](int u, float4 (&tq_)[9], uint32_t dep) {
+          const uint32_t br = bits(mcr[u >> 1], u), bg = bits(mcg[u >> 1], u), bb = bits(mcb[u >> 1], u);
 #pragma unroll
-        for (int u = 0; u < PX; ++u) {
-          const float4 c0 = tx0, c1 = tx1, c2 = tx2;
-          const float dg = tdg, db = tdb;
-          const float qr = __saturatef(cur.r[u]), qg = __saturatef(cur.g[u]),
-                      qb = __saturatef(cur.b[u]);
-          float dr, dg_, db_;
-          const uint32_t br = cbracket(qr, tdm1, tdm2, dr);
-#if FWD_BREUSE
-          const uint32_t bg = nbg, bb = nbb;
-          dg_ = dg;
-          db_ = db;
-#else
-          const uint32_t bg = cbracket(qg, tdm1, tdm2, dg_);
-          const uint32_t bb = cbracket(qb, tdm1, tdm2, db_);
-#endif
-          float er, eg, eb;
-          const uint32_t sr = cbracket(qr, sdm1, sdm2, er);
-          const uint32_t sg = cbracket(qg, sdm1, sdm2, eg);
-          const uint32_t sb = cbracket(qb, sdm1, sdm2, eb);
-          const uint32_t ur = br * cst48 + lutK;
-          const uint32_t ag = ur + bg * 48u, ab = ur + bb * 48u + pair_bytes;
-          const uint32_t sa = slotK + (uint32_t)jxs[u] * jx_bytes;
-          // every shared-memory gather of the pixel back to back (lds4 is
-          // volatile, so program order is issue order): nine LDS.128 in
-          // flight per warp instead of one cell's three at a time
-          const float4 rg0 = lds4(ag), rg1 = lds4(ag + 16), rg2 = lds4(ag + 32);
-#if FWD_TEX_RB
-          const int tr = (int)(br * cst3 + bb * 3u + texKrb);
-          const float4 rb0 = texv4(p.tex, tr), rb1 = texv4(p.tex, tr + 1), rb2 = texv4(p.tex, tr + 2);
-          (void)ab;
-#else
-          const float4 rb0 = lds4(ab), rb1 = lds4(ab + 16), rb2 = lds4(ab + 32);
-#endif
-          const float4 s0 = lds4(sa + sr * 16u);
-          const float4 s1 = lds4(sa + chan_bytes + sg * 16u);
-          const float4 s2 = lds4(sa + 2u * chan_bytes + sb * 16u);
-          if (u + 1 < PX) {
-            // next pixel's texture gathers, issued after this pixel's shared
-            // gathers: the index carries a (never taken) dependency on the
-            // last LDS so ptxas cannot hoist every TLD of the chunk to its top
-            // (which starves the LDS of registers)
-            nbg = cbracket(__saturatef(cur.g[u + 1]), tdm1, tdm2, tdg);
-            nbb = cbracket(__saturatef(cur.b[u + 1]), tdm1, tdm2, tdb);
-            const int ti = (int)(nbg * cst3 + nbb * 3u + texK) + (FWD_TEXDEP && s2.w != s2.w ? 1 : 0);
-            tx0 = texv4(p.tex, ti);
-            tx1 = texv4(p.tex, ti + 1);
-            tx2 = texv4(p.tex, ti + 2);
+          for (int pr = 0; pr < 3; ++pr) {
+            const uint32_t ba = pr == 2 ? bg : br, bbv = pr == 0 ? bg : bb;
+            const uint32_t t0 = ba * cst + bbv + texK + (uint32_t)(L.plane_off(pr, 0) / 4) + dep;
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk)
+              if (!plane_in_smem(3 * pr + kk)) tq_[3 * pr + kk] = texv4(p.tex, (int)(t0 + kk * ptex));
           }
+        };
+        tex_issue(0, tq, 0u);
+        float o0[kPx], o1[kPx], o2[kPx];
+#pragma unroll
+        for (int u = 0; u < kPx; ++u) {
+          if ((u & 1) == 0) grid_brackets(u >> 1);
+          if (u == 2) {
+            colour_brackets(1);
+            tex_issue(2, tq, 0u);
+          }
+          const uint32_t br = bits(mcr[u >> 1], u), bg = bits(mcg[u >> 1], u), bb = bits(mcb[u >> 1], u);
+          const float a_r = lo(dr[u >> 1], u), a_g = lo(dg[u >> 1], u), a_b = lo(db[u >> 1], u);
+          // shared-memory planes
+          float4 c[9];
+          const uint32_t ur = br * cst16 + lutK, ug = bg * cst16 + lutK;
+          const uint32_t cell_a[3] = {ur + bg * 16u, ur + bb * 16u, ug + bb * 16u};
+#pragma unroll
+          for (int idx = 0; idx < 9; ++idx)
+            if (plane_in_smem(idx)) c[idx] = lds4(cell_a[idx / 3] + (uint32_t)smem_plane_slot(idx) * plane_bytes);
+          const uint32_t sa = slotK + bits(mx[u >> 1], u) * jx_bytes;
+          const float4 s0 = lds4(sa + bits(msr[u >> 1], u) * 16u);
+          const float4 s1 = lds4(sa + chan_bytes + bits(msg[u >> 1], u) * 16u);
+          const float4 s2 = lds4(sa + 2u * chan_bytes + bits(msb[u >> 1], u) * 16u);
+#pragma unroll
+          for (int idx = 0; idx < 9; ++idx)
+            if (!plane_in_smem(idx)) c[idx] = tq[idx];
+          if (u + 1 < kPx && u != 1) {
+            // next pixel's texture gathers, after this pixel's shared gathers;
+            // the (never taken) dependency on the last LDS stops ptxas from
+            // hoisting all of the chunk's TLDs to its top
+            tex_issue(u + 1, tq, s2.w != s2.w ? 1u : 0u);
+          }
+          // LUT pairs: v = A + B a + (C + D a) b, channels 0/1 on FP32x2
           float2 acc01;
           float acc2;
-          cell_term<true>(rg0, rg1, rg2, dr, dg_, acc01, acc2);    // pair rg (shared memory)
-          cell_term<false>(rb0, rb1, rb2, dr, db_, acc01, acc2);   // pair rb (shared memory)
-          cell_term<false>(c0, c1, c2, dg, db, acc01, acc2);       // pair gb (texture path)
-          // grids: one merged (xy + xc + yc) coefficient cell per channel
-          const float ex = exs[u];
-          o0[u] = acc01.x + slot_term(s0, ex, er);
-          o1[u] = acc01.y + slot_term(s1, ex, eg);
-          o2[u] = acc2 + slot_term(s2, ex, eb);
+#pragma unroll
+          for (int pr = 0; pr < 3; ++pr) {
+            const float da = pr == 2 ? a_g : a_r, dbv = pr == 0 ? a_g : a_b;
+            const float4 k0 = c[3 * pr], k1 = c[3 * pr + 1], k2 = c[3 * pr + 2];
+            const float2 s01 = __ffma2_rn(f2(k1.z, k1.w), f2(da), f2(k1.x, k1.y));  // C + D a
+            const float2 ts2 = __ffma2_rn(f2(k2.z, k2.w), f2(da), f2(k2.x, k2.y));  // {A2 + B2 a, C2 + D2 a}
+            if (pr == 0) {
+              acc01 = __ffma2_rn(s01, f2(dbv), __ffma2_rn(f2(k0.z, k0.w), f2(da), f2(k0.x, k0.y)));
+              acc2 = __fmaf_rn(ts2.y, dbv, ts2.x);
+            } else {
+              acc01 = __ffma2_rn(f2(k0.z, k0.w), f2(da), __fadd2_rn(acc01, f2(k0.x, k0.y)));
+              acc01 = __ffma2_rn(s01, f2(dbv), acc01);
+              acc2 = __fmaf_rn(ts2.y, dbv, acc2 + ts2.x);
+            }
+          }
+          // grids: one merged (xy + xc + yc) slot per channel {M, M', N, N'}
+          const float e_x = lo(ex[u >> 1], u);
+          const float2 p0 = __ffma2_rn(f2(s0.z, s0.w), f2(e_x), f2(s0.x, s0.y));
+          const float2 p1 = __ffma2_rn(f2(s1.z, s1.w), f2(e_x), f2(s1.x, s1.y));
+          const float2 p2 = __ffma2_rn(f2(s2.z, s2.w), f2(e_x), f2(s2.x, s2.y));
+          const float2 o01 = __fadd2_rn(acc01, f2(__fmaf_rn(p0.y, lo(er[u >> 1], u), p0.x),
+                                                  __fmaf_rn(p1.y, lo(eg[u >> 1], u), p1.x)));
+          o0[u] = o01.x;
+          o1[u] = o01.y;
+          o2[u] = acc2 + __fmaf_rn(p2.y, lo(eb[u >> 1], u), p2.x);
           if (CHECK) bad |= !(isfinite(o0[u]) && isfinite(o1[u]) && isfinite(o2[u]));
         }
         if (LOSS) {  // gY = (Y - T) * 2/N, loss partial, max |gY| (pixels past the row end excluded)
-          if (FWD_TGT_LATE)
-            Src<kF32>::template load<PX>(tsrc, pl, cur_y, xl, p.w, vec_out, tgt.r, tgt.g, tgt.b);
 #pragma unroll
-          for (int u = 0; u < PX; ++u) {
-            const bool in_row = xof(u) < p.w;
+          for (int u = 0; u < kPx; ++u) {
+            const bool in_row = xl + u < p.w;
             const float r0 = o0[u] - tgt.r[u], r1 = o1[u] - tgt.g[u], r2 = o2[u] - tgt.b[u];
             o0[u] = r0 * p.gscale;
             o1[u] = r1 * p.gscale;
@@ -620,29 +444,10 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
             }
           }
         }
-        if constexpr (ILV) {
-          float* pp = static_cast<float*>(dst) + (long long)cur_y * p.w;
-#pragma unroll
-          for (int u = 0; u < PX; ++u)
-            if (xof(u) < p.w) {
-              __stcs(pp + xof(u), o0[u]);
-              __stcs(pp + opl + xof(u), o1[u]);
-              __stcs(pp + 2 * opl + xof(u), o2[u]);
-            }
-        } else {
-          Dst<OUTF>::template store<PX>(dst, opl, cur_y, xl, p.w, vec_out, o0, o1, o2);
-        }
-#if FWD_REGPF
-        cur = nxt;
-#else
-        if (nxt_y <= y_last) {
-          load_chunk(src, nxt_y, nxt_k, vec_in, cur);
-          if (LOSS && !FWD_TGT_LATE)
-            load_target(tsrc, nxt_y, nxt_k, vec_out, tgt);
-        }
-#endif
-        cur_y = nxt_y;
-        cur_k = nxt_k;
+        Dst<OUTF>::template store<kPx>(dst, opl, y, xl, p.w, vec_out, o0, o1, o2);
+        if (has_next) load(ny, nk);
+        cy = ny;
+        ck = nk;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8u * (n % kRing));
@@ -654,7 +459,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
       }
     }
     nrow = n0 + (uint32_t)cnt;
-    r += y_last - y_first + 1;
+    g_seg = g_img_end;
     if (LOSS) {  // this image's partials: warp reduction, one atomic per warp
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
@@ -672,177 +477,61 @@ __global__ void __launch_bounds__(NW * 32, 1) fused_fwd_kernel(FwdParams p) {
   if (CHECK) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.nonfinite, 1);
   }
-#ifdef FWD_DBG_TIMES
-  __syncthreads();
-  if (CHECK && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    reinterpret_cast<unsigned long long*>(p.nonfinite + 2)[2 * blockIdx.x + 1] = t;
-  }
-#endif
 }
 
+// dynamic shared memory of the kernel: staged planes + the slot ring
 size_t fwd_smem_bytes(int dt, int ds) {
   const TableLayout L = TableLayout::make(dt, ds);
-  // staged tables + double-buffered per-row grid slots [jx][c][jc] (float4)
-  return (size_t)smem_tables_bytes(L) + kRing * (size_t)(ds - 1) * 3 * (ds - 1) * 16;
+  return (size_t)staged_bytes(L) + kRing * (size_t)L.slot_entries() * 16;
 }
-
-// Keep at least this much of the 256 KB L1/shared array as L1 so the
-// texture-path LUT pair stays resident; the column table is added only if it
-// fits under the limit.
-constexpr size_t kSmemForL1Tex = 196 * 1024 - 2048;
 
 int fwd_max_smem_bytes() { return kMaxSmemBytes - kSmemReserve; }
 
+// Shared-memory carve-out granularity of the 256 KB L1/shared array (KB)
+// and the L1 the texture-path planes want to stay resident in.
+static int carveout_kb(size_t smem) {
+  static const int kOpts[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
+  for (int o : kOpts)
+    if ((size_t)o * 1024 >= smem + 1024) return o;
+  return 228;
+}
+
 static int g_num_sms = 0;
 
-// ---- texture objects over packed-table buffers --------------------------------
-// One linear float4 texture per (device, buffer, size), cached; evicted
-// objects are destroyed only after an event recorded behind their last use
-// has completed, so kernels still in flight never lose their texture.
-namespace {
-struct TexEntry {
-  int dev;
-  const void* base;
-  size_t bytes;
-  cudaTextureObject_t tex;
-  cudaEvent_t last_use;
-  unsigned long long stamp;
-  bool pinned;  // referenced by a captured CUDA graph: never retired
-};
-struct TexRetired {
-  cudaTextureObject_t tex;
-  cudaEvent_t ev;
-};
-std::mutex g_tex_mu;
-std::vector<TexEntry> g_tex;
-std::vector<TexRetired> g_tex_retired;
-unsigned long long g_tex_clock = 0;
-constexpr size_t kTexCache = 32;
-
-void reap_retired() {
-  for (size_t i = 0; i < g_tex_retired.size();) {
-    if (cudaEventQuery(g_tex_retired[i].ev) == cudaSuccess) {
-      cudaDestroyTextureObject(g_tex_retired[i].tex);
-      cudaEventDestroy(g_tex_retired[i].ev);
-      g_tex_retired[i] = g_tex_retired.back();
-      g_tex_retired.pop_back();
-    } else {
-      cudaGetLastError();  // clear cudaErrorNotReady
-      ++i;
-    }
-  }
-}
-
-bool capturing(cudaStream_t st) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return cs != cudaStreamCaptureStatusNone;
-}
-
-// Texture over [base, base + bytes); base must be textureAlignment-aligned.
-// During stream capture no events are queried or recorded and the entry is
-// pinned, since the graph keeps using the texture object on every replay.
-cudaError_t tex_for(int dev, const void* base, size_t bytes, cudaStream_t st, cudaTextureObject_t* out) {
-  std::lock_guard<std::mutex> lock(g_tex_mu);
-  const bool cap = capturing(st);
-  if (!cap) reap_retired();
-  TexEntry* hit = nullptr;
-  for (auto& e : g_tex)
-    if (e.dev == dev && e.base == base && e.bytes == bytes) hit = &e;
-  if (!hit) {
-    if (g_tex.size() >= kTexCache) {  // retire the least recently used unpinned entry
-      long lru = -1;
-      for (size_t i = 0; i < g_tex.size(); ++i)
-        if (!g_tex[i].pinned && (lru < 0 || g_tex[i].stamp < g_tex[lru].stamp)) lru = (long)i;
-      if (lru >= 0) {
-        g_tex_retired.push_back({g_tex[lru].tex, g_tex[lru].last_use});
-        g_tex[lru] = g_tex.back();
-        g_tex.pop_back();
-      }
-    }
-    cudaResourceDesc rd = {};
-    rd.resType = cudaResourceTypeLinear;
-    rd.res.linear.devPtr = const_cast<void*>(base);
-    rd.res.linear.desc = cudaCreateChannelDesc<float4>();
-    rd.res.linear.sizeInBytes = bytes;
-    cudaTextureDesc td = {};
-    td.readMode = cudaReadModeElementType;
-    TexEntry e{dev, base, bytes, 0, nullptr, 0, false};
-    cudaError_t err = cudaCreateTextureObject(&e.tex, &rd, &td, nullptr);
-    if (err != cudaSuccess) return err;
-    err = cudaEventCreateWithFlags(&e.last_use, cudaEventDisableTiming);
-    if (err != cudaSuccess) return err;
-    g_tex.push_back(e);
-    hit = &g_tex.back();
-  }
-  hit->stamp = ++g_tex_clock;
-  hit->pinned |= cap;
-  *out = hit->tex;
-  return cudaSuccess;
-}
-
-// Marks the texture's last use after the launch just issued on `st`.
-cudaError_t tex_mark_used(cudaTextureObject_t tex, cudaStream_t st) {
-  if (capturing(st)) return cudaSuccess;
-  std::lock_guard<std::mutex> lock(g_tex_mu);
-  for (auto& t : g_tex)
-    if (t.tex == tex) return cudaEventRecord(t.last_use, st);
-  return cudaSuccess;
-}
-}  // namespace
-
-// Texture object over a batch of packed tables (also used by the backward).
-cudaError_t fwd_texture(const float* tables, int batch, const TableLayout& L, cudaStream_t st,
-                        cudaTextureObject_t* tex, int* tex_base) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int talign = 512;
-  cudaDeviceGetAttribute(&talign, cudaDevAttrTextureAlignment, dev);
-  const uintptr_t tb = reinterpret_cast<uintptr_t>(tables);
-  const uintptr_t base = tb / (uintptr_t)talign * (uintptr_t)talign;
-  const size_t bytes = (size_t)(tb - base) + (size_t)batch * L.bytes();
-  *tex_base = (int)((tb - base) / 16);
-  return tex_for(dev, reinterpret_cast<const void*>(base), bytes, st, tex);
-}
-
-cudaError_t fwd_texture_used(cudaTextureObject_t tex, cudaStream_t st) { return tex_mark_used(tex, st); }
-
 template <int DT, int DS, int IN, int OUT>
-static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t smem,
-                               cudaStream_t st) {
-  auto kern = check ? fused_fwd_kernel<DT, DS, true, kPx, kFwdWarps, IN, OUT>
-                    : fused_fwd_kernel<DT, DS, false, kPx, kFwdWarps, IN, OUT>;
-  // function attributes are set once per (instantiation, device, smem size);
-  // setting them is not a stream operation, so graph capture does not see it
+static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t smem, cudaStream_t st) {
+  auto kern = check ? fused_fwd_kernel<DT, DS, true, IN, OUT> : fused_fwd_kernel<DT, DS, false, IN, OUT>;
+  // Function attributes are set once per (instantiation, device): the largest
+  // dynamic shared memory any launch may request (tables + slots + the widest
+  // column table), so concurrent launches / captured graphs never see the
+  // limit lowered under them.  Setting them is not a stream operation.
   constexpr int kMaxDev = 64;
-  static std::atomic<size_t> configured[kMaxDev][2];
+  static std::atomic<int> configured[kMaxDev][2];
   int dev = 0;
   cudaGetDevice(&dev);
-  std::atomic<size_t>* seen = dev < kMaxDev ? &configured[dev][check] : nullptr;
-  cudaError_t e = cudaSuccess;
-  if (!seen || seen->load(std::memory_order_relaxed) != smem) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (dev >= kMaxDev || configured[dev][check].load(std::memory_order_acquire) == 0) {
+    const int maxsm = fwd_max_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
     if (e != cudaSuccess) return e;
-    // smallest shared-memory carve-out that fits: the rest of the 256 KB stays
-    // L1 for the texture-path LUT pair
-    const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
-    if (e != cudaSuccess) return e;
-    if (seen) seen->store(smem, std::memory_order_relaxed);
+    if (dev < kMaxDev) configured[dev][check].store(1, std::memory_order_release);
   }
-  // Programmatic dependent launch: the kernel's prologue (barriers, column
-  // table) may overlap the tail of the table-packing kernel before it; every
-  // global access comes after griddepcontrol.wait.
+  // smallest carve-out that fits (a hint, not a limit): the rest of the
+  // 256 KB array stays L1 for the texture-path planes
+  static std::atomic<int> carve[kMaxDev][2];
+  const int kb = carveout_kb(smem);
+  if (dev < kMaxDev && carve[dev][check].load(std::memory_order_relaxed) != kb) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (kb * 100 + 227) / 228);
+    if (e != cudaSuccess) return e;
+    carve[dev][check].store(kb, std::memory_order_relaxed);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kFwdWarps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
+  // Programmatic dependent launch: the kernel's prologue (barriers, column
+  // table) may overlap the tail of the table-packing kernel before it; every
+  // global access comes after griddepcontrol.wait.
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -861,36 +550,7 @@ static cudaError_t launch_fmt(const FwdParams& p, const TableLayout& L, bool chk
 }
 
 bool fused_fwd_formats_supported(int in_fmt, int out_fmt) {
-  if (in_fmt < kF32 || in_fmt > kU16 || out_fmt < kF32 || out_fmt > kU16) return false;
-  if (in_fmt == kF32 && out_fmt == kF32) return true;
-  return kPx == 4;
-}
-
-cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,
-                             int h_total, const float* tables, const TableLayout& L,
-                             int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
-  return launch_fused_fwd_io(rgb, kF32, out, kF32, batch, h, w, y0, h_total, tables, L, nonfinite,
-                             st, pl_in, pl_out);
-}
-
-static cudaError_t launch_fwd_impl(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
-                                   int w, int y0, int h_total, const float* tables, const TableLayout& L,
-                                   int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out,
-                                   const float* target, double* loss, float* gmax, float gscale);
-
-cudaError_t launch_fused_fwd_l2(const float* rgb, const float* target, float* gy, int batch, int h, int w,
-                                int y0, int h_total, const float* tables, const TableLayout& L,
-                                double* loss, float* gmax, float gscale, cudaStream_t st) {
-  return launch_fwd_impl(rgb, kF32, gy, kL2Grad, batch, h, w, y0, h_total, tables, L, nullptr, st, 0, 0,
-                         target, loss, gmax, gscale);
-}
-
-cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
-                                int w, int y0, int h_total, const float* tables, const TableLayout& L,
-                                int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
-  if (!fused_fwd_formats_supported(in_fmt, out_fmt)) return cudaErrorInvalidValue;
-  return launch_fwd_impl(in, in_fmt, out, out_fmt, batch, h, w, y0, h_total, tables, L, nonfinite, st,
-                         pl_in, pl_out, nullptr, nullptr, nullptr, 0.f);
+  return in_fmt >= kF32 && in_fmt <= kU16 && out_fmt >= kF32 && out_fmt <= kU16;
 }
 
 static cudaError_t launch_fwd_impl(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
@@ -923,32 +583,20 @@ static cudaError_t launch_fwd_impl(const void* in, int in_fmt, void* out, int ou
   p.gscale = gscale;
   const long long rows = (long long)batch * h;
   if (rows == 0 || w == 0) return cudaSuccess;
-  // texture over the whole batch of tables, base aligned down to textureAlignment
-  int talign = 512;
-  cudaDeviceGetAttribute(&talign, cudaDevAttrTextureAlignment, dev);
-  const uintptr_t tb = reinterpret_cast<uintptr_t>(tables);
-  const uintptr_t base = tb / (uintptr_t)talign * (uintptr_t)talign;
-  const size_t bytes = (size_t)(tb - base) + (size_t)batch * L.bytes();
-  p.tex_base = (int)((tb - base) / 16);
-  cudaError_t e = tex_for(dev, reinterpret_cast<const void*>(base), bytes, st, &p.tex);
+  cudaError_t e = table_texture(tables, (size_t)batch * L.bytes(), st, &p.tex, &p.tex_base);
   if (e != cudaSuccess) return e;
   long long grid = g_num_sms;
   const long long chunks = rows * ((w + kChunk - 1) / kChunk);
   if (grid > chunks) grid = chunks;
-  size_t smem = fwd_smem_bytes(L.dt, L.ds);
-  const size_t col_bytes = (size_t)((w + 3) & ~3) * 4;
-  p.col_smem = w < FWD_COLTAB_MAXW && smem + col_bytes <= kSmemForL1Tex ? 1 : 0;
-  if (p.col_smem) smem += col_bytes;
+  const size_t smem = fwd_smem_bytes(L.dt, L.ds);
   const bool chk = nonfinite != nullptr;
   const int g = (int)grid;
   const int fmt = in_fmt * 3 + out_fmt;
   if (out_fmt == kL2Grad) {
     e = launch_fmt<kF32, kL2Grad>(p, L, chk, g, smem, st);
-  } else if (fmt == kF32 * 3 + kF32) {
-    e = launch_fmt<kF32, kF32>(p, L, chk, g, smem, st);
   } else {
-#if FWD_PX == 4
     switch (fmt) {
+      case kF32 * 3 + kF32: e = launch_fmt<kF32, kF32>(p, L, chk, g, smem, st); break;
       case kU8 * 3 + kU8: e = launch_fmt<kU8, kU8>(p, L, chk, g, smem, st); break;
       case kU16 * 3 + kU16: e = launch_fmt<kU16, kU16>(p, L, chk, g, smem, st); break;
       case kU8 * 3 + kF32: e = launch_fmt<kU8, kF32>(p, L, chk, g, smem, st); break;
@@ -958,12 +606,31 @@ static cudaError_t launch_fwd_impl(const void* in, int in_fmt, void* out, int ou
       case kU8 * 3 + kU16: e = launch_fmt<kU8, kU16>(p, L, chk, g, smem, st); break;
       default: e = launch_fmt<kU16, kU8>(p, L, chk, g, smem, st); break;
     }
-#else
-    e = cudaErrorInvalidValue;
-#endif
   }
   if (e != cudaSuccess) return e;
-  return tex_mark_used(p.tex, st);
+  return table_texture_used(p.tex, st);
+}
+
+cudaError_t launch_fused_fwd(const float* rgb, float* out, int batch, int h, int w, int y0,
+                             int h_total, const float* tables, const TableLayout& L,
+                             int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
+  return launch_fwd_impl(rgb, kF32, out, kF32, batch, h, w, y0, h_total, tables, L, nonfinite, st, pl_in,
+                         pl_out, nullptr, nullptr, nullptr, 0.f);
+}
+
+cudaError_t launch_fused_fwd_l2(const float* rgb, const float* target, float* gy, int batch, int h, int w,
+                                int y0, int h_total, const float* tables, const TableLayout& L,
+                                double* loss, float* gmax, float gscale, cudaStream_t st) {
+  return launch_fwd_impl(rgb, kF32, gy, kL2Grad, batch, h, w, y0, h_total, tables, L, nullptr, st, 0, 0,
+                         target, loss, gmax, gscale);
+}
+
+cudaError_t launch_fused_fwd_io(const void* in, int in_fmt, void* out, int out_fmt, int batch, int h,
+                                int w, int y0, int h_total, const float* tables, const TableLayout& L,
+                                int* nonfinite, cudaStream_t st, long long pl_in, long long pl_out) {
+  if (!fused_fwd_formats_supported(in_fmt, out_fmt)) return cudaErrorInvalidValue;
+  return launch_fwd_impl(in, in_fmt, out, out_fmt, batch, h, w, y0, h_total, tables, L, nonfinite, st,
+                         pl_in, pl_out, nullptr, nullptr, nullptr, 0.f);
 }
 
 }  // namespace svdlut

@@ -69,6 +69,12 @@ cudaError_t launch_reconstruct_bwd(const float* u, const float* s, const float* 
                                    const float* dplanes, int batch, int dt, int ns, float* du,
                                    float* ds, float* dvt, cudaStream_t st);
 
+// texture object over a batch of packed tables (svdlut_tex.cu); *tex_base is
+// the texel index of `tables`; mark the use after each launch on `st`
+cudaError_t table_texture(const float* tables, size_t bytes, cudaStream_t st, cudaTextureObject_t* tex,
+                          int* tex_base);
+cudaError_t table_texture_used(cudaTextureObject_t tex, cudaStream_t st);
+
 int fwd_max_smem_bytes();
 // dynamic shared memory the fast kernel needs for (d_t, d_s): tables + per-warp row tables
 size_t fwd_smem_bytes(int dt, int ds);

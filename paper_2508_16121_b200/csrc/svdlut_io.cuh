@@ -68,6 +68,9 @@ __device__ __forceinline__ void io_st_u8(void* p, uint32_t v) {
   asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "h"((uint16_t)v) : "memory");
 }
 
+__device__ __forceinline__ void io_prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void io_prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -145,6 +148,13 @@ struct Src<kF32> {
       b[u] = io_ld_f(p + 2 * pl + xx);
     }
   }
+  // L1 prefetch of a lane's PX samples per channel (issued a chunk ahead)
+  static __device__ __forceinline__ void prefetch_l1(const void* img, long long pl, int y, int x, int w) {
+    const float* p = static_cast<const float*>(img) + (long long)y * w + min(x, w - 1);
+    io_prefetch_l1(p);
+    io_prefetch_l1(p + pl);
+    io_prefetch_l1(p + 2 * pl);
+  }
   static __device__ __forceinline__ void prefetch_row(const void* img, long long pl, long long plane_len,
                                                       int y, int w) {
 #pragma unroll
@@ -204,6 +214,9 @@ struct SrcHwc {
       g[u] = io_decode<FMT>(v[3 * u + 1]);
       b[u] = io_decode<FMT>(v[3 * u + 2]);
     }
+  }
+  static __device__ __forceinline__ void prefetch_l1(const void* img, long long, int y, int x, int w) {
+    io_prefetch_l1(static_cast<const char*>(img) + ((long long)y * w + min(x, w - 1)) * 3 * kB);
   }
   static __device__ __forceinline__ void prefetch_row(const void* img, long long, long long plane_len,
                                                       int y, int w) {

@@ -61,7 +61,8 @@ constexpr int kPackBand = 4;  // LUT cell rows per pack block
 // skips materialising the planes.
 //   blocks [0, 9*nbands) one band of kPackBand cell rows of LUT plane (c, p):
 //                        the band's vertex rows are reconstructed into shared
-//                        memory, then channel c's 4 floats of each cell written
+//                        memory, then channel c's 4 coefficients of each cell
+//                        written into the chunk planes
 //   remaining blocks     merged grid cells / vertices and padding
 __global__ void pack_kernel(const float* __restrict__ lp, const float* __restrict__ fu,
                             const float* __restrict__ fs, const float* __restrict__ fvt, int ns,
@@ -84,12 +85,13 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
 
   const int nbands = (dt - 1 + kPackBand - 1) / kPackBand;
   if (blockIdx.x < 9 * nbands) {
-    // plane (c, p), cell rows [i0, i1): vertex rows [i0, i1] staged in smem
+    // plane (c, p), cell rows [i0, i1): vertex rows [v0, v1] staged in smem
     const int cpi = blockIdx.x / nbands, band = blockIdx.x - cpi * nbands;
     const int c = cpi / 3, p = cpi - 3 * c;
     const int i0 = band * kPackBand, i1 = min(i0 + kPackBand, dt - 1);
+    const int v0 = i0, v1 = i1;
     const long long cp = b * 9 + c * 3 + p;
-    const int nv = (i1 - i0 + 1) * dt;
+    const int nv = (v1 - v0 + 1) * dt;
     if (!lp && stage_factors) {
       // the band's U rows, S and all of Vt into shared memory first (one
       // round of global latency instead of one per term of every dot product),
@@ -97,8 +99,8 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
       float* Us = Ts + (kPackBand + 1) * dt;
       float* Ss = Us + (kPackBand + 1) * ns;
       float* Vs = Ss + ns;
-      const float* U = fu + cp * dt * ns + (long long)i0 * ns;
-      for (int e = threadIdx.x; e < (i1 - i0 + 1) * ns; e += blockDim.x) Us[e] = U[e];
+      const float* U = fu + cp * dt * ns + (long long)v0 * ns;
+      for (int e = threadIdx.x; e < (v1 - v0 + 1) * ns; e += blockDim.x) Us[e] = U[e];
       for (int e = threadIdx.x; e < ns; e += blockDim.x) Ss[e] = fs[cp * ns + e];
       for (int e = threadIdx.x; e < ns * dt; e += blockDim.x) Vs[e] = fvt[cp * ns * dt + e];
       __syncthreads();
@@ -108,7 +110,7 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
       }
     } else {
       for (int e = threadIdx.x; e < nv; e += blockDim.x) {
-        const int i = i0 + e / dt, j = e - (e / dt) * dt;
+        const int i = v0 + e / dt, j = e - (e / dt) * dt;
         if (lp) {
           Ts[e] = lp[cp * dt * dt + i * dt + j];
         } else {
@@ -118,18 +120,26 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
     }
     __syncthreads();
     const double w = (double)W[c * 3 + p];
-    float* base = T + L.pair_off(p);
+    float* P0 = T + L.plane_off(p, 0);
+    const int sA = coef_slot(c, 0), sB = coef_slot(c, 1), sC = coef_slot(c, 2), sD = coef_slot(c, 3);
     for (int e = threadIdx.x; e < (i1 - i0) * L.cst; e += blockDim.x) {
       const int il = e / L.cst, j = e - il * L.cst;
-      Coef q = {0.f, 0.f, 0.f, 0.f};
-      if (j < dt - 1)
-        q = cell_coef(w * Ts[il * dt + j], w * Ts[(il + 1) * dt + j], w * Ts[il * dt + j + 1],
-                      w * Ts[(il + 1) * dt + j + 1]);
-      float* dst = base + ((i0 + il) * L.cst + j) * 12;
-      dst[cell_index(c, 0)] = q.a;
-      dst[cell_index(c, 1)] = q.b;
-      dst[cell_index(c, 2)] = q.c;
-      dst[cell_index(c, 3)] = q.d;
+      const int i = i0 + il;
+      double q[4] = {0.0, 0.0, 0.0, 0.0};
+      if (j < dt - 1) {
+        const float* R0 = Ts + (i - v0) * dt;
+        const double p00 = w * R0[j], p10 = w * R0[dt + j];
+        const double p01 = w * R0[j + 1], p11 = w * R0[dt + j + 1];
+        q[0] = p00;                            // A
+        q[1] = p10 - p00;                      // B
+        q[2] = p01 - p00;                      // C
+        q[3] = (p11 - p10) - (p01 - p00);      // D
+      }
+      const int cell = i * L.cst + j;
+      P0[(sA >> 2) * L.plane_floats + cell * 4 + (sA & 3)] = (float)q[0];
+      P0[(sB >> 2) * L.plane_floats + cell * 4 + (sB & 3)] = (float)q[1];
+      P0[(sC >> 2) * L.plane_floats + cell * 4 + (sC & 3)] = (float)q[2];
+      P0[(sD >> 2) * L.plane_floats + cell * 4 + (sD & 3)] = (float)q[3];
     }
     return;
   }
@@ -137,9 +147,8 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
   const int n_xc = 3 * (ds - 1) * (ds - 1);
   const int n_gxy = ds * ds;  // vertices (3 floats each)
   const int n_gyc = 3 * ds * ds;
-  const int n_pad = L.lut2_off - (L.gyc_off + n_gyc);
-  const int n_tail = L.total_floats - (L.lut2_off + L.pair_floats);
-  const int total = n_xc + n_gxy + n_gyc + n_pad + n_tail;
+  const int n_tail = L.total_floats - (L.gyc_off + n_gyc);
+  const int total = n_xc + n_gxy + n_gyc + n_tail;
   const int gb0 = 9 * nbands;
   for (int e = (blockIdx.x - gb0) * blockDim.x + threadIdx.x; e < total;
        e += (gridDim.x - gb0) * blockDim.x) {
@@ -187,12 +196,7 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
       continue;
     }
     r -= n_gyc;
-    if (r < n_pad) {
-      T[L.gyc_off + n_gyc + r] = 0.f;  // padding before lut2
-      continue;
-    }
-    r -= n_pad;
-    T[L.lut2_off + L.pair_floats + r] = 0.f;  // tail padding
+    T[L.gyc_off + n_gyc + r] = 0.f;  // tail padding
   }
 }
 

@@ -145,11 +145,11 @@ def _image(rgb, batch):
     return rgb
 
 
-def apply(rgb, tables, out=None, y0=0, h_total=None, variant=-1, nonfinite=None):
+def apply(rgb, tables, out=None, y0=0, h_total=None, nonfinite=None):
     """Fused slice + LUT apply (fast fp32 kernel) from packed tables.
 
     ``nonfinite``: optional int32 CUDA tensor (1 element) OR-ed with 1 if any
-    output is NaN/Inf.  ``variant`` is reserved.  One kernel launch.
+    output is NaN/Inf.  One kernel launch.
     """
     rgb = _image(rgb, tables.batch)
     b, _, h, w = rgb.shape
@@ -159,8 +159,7 @@ def apply(rgb, tables, out=None, y0=0, h_total=None, variant=-1, nonfinite=None)
     elif out.shape != rgb.shape or not out.is_contiguous() or out.dtype != torch.float32:
         raise DimensionMismatch("out must be a contiguous float32 tensor shaped like rgb")
     _lib.call("svdlut_fused_fwd_packed_ex", _p(rgb), b, h, w, y0, h_total, _p(tables.buf),
-              tables.d_t, tables.d_s, _p(out), _p(None), 0, _p(nonfinite), variant,
-              _stream(rgb))
+              tables.d_t, tables.d_s, _p(out), _p(None), 0, _p(nonfinite), _stream(rgb))
     return out
 
 

@@ -1,0 +1,54 @@
+"""Python mirror of the packed-table layout (paper_2508_16121_b200/csrc/svdlut_common.cuh).
+
+Used by the boundary test (sizes) and by the poisoned-table GPU test, which
+builds packed tables by hand so that the fused kernel's output reveals the
+cell it selected.  Floats throughout.
+"""
+
+import numpy as np
+
+
+def cst_for(dt):
+    return (dt - 1) + ((3 - (dt - 1)) & 7)
+
+
+class Layout:
+    def __init__(self, dt, ds):
+        self.dt, self.ds = dt, ds
+        self.cst = cst_for(dt)
+        self.plane_floats = (dt - 1) * self.cst * 4
+        self.lut_off = 0
+        self.xc_off = self.lut_off + 9 * self.plane_floats
+        self.gxy_off = self.xc_off + 3 * (ds - 1) * (ds - 1) * 4
+        self.gyc_off = self.gxy_off + ((ds * ds * 3 + 3) & ~3)
+        self.total_floats = (self.gyc_off + 3 * ds * ds + 31) & ~31
+
+    @property
+    def bytes(self):
+        return self.total_floats * 4
+
+    def plane_off(self, p, k):
+        return self.lut_off + (3 * p + k) * self.plane_floats
+
+
+def coef_slot(c, q):
+    """Float position (0..11) of coefficient q (A, B, C, D) of channel c in a
+    cell's three chunks {A0 A1 B0 B1} {C0 C1 D0 D1} {A2 C2 B2 D2}."""
+    if c < 2:
+        return (c, 2 + c, 4 + c, 6 + c)[q]
+    return (8, 10, 9, 11)[q]
+
+
+def write_cells(table, L, p, c, coef):
+    """Write coefficient arrays coef (4, dt-1, dt-1) = (A, B, C, D) of channel
+    c, pair p (cells (i, j)), into a flat table."""
+    n = L.dt - 1
+    for q in range(4):
+        slot = coef_slot(c, q)
+        base = L.plane_off(p, slot // 4)
+        plane = table[base:base + L.plane_floats].reshape(n, L.cst, 4)
+        plane[:, :n, slot % 4] = coef[q]
+
+
+def empty_table(L):
+    return np.zeros(L.total_floats, np.float32)

@@ -47,21 +47,17 @@ def test_version_and_status_names(lib):
 
 
 def layout_bytes(dt, ds):
-    """Python mirror of TableLayout (svdlut_common.cuh)."""
-    cst = (dt - 1) + ((3 - (dt - 1)) & 7)
-    pair = (dt - 1) * cst * 12
-    xc = 2 * pair
-    gxy = xc + 3 * (ds - 1) * (ds - 1) * 4
-    gyc = gxy + ((ds * ds * 3 + 3) & ~3)
-    lut2 = (gyc + 3 * ds * ds + 31) & ~31
-    return ((lut2 + pair + 31) & ~31) * 4
+    from _layout import Layout
+
+    return Layout(dt, ds).bytes
 
 
 def test_table_sizes(lib):
-    # d_t=33, d_s=17: LUT row stride 35 (= 3 mod 8) -> 3 pairs of 32*35 cells x 48 B
+    # d_t=33, d_s=17: 9 chunk planes of 32 x 35 cells (row stride 35 = 3 mod 8)
+    # x 16 B, then the merged grid block
     assert 35 % 8 == 3
     assert lib.svdlut_table_bytes(33, 17) == layout_bytes(33, 17)
-    assert layout_bytes(33, 17) >= 3 * 32 * 35 * 48 + 3 * 16 * 16 * 16 + 17 * 17 * 12 + 3 * 17 * 17 * 4
+    assert layout_bytes(33, 17) >= 9 * 32 * 35 * 16 + 3 * 16 * 16 * 16 + 17 * 17 * 12 + 3 * 17 * 17 * 4
     for dt, ds in ((2, 2), (7, 8), (17, 8), (65, 33)):
         assert lib.svdlut_table_bytes(dt, ds) == layout_bytes(dt, ds)
     assert lib.svdlut_table_bytes(1, 17) == 0

@@ -34,13 +34,13 @@ def T(a, dev):
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
 
-def fast(c, dev, variant=-1, y0=0, h_total=None, rgb=None):
+def fast(c, dev, y0=0, h_total=None, rgb=None):
     from paper_2508_16121_b200 import device
 
     tables = device.pack_tables(T(c["lp"], dev), T(c["lw"], dev), T(c["lb"], dev), T(c["gp"], dev),
                                 T(c["gw"], dev), T(c["gb"], dev))
     x = T(c["rgb"] if rgb is None else rgb, dev)
-    return device.apply(x, tables, variant=variant, y0=y0, h_total=h_total)[0].cpu().numpy()
+    return device.apply(x, tables, y0=y0, h_total=h_total)[0].cpu().numpy()
 
 
 def exact(c, dev):
@@ -61,15 +61,14 @@ def test_exact_kernel_bit_identical_to_reference_golden(golden, dev):
         assert np.array_equal(exact(c, dev), c["want"]), name
 
 
-@pytest.mark.parametrize("variant", [0, 1])
-def test_fast_kernel_within_tolerance_on_golden(golden, dev, variant):
+def test_fast_kernel_within_tolerance_on_golden(golden, dev):
     from paper_2508_16121_b200 import device
 
     for name in golden["tr_cases"]:
         c = golden_case(golden, str(name))
         if not device.fast_supported(c["lp"].shape[2], c["gp"].shape[2]):
             continue
-        err = np.abs(fast(c, dev, variant) - c["want"]).max()
+        err = np.abs(fast(c, dev) - c["want"]).max()
         assert err <= TOL, (name, err)
 
 
@@ -109,10 +108,9 @@ def test_config2_4k_fast_and_exact_vs_oracle(dev, oracle_mod):
     c = dict(rgb=case.rgb, lp=planes, lw=case.lw, lb=case.lb, gp=case.grid_planes, gw=case.gw,
              gb=case.gb)
     want = oracle_out(oracle_mod, c)
-    for variant in (0, 1):
-        got = fast(c, dev, variant)
-        err = float(np.abs(got - want).max())
-        assert err <= TOL, (variant, err)
+    got = fast(c, dev)
+    err = float(np.abs(got - want).max())
+    assert err <= TOL, err
     assert np.array_equal(exact(c, dev), want)
     # full-size index check
     idx = device.indices(T(case.rgb, dev), 33, 17)[0]
@@ -158,8 +156,7 @@ def test_batch_equals_per_image(dev, oracle_mod):
 def test_odd_sizes(dev, oracle_mod, w, h):
     c = make_inputs(w, h, d_t=33, d_s=17, seed=w, low=-0.5, high=1.5)
     want = oracle_out(oracle_mod, c)
-    for variant in (0, 1):
-        assert np.abs(fast(c, dev, variant) - want).max() <= TOL, variant
+    assert np.abs(fast(c, dev) - want).max() <= TOL
 
 
 def test_misaligned_buffers_use_scalar_path(dev, oracle_mod):
@@ -173,7 +170,7 @@ def test_misaligned_buffers_use_scalar_path(dev, oracle_mod):
     x.copy_(T(c["rgb"], dev)[None])
     tables = device.pack_tables(T(c["lp"], dev), T(c["lw"], dev), T(c["lb"], dev), T(c["gp"], dev),
                                 T(c["gw"], dev), T(c["gb"], dev))
-    got = device.apply(x, tables, variant=0)[0].cpu().numpy()
+    got = device.apply(x, tables)[0].cpu().numpy()
     assert np.abs(got - oracle_out(oracle_mod, c)).max() <= TOL
 
 

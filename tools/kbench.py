@@ -1,10 +1,10 @@
-"""Kernel-level timing of the fused forward variants (development tool).
+"""Kernel-level timing of the fused forward (development tool).
 
-    python tools/kbench.py [--reps 50] [--only smooth|uniform] [--variant V] [--once]
+    [SVDLUT_LIB=<variant .so>] python tools/kbench.py [--reps 50] [--only smooth|uniform] [--once]
 
-Prints one line per (workload, variant): kernel µs (CUDA events over `reps`
-launches rotating 4 buffer sets), GB/s at 24 B/pixel, fraction of the measured
-HBM copy peak.  --once launches each variant once (for ncu captures).
+Prints one line per workload: kernel µs (CUDA events over `reps` launches
+rotating 4 buffer sets), GB/s at 24 B/pixel, fraction of the measured HBM copy
+peak.  --once launches the kernel once (for ncu captures).
 """
 
 import argparse
@@ -26,7 +26,6 @@ from paper_2508_16121_b200 import device, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--only", default=None)
-ap.add_argument("--variant", type=int, default=None)
 ap.add_argument("--once", action="store_true")
 ap.add_argument("--h", type=int, default=2160)
 ap.add_argument("--w", type=int, default=3840)
@@ -38,7 +37,6 @@ peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if 
 H, W = a.h, a.w
 work = {"smooth": lambda: synth.make_case(0, h=H, w=W),
         "uniform": lambda: synth.uniform_case(0, H, W)}
-variants = [a.variant] if a.variant is not None else [0, 1]
 for name, mk in work.items():
     if a.only and name != a.only:
         continue
@@ -50,21 +48,20 @@ for name, mk in work.items():
     base = T(case.rgb)[None]
     ins = [base] + [torch.roll(base, 17 * i, 3).contiguous() for i in range(1, 4)]
     outs = [torch.empty_like(base) for _ in range(4)]
-    for v in variants:
-        if a.once:
-            device.apply(ins[0], tables, out=outs[0], variant=v)
-            torch.cuda.synchronize()
-            print(f"{name} variant={v} launched once")
-            continue
-        for i in range(5):
-            device.apply(ins[i % 4], tables, out=outs[i % 4], variant=v)
-        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        e0.record()
-        for i in range(a.reps):
-            device.apply(ins[i % 4], tables, out=outs[i % 4], variant=v)
-        e1.record()
+    if a.once:
+        device.apply(ins[0], tables, out=outs[0])
         torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / a.reps
-        gbs = 24 * H * W / (us * 1e-6) / 1e9
-        print(f"{name:8s} variant={v} {us:8.2f} us  {gbs:7.1f} GB/s  frac={gbs / peak:.3f}  "
-              f"{H * W / us:.0f} MP/s")
+        print(f"{name} launched once")
+        continue
+    for i in range(5):
+        device.apply(ins[i % 4], tables, out=outs[i % 4])
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for i in range(a.reps):
+        device.apply(ins[i % 4], tables, out=outs[i % 4])
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / a.reps
+    gbs = 24 * H * W / (us * 1e-6) / 1e9
+    print(f"{os.environ.get('SVDLUT_LIB', 'default')} {name:8s} {H}x{W} {us:8.2f} us  {gbs:7.1f} GB/s  "
+          f"frac={gbs / peak:.3f}  {H * W / us:.0f} MP/s")

@@ -89,8 +89,13 @@ int main() {
   for (auto& kk : ks) {
     CK(cudaFuncSetAttribute(kk.k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_FLOATS * 4));
     for (int pat = 0; pat < 8; ++pat) {
-      for (int am = 0; am < 3; ++am) {
-        int mask = am == 0 ? -1 : (am == 1 ? 0x0000FFFF : 0x55555555);
+      for (int am = 0; am < 5; ++am) {
+        // all / first 16 lanes / even lanes / one quarter-warp (lanes 0-7) /
+        // one lane per quarter-warp: do predicated-off 8-lane phases of an
+        // LDS.128 cost wavefronts?
+        const int masks[5] = {-1, 0x0000FFFF, 0x55555555, 0x000000FF, 0x01010101};
+        const char* mnames[5] = {"all ", "lo16", "even", "q0  ", "1/q "};
+        int mask = masks[am];
         kk.k<<<nsm, threads, SMEM_FLOATS * 4>>>(pat, mask, out, cyc);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
@@ -98,7 +103,7 @@ int main() {
         double avg = 0; for (int i = 0; i < nsm; ++i) avg += hc[i]; avg /= nsm;
         double per = avg / ((double)ITERS * (threads / 32));
         printf("LDS.%d pat=%-20s mask=%s  cycles/warp-instr/SM=%.3f\n", kk.w * 32, names[pat],
-               am == 0 ? "all " : (am == 1 ? "lo16" : "even"), per);
+               mnames[am], per);
       }
     }
   }
