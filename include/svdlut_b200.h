@@ -219,10 +219,13 @@ int svdlut_fused_fwd_l2(const float* rgb, const float* target, int batch, int h,
                         float* gmax, float gscale, void* stream);
 
 /* svdlut_fused_bwd with optional packed `tables` (from svdlut_pack_tables*,
- * biases are irrelevant to the backward) and optional per-image `gmax`
- * (>= max |gy|, e.g. from svdlut_fused_fwd_l2); NULL recomputes either. */
+ * biases are irrelevant to the backward) and optional per-image statistics
+ * of gy: `gmax` (>= max |gy|, e.g. from svdlut_fused_fwd_l2) and `gsumsq`
+ * (sum of gy^2, f64, may be NULL).  The vertex scatter is 32-bit fixed point
+ * scaled by B = min(gmax, 6 rms(gy)); pixels with |gy| > B scatter through
+ * f32 atomics instead.  NULL gmax recomputes both statistics. */
 int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h, int w, int y0,
-                            int h_total, const void* tables, const float* gmax,
+                            int h_total, const void* tables, const float* gmax, const double* gsumsq,
                             const float* lut_planes, const float* lw, int d_t,
                             const float* grid_planes, const float* gw, int k, int d_s, float* gx,
                             float* dlut_planes, float* dlw, float* dlb, float* dgrid_planes,

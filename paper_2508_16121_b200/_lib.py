@@ -54,8 +54,8 @@ _SIGS = {
     "svdlut_apply_lut3d": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp]),
     "svdlut_fused_fwd_l2": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _vp, _vp,
                                  ctypes.c_float, _vp]),
-    "svdlut_fused_bwd_packed": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _i,
-                                     _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "svdlut_fused_bwd_packed": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp,
+                                     _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "svdlut_occurrence": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "svdlut_fused_fwd_io": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _i, _vp, _vp]),
     "svdlut_enhance_host_io": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,

@@ -62,9 +62,12 @@ def l2_step(rgb, target, u, s, vt, lw, lb, grid_planes, gw, gb, need_gx=True):
     """
     planes = device.reconstruct(u, s, vt)
     tables = device.pack_tables(planes, lw, lb, grid_planes, gw, gb)
-    gy, loss_sum, gmax = device.apply_l2(rgb, target, tables)
+    gscale = 2.0 / rgb.numel()
+    gy, loss_sum, gmax = device.apply_l2(rgb, target, tables, gscale=gscale)
+    # sum gY^2 per image = gscale^2 * sum (Y - T)^2: sets the scatter's
+    # fixed-point bound (outlier residuals take the f32 path)
     g = device.fused_backward(rgb, gy, planes, lw, grid_planes, gw, need_gx=need_gx, tables=tables,
-                              gmax=gmax)
+                              gmax=gmax, gsumsq=loss_sum * (gscale * gscale))
     du, ds, dvt = device.reconstruct_backward(u, s, vt, g["dlut_planes"])
     return {"loss": loss_sum.sum() / rgb.numel(), "gx": g["gx"], "u": du, "s": ds, "vt": dvt,
             "lw": g["dlw"], "lb": g["dlb"], "grid_planes": g["dgrid_planes"], "gw": g["dgw"],

@@ -76,7 +76,7 @@ size_t bwd_workspace_bytes(int batch, int h, int w, int dt, int ds, int k) {
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
   return rup((size_t)batch * L.bytes()) + rup((size_t)batch * A.total * 4) +
-         rup((size_t)batch * (3 + k) * 4) + rup((size_t)batch * 4) + 256;
+         rup((size_t)batch * (3 + k) * 4) + rup((size_t)batch * 4) + rup((size_t)batch * 8) + 256;
 }
 
 struct BwdParams {
@@ -91,7 +91,8 @@ struct BwdParams {
   int tex_base;
   double rcp_w, rcp_h;
   float* E;            // global accumulators, batch * A.total
-  const float* gmax;   // per image max|gY| (fixed-point scale)
+  const float* gmax;   // per image max|gY|
+  const double* gss;   // per image sum of gY^2 (may be NULL): outlier bound
 };
 
 __device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
@@ -108,8 +109,12 @@ __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, floa
 }
 
 // Scatter values are accumulated as 32-bit fixed point: v * S with
-// S = 2^16 / max|gY| of the image, so one contribution is at most 2^16 in
-// magnitude (resolution 1.5e-5 max|gY|).  Conversion is an add of 1.5*2^23
+// S = 2^16 / B, B = min(max|gY|, kOutlierSigmas * rms(gY)) of the image, so
+// one contribution is at most 2^16 in magnitude (resolution 2^-16 B).
+// Pixels with some |gY| > B (heavy-tailed residuals) would either overflow
+// that bound or, with B = max|gY|, leave the rest of the image with too
+// coarse a resolution; they scatter through global f32 atomics instead
+// (rare by construction).  Conversion is an add of 1.5*2^23
 // (round to nearest even on the FMA pipe).  Shared integer atomics are native
 // (ATOMS.ADD, ~2 cycles per warp instruction with distinct addresses, measured
 // in tools/microbench/atomicbench.cu) whereas shared f32 atomics are CAS loops
@@ -124,6 +129,7 @@ __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, floa
 // kMaxFlushPx pixels may accumulate between flushes (rows <= kMaxFlushPx px).
 constexpr int kMaxFlushPx = 32767;
 constexpr float kFixedOne = 65536.0f;
+constexpr float kOutlierSigmas = 6.0f;
 __device__ __forceinline__ int to_fixed(float v, float S) {
   return __float_as_int(__fmaf_rn(v, S, 12582912.0f)) - 0x4B400000;
 }
@@ -259,8 +265,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       copy(sbase + 3u * plane_bytes, reinterpret_cast<const char*>(tb + L.xc_off), grid_bytes);
     }
     for (int i = threadIdx.x; i < A.total; i += blockDim.x) Ei[i] = 0;
-    const float gm = p.gmax[b];
+    float gm = p.gmax[b];
+    if (p.gss) gm = fminf(gm, kOutlierSigmas * (float)sqrt(p.gss[b] / (3.0 * (double)pl)));
     const float S = gm > 0.f ? kFixedOne / gm : 1.0f;  // fixed-point scale of this image
+    const float bound = gm > 0.f ? gm : 3.4e38f;       // |gY| above: global slow path
     const float invS = 1.0f / S;
     float* Eg = p.E + (long long)b * A.total;
     int px_since_flush = 0;
@@ -329,6 +337,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           const bool valid = xl + u < p.w;
           const float g0 = valid ? cur.y0[u] : 0.f, g1 = valid ? cur.y1[u] : 0.f,
                       g2 = valid ? cur.y2[u] : 0.f;
+          // outliers take the f32 slow path; the fixed-point path sees zeros
+          const bool big = fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))) > bound;
+          const float f0 = big ? 0.f : g0, f1 = big ? 0.f : g1, f2 = big ? 0.f : g2;
           gsum0 += g0;
           gsum1 += g1;
           gsum2 += g2;
@@ -382,9 +393,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // ---- scatter: LUT pairs, one fixed-point atomic per value ----
           if (valid) {
             const int ir = (int)(br - kMagic), ig = (int)(bg - kMagic), ib = (int)(bb - kMagic);
-            const float q0 = rc0 == 0 ? g0 : (rc0 == 1 ? g1 : g2);  // gY in this lane's channel order
-            const float q1 = rc1 == 0 ? g0 : (rc1 == 1 ? g1 : g2);
-            const float q2 = rc2 == 0 ? g0 : (rc2 == 1 ? g1 : g2);
+            const float q0 = rc0 == 0 ? f0 : (rc0 == 1 ? f1 : f2);  // gY in this lane's channel order
+            const float q1 = rc1 == 0 ? f0 : (rc1 == 1 ? f1 : f2);
+            const float q2 = rc2 == 0 ? f0 : (rc2 == 1 ? f1 : f2);
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
               const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
@@ -405,10 +416,47 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               }
             }
           }
+          if (big) {  // every scatter of this pixel straight to the global f32 sums
+            const float gg[3] = {g0, g1, g2};
+            const int ii[3] = {(int)(br - kMagic), (int)(bg - kMagic), (int)(bb - kMagic)};
+            const float dd[3] = {dr, dg, db};
+#pragma unroll
+            for (int pr = 0; pr < 3; ++pr) {
+              const int a = pr == 2 ? 1 : 0, bq = pr == 0 ? 1 : 2;
+              float* e = Eg + A.lut_off + ((pr * dt + ii[a]) * (dt + 1) + ii[bq]) * 3;
+#pragma unroll
+              for (int kc = 0; kc < 4; ++kc) {
+                const float wgt = ((kc & 1) ? dd[a] : 1.f - dd[a]) * ((kc & 2) ? dd[bq] : 1.f - dd[bq]);
+                float* ec = e + ((kc & 1) ? (dt + 1) * 3 : 0) + ((kc & 2) ? 3 : 0);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) atomicAdd(ec + c, gg[c] * wgt);
+              }
+            }
+            const int jcs[3] = {(int)(sr - kMagic), (int)(sg - kMagic), (int)(sb - kMagic)};
+            const float ecs[3] = {er, eg, eb};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              float* xy = Eg + A.grid_off + c * ds * ds + jx * ds + jy;
+              atomicAdd(xy, gg[c] * (1.f - ex) * (1.f - ey));
+              atomicAdd(xy + ds, gg[c] * ex * (1.f - ey));
+              atomicAdd(xy + 1, gg[c] * (1.f - ex) * ey);
+              atomicAdd(xy + ds + 1, gg[c] * ex * ey);
+              float* xc = Eg + A.grid_off + 3 * ds * ds + c * ds * ds + jx * ds + jcs[c];
+              atomicAdd(xc, gg[c] * (1.f - ex) * (1.f - ecs[c]));
+              atomicAdd(xc + ds, gg[c] * ex * (1.f - ecs[c]));
+              atomicAdd(xc + 1, gg[c] * (1.f - ex) * ecs[c]);
+              atomicAdd(xc + ds + 1, gg[c] * ex * ecs[c]);
+              float* yc = Eg + A.grid_off + 6 * ds * ds + c * ds * ds + jy * ds + jcs[c];
+              atomicAdd(yc, gg[c] * (1.f - ey) * (1.f - ecs[c]));
+              atomicAdd(yc + ds, gg[c] * ey * (1.f - ecs[c]));
+              atomicAdd(yc + 1, gg[c] * (1.f - ey) * ecs[c]);
+              atomicAdd(yc + ds + 1, gg[c] * ey * ecs[c]);
+            }
+          }
           // ---- grids: xc + yc runs per channel (key = guide cell; x-cell checked) ----
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const float gc = c == 0 ? g0 : (c == 1 ? g1 : g2);
+            const float gc = c == 0 ? f0 : (c == 1 ? f1 : f2);
             const int jc = (int)((c == 0 ? sr : (c == 1 ? sg : sb)) - kMagic);
             const float ec = c == 0 ? er : (c == 1 ? eg : eb);
             const int key = valid ? (jx << 8) | jc : -1;
@@ -434,12 +482,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
             const float w00 = (1.f - ex) * (1.f - ey), w10 = ex * (1.f - ey);
             const float w01 = (1.f - ex) * ey, w11 = ex * ey;
             if (jx == jx_first) {
-              axy[0] += g0 * w00; axy[1] += g1 * w00; axy[2] += g2 * w00;
-              axy[3] += g0 * w10; axy[4] += g1 * w10; axy[5] += g2 * w10;
-              axy[6] += g0 * w01; axy[7] += g1 * w01; axy[8] += g2 * w01;
-              axy[9] += g0 * w11; axy[10] += g1 * w11; axy[11] += g2 * w11;
+              axy[0] += f0 * w00; axy[1] += f1 * w00; axy[2] += f2 * w00;
+              axy[3] += f0 * w10; axy[4] += f1 * w10; axy[5] += f2 * w10;
+              axy[6] += f0 * w01; axy[7] += f1 * w01; axy[8] += f2 * w01;
+              axy[9] += f0 * w11; axy[10] += f1 * w11; axy[11] += f2 * w11;
             } else if (valid) {  // the lane's pixels straddle an x-cell boundary
-              const float gg[3] = {g0, g1, g2};
+              const float gg[3] = {f0, f1, f2};
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
                 int* e = E_xy + c * ds * ds + jx * ds + jy;
@@ -567,11 +615,12 @@ __global__ void finalize_kernel(const float* __restrict__ lp, const float* __res
   }
 }
 
-// max|gY| per image (positive floats order like their bit patterns).
-__global__ void absmax_kernel(const float* __restrict__ gy, long long per_img, float* gmax) {
+// max|gY| and sum gY^2 per image (positive floats order like their bit patterns).
+__global__ void gy_stats_kernel(const float* __restrict__ gy, long long per_img, float* gmax, double* gss) {
   const long long b = blockIdx.y;
   const float* base = gy + b * per_img;
   float m = 0.f;
+  double sq = 0.0;
   const bool vec = (per_img % 4 == 0) && ((reinterpret_cast<uintptr_t>(gy) & 15) == 0);
   if (vec) {
     const float4* g = reinterpret_cast<const float4*>(base);
@@ -579,14 +628,23 @@ __global__ void absmax_kernel(const float* __restrict__ gy, long long per_img, f
          i += (long long)gridDim.x * blockDim.x) {
       const float4 v = __ldcs(g + i);
       m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      sq += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
     }
   } else {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_img;
-         i += (long long)gridDim.x * blockDim.x)
+         i += (long long)gridDim.x * blockDim.x) {
       m = fmaxf(m, fabsf(base[i]));
+      sq += (double)base[i] * base[i];
+    }
   }
-  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(gmax + b), __float_as_int(m));
+  for (int off = 16; off > 0; off >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    sq += __shfl_xor_sync(0xffffffffu, sq, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(reinterpret_cast<int*>(gmax + b), __float_as_int(m));
+    atomicAdd(gss + b, sq);
+  }
 }
 
 cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w, int y0,
@@ -594,7 +652,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
                              const float* gp, const float* gw, int k, int ds, float* gx,
                              float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
                              float* dgb, void* ws, size_t ws_bytes, cudaStream_t st,
-                             const float* tables_in, const float* gmax_in) {
+                             const float* tables_in, const float* gmax_in, const double* gss_in) {
   (void)ws_bytes;
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
@@ -610,18 +668,22 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   float* zb = (float*)wp;  // zero biases (biases do not enter any derivative)
   wp += rup((size_t)batch * (3 + k) * 4);
   float* gmax = (float*)wp;
+  wp += rup((size_t)batch * 4);
+  double* gss = (double*)wp;
   cudaError_t e;
   if ((e = cudaMemsetAsync(zb, 0, (size_t)batch * (3 + k) * 4, st)) != cudaSuccess) return e;
   if (gmax_in) {
-    gmax = const_cast<float*>(gmax_in);  // caller-provided bound on max |gY| per image
+    gmax = const_cast<float*>(gmax_in);  // caller-provided max |gY| per image
+    gss = const_cast<double*>(gss_in);   // and sum gY^2 (may be NULL: bound = max)
   } else {
     if ((e = cudaMemsetAsync(gmax, 0, (size_t)batch * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(gss, 0, (size_t)batch * 8, st)) != cudaSuccess) return e;
     const long long per = 3LL * h * w;
     long long blocks = (per / 4 + 255) / 256;
     if (blocks > 512) blocks = 512;
     if (blocks < 1) blocks = 1;
     dim3 g((unsigned)blocks, batch);
-    absmax_kernel<<<g, 256, 0, st>>>(gy, per, gmax);
+    gy_stats_kernel<<<g, 256, 0, st>>>(gy, per, gmax, gss);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if ((e = cudaMemsetAsync(E, 0, (size_t)batch * A.total * 4, st)) != cudaSuccess) return e;
@@ -646,6 +708,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   p.rcp_h = 1.0 / (double)(h_total - 1);
   p.E = E;
   p.gmax = gmax;
+  p.gss = gss;
   if ((e = table_texture(tables, (size_t)batch * L.bytes(), st, &p.tex, &p.tex_base)) != cudaSuccess) return e;
   const long long rows = (long long)batch * h;
   if (rows > 0 && w > 0) {

@@ -377,7 +377,7 @@ int svdlut_fused_fwd_l2(const float* rgb, const float* target, int batch, int h,
 }
 
 int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h, int w, int y0,
-                            int h_total, const void* tables, const float* gmax,
+                            int h_total, const void* tables, const float* gmax, const double* gsumsq,
                             const float* lut_planes, const float* lw, int d_t,
                             const float* grid_planes, const float* gw, int k, int d_s, float* gx,
                             float* dlut_planes, float* dlw, float* dlb, float* dgrid_planes,
@@ -399,7 +399,7 @@ int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h,
     return fail(SVDLUT_ERR_INVALID_ARGUMENT, "workspace too small (%zu < %zu)", workspace_bytes, need);
   CUDA_TRY(launch_fused_bwd(rgb, gy, batch, h, w, y0, h_total, lut_planes, lw, d_t, grid_planes, gw, k,
                             d_s, gx, dlut_planes, dlw, dlb, dgrid_planes, dgw, dgb, workspace,
-                            workspace_bytes, (cudaStream_t)stream, (const float*)tables, gmax),
+                            workspace_bytes, (cudaStream_t)stream, (const float*)tables, gmax, gsumsq),
            "fused backward");
   return SVDLUT_OK;
 }

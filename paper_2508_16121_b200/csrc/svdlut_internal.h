@@ -62,7 +62,8 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
                              const float* gp, const float* gw, int k, int ds, float* gx,
                              float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
                              float* dgb, void* ws, size_t ws_bytes, cudaStream_t st,
-                             const float* tables_in = nullptr, const float* gmax_in = nullptr);
+                             const float* tables_in = nullptr, const float* gmax_in = nullptr,
+                             const double* gss_in = nullptr);
 size_t bwd_workspace_bytes(int batch, int h, int w, int dt, int ds, int k);
 
 cudaError_t launch_reconstruct_bwd(const float* u, const float* s, const float* vt,

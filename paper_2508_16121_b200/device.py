@@ -320,13 +320,13 @@ def apply_l2(rgb, target, tables, gscale=None, y0=0, h_total=None):
 
 
 def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None, need_gx=True,
-                   tables=None, gmax=None):
+                   tables=None, gmax=None, gsumsq=None):
     """Gradients of the fused apply w.r.t. the input and every table.
 
-    ``tables`` (the forward's PackedTables) and ``gmax`` (per-image bound on
-    max |gy|, e.g. from apply_l2) skip the backward's own table packing and
-    max-reduction pass.  Returns dict(gx, dlut_planes, dlw, dlb, dgrid_planes,
-    dgw, dgb).
+    ``tables`` (the forward's PackedTables) and ``gmax`` / ``gsumsq``
+    (per-image max |gy| and float64 sum of gy^2, e.g. from apply_l2) skip the
+    backward's own table packing and statistics pass.  Returns dict(gx,
+    dlut_planes, dlw, dlb, dgrid_planes, dgw, dgb).
     """
     lp = _f32(lut_planes, "lut_planes", 5)
     lw = _f32(lw, "lw", 3)
@@ -354,8 +354,10 @@ def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None,
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     if gmax is not None and (gmax.dtype != torch.float32 or gmax.numel() != b):
         raise DimensionMismatch("gmax must be a float32 tensor with one entry per image")
+    if gsumsq is not None and (gsumsq.dtype != torch.float64 or gsumsq.numel() != b or gmax is None):
+        raise DimensionMismatch("gsumsq must be a float64 tensor with one entry per image (with gmax)")
     _lib.call("svdlut_fused_bwd_packed", _p(rgb), _p(gy), b, h, w, y0, h_total,
-              _p(tables.buf if tables is not None else None), _p(gmax), _p(lp), _p(lw), d_t,
+              _p(tables.buf if tables is not None else None), _p(gmax), _p(gsumsq), _p(lp), _p(lw), d_t,
               _p(gp), _p(gw), k, d_s, _p(g["gx"]), _p(g["dlut_planes"]), _p(g["dlw"]),
               _p(g["dlb"]), _p(g["dgrid_planes"]), _p(g["dgw"]), _p(g["dgb"]), _p(ws), ws_bytes,
               _stream(rgb))

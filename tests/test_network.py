@@ -105,6 +105,18 @@ def test_run_model_end_to_end_gpu(golden, ngold):
     __graft_entry__.build_library()
     y = network.run_model(Image(720, 480, c1_input()), network.random_init(0))
     assert np.abs(y.data[:, ::7, ::11] - golden["c1_out_sub"]).max() <= OUT_TOL
+    # all 1.04 M samples: the reference output is rebuilt bit-exactly from the
+    # reference's own tables by the oracle (its SHA is the reference's,
+    # test_oracle.test_config1_end_to_end_bit_exact)
+    import hashlib
+
+    import oracle
+
+    planes = oracle.reconstruct(golden["c1_u"], golden["c1_s"], golden["c1_vt"])
+    ref = oracle.fused_fwd(c1_input(), planes, golden["c1_lw"], golden["c1_lb"], golden["c1_gp"],
+                           golden["c1_gw"], golden["c1_gb"], threads=oracle.max_threads())
+    assert hashlib.sha256(ref.tobytes()).hexdigest() == str(golden["c1_out_sha"])
+    assert np.abs(y.data - ref).max() <= OUT_TOL
     p_small = network.random_init(3, network.HyperParams(**SMALL))
     y = network.run_model(Image(300, 200, sm_input()), p_small)
     assert np.abs(y.data[:, ::3, ::5] - ngold["sm_out_sub"]).max() <= OUT_TOL
