@@ -8,9 +8,13 @@ float32 smooth-field image with its own SVD factors / grids / weights
 hot path on one batch: LUT reconstruction from U,S,Vt + table packing + fused
 slice/LUT apply, as CUDA kernels on the current stream.  Four input/output
 buffer sets rotate between steps (4 x 199 MB > 126 MB L2), so every step
-streams from HBM.  Multi-GPU: one process per GPU (torchrun), each rank its
-own image (per-image sharding, no data-path collective) -> "scaling": "weak";
-time = max over ranks of the CUDA-event time (NCCL all_reduce MAX).
+streams from HBM.  Multi-GPU: one process per GPU, each rank its own image
+(per-image sharding, no data-path collective) -> "scaling": "weak"; time = max
+over ranks of the CUDA-event time (NCCL all_reduce MAX).  `--gpus N` without
+a launcher re-executes itself under torch.distributed.run with N ranks.  At
+every N the line also carries the strong-scaled configs 3 (16 x 4K images over
+N ranks) and 4 (one 8K image in N row strips), each with a bitwise check of
+the sharded outputs against the 1-GPU result (outside the timed region).
 
 Reported besides the contract keys:
   roofline      fused-kernel achieved GB/s (24 B/pixel algorithmic) vs the
@@ -51,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-3 / config-4 fields")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (2 = headline; 3 batched 16x4K per-image shards, "
                          "4 8K row strips, 5 training step on 8x1080p)")
@@ -185,9 +190,53 @@ def cpu_single_thread(case, frames=2):
     return H * W * frames / (time.perf_counter() - t0) / 1e6
 
 
+def ref_numba(mode, threads, frames):
+    """The unmodified reference (numba, baseline/_ref) timed in a fresh
+    process with a fresh NUMBA_CACHE_DIR (tools/ref_numba.py)."""
+    import subprocess
+    import tempfile
+
+    with tempfile.TemporaryDirectory(prefix="numba_ref_") as cache:
+        env = dict(os.environ, NUMBA_CACHE_DIR=cache, PYTHONDONTWRITEBYTECODE="1")
+        res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ref_numba.py"), mode, "--threads",
+                              str(threads), "--frames", str(frames)], env=env, capture_output=True, text=True,
+                             timeout=900)
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    if res.returncode or not lines:
+        return {"unavailable": (res.stderr.strip().splitlines() or ["no output"])[-1][:200]}
+    return json.loads(lines[-1])
+
+
 def run_reference_arm(a):
+    """The reference's CPU implementation of the path on this box's host
+    cores, rank 0 only.  `value`: the C restatement of the reference kernel
+    (oracle/svdlut_oracle.c, bit-identical output, all cores; the reference
+    is a numba package, not compiled code, so there is no oracle/_ref); the
+    unmodified reference itself (numba fused_enhance from baseline/_ref, N
+    threads and 1 thread, fresh caches) is reported beside it."""
     rank, world, _ = dist_env()
     if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    if a.config == 1:
+        r = ref_numba("model", 1, max(3, a.steps))
+        value = r.get("mps")
+        line = {
+            "impl": "reference", "metric": "megapixels/sec full model forward (resize + backbone + heads + "
+                                           "tables + fused apply) at 720x480 fp32",
+            "value": round(value, 4) if value else None, "unit": UNIT, "n_gpus": world, "steps": max(3, a.steps),
+            "warmup": 1, "ms_per_step": r.get("ms_median"), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 backbone / f64 apply", "data": "synthetic (uniform image, seed 0)",
+            "config": {"workload": "config1: reference network.run_model(720x480, random_init(0)) on the host "
+                                   "(numpy backbone + numba fused_enhance, 1 thread)"},
+            "cpu_baseline": {"value": round(value, 4) if value else None, "unit": UNIT, "cores": 1,
+                             "kind": "reference", "sample": "run_model on one 720x480 image per step", **r},
+            "e2e": {"value": round(value, 4) if value else None, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        if value is None:
+            line = {"impl": "reference", "unavailable": r.get("unavailable", "reference run failed")}
+        print(json.dumps(line), flush=True)
         return 0
     from paper_2508_16121_b200 import synth
 
@@ -197,6 +246,9 @@ def run_reference_arm(a):
     times = times[max(0, a.warmup):] or times
     total = sum(times)
     value = H * W * len(times) / total / 1e6
+    # the unmodified reference: parallel twin in its own fresh process first, then the serial one
+    numba_n = ref_numba("fused", threads, 3)
+    numba_1 = ref_numba("fused", 1, 2)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
         "n_gpus": world, "steps": len(times), "warmup": a.warmup,
@@ -204,13 +256,147 @@ def run_reference_arm(a):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(1),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": "full 3x2160x3840 frame per step (reconstruct + fused apply), "
                                    "oracle/svdlut_oracle.c on pthreads"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_numba": {"threads_n": numba_n, "threads_1": numba_1,
+                            "what": "unmodified reference svdlut (baseline/_ref): reconstruct_lut + "
+                                    "fused_enhance(threads) per 4K frame (mps, public API) and the numba "
+                                    "twin alone (kernel_mps); fresh NUMBA_CACHE_DIR per process"},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------------------- launcher
+def free_port():
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(a):
+    """`bench.py --gpus N` (N > 1) started without a launcher: re-execute
+    under torch.distributed.run with one rank per GPU; returns the exit code,
+    or None when already inside a launcher (or N == 1)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import subprocess
+
+    import torch
+
+    n = torch.cuda.device_count()
+    if n < a.gpus and not os.environ.get("BENCH_SINGLE_DEVICE_TEST"):
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {a.gpus} but {n} CUDA devices visible"}),
+              flush=True)
+        return 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(a.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def coll_device(dev):
+    """Device of the host-side collectives (gloo in the single-device test)."""
+    import torch
+
+    return torch.device("cpu") if os.environ.get("BENCH_SINGLE_DEVICE_TEST") else dev
+
+
+# --------------------------------------------------------------------------- configs 3 / 4 at N
+def extra_configs(a, rank, world, dev):
+    """Strong-scaled config 3 (16 x 4K images, own tables each, rank r takes a
+    contiguous block) and config 4 (one 8K image, rank r takes a strip of
+    rows with (y0, H_total)) at this world size: K timed steps between
+    barriers, max over ranks; then, outside the timed region, the sharded
+    outputs are checked bitwise against a single-GPU run on rank 0 (config 4:
+    all strips gathered; config 3: the last rank's block, recomputed)."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_16121_b200 import device, parallel, synth
+
+    cdev = coll_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    keys = ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+
+    def timed(step):
+        for _ in range(max(3, a.warmup)):
+            step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return parallel.max_over_ranks(e0.elapsed_time(e1) / a.steps, device=cdev)
+
+    def tables_of(case):
+        p = {k: T(getattr(case, k)) for k in keys}
+        return device.pack_tables_factors(*(p[k] for k in keys))
+
+    out = {}
+    # ---- config 3 ----
+    lo, hi = parallel.image_block(16, world, rank)
+    case3 = synth.make_batch(list(range(lo, hi)))
+    x3 = T(case3.rgb)
+    p3 = {k: T(getattr(case3, k)) for k in keys}
+    y3 = torch.empty_like(x3)
+
+    def step3():
+        device.apply(x3, device.pack_tables_factors(*(p3[k] for k in keys)), out=y3)
+
+    ms3 = timed(step3)
+    h3 = torch.tensor(list(hashlib.sha256(y3.cpu().numpy().tobytes()).digest()[:8]), dtype=torch.int64,
+                      device=cdev)
+    ok3 = True
+    if world > 1:
+        hs = [torch.zeros_like(h3) for _ in range(world)]
+        dist.all_gather(hs, h3)
+        if rank == 0:  # the last rank's images recomputed here
+            llo, lhi = parallel.image_block(16, world, world - 1)
+            c = synth.make_batch(list(range(llo, lhi)))
+            ref = device.apply(T(c.rgb), tables_of(c))
+            want = list(hashlib.sha256(ref.cpu().numpy().tobytes()).digest()[:8])
+            ok3 = hs[-1].tolist() == want
+    out["config3"] = {"workload": "16 x 3x2160x3840 fp32 smooth fields, own factors/grids each, "
+                                  f"{hi - lo} per rank (strong scaling over {world})",
+                      "value": round(16 * H * W / (ms3 * 1e-3) / 1e6, 3), "unit": UNIT,
+                      "ms_per_step": round(ms3, 5), "scaling": "strong",
+                      "bitwise_vs_1gpu": ok3 if world > 1 else "n/a (1 GPU)"}
+    del x3, y3, p3
+    # ---- config 4 ----
+    full = synth.make_case(0, h=4320, w=7680)
+    y0, y1 = parallel.strip_rows(4320, world, rank)
+    x4 = T(full.rgb[None, :, y0:y1])
+    t4 = tables_of(full)
+    y4 = torch.empty_like(x4)
+
+    def step4():
+        device.apply(x4, t4, out=y4, y0=y0, h_total=4320)
+
+    ms4 = timed(step4)
+    ok4 = True
+    if world > 1:
+        g = parallel.gather_rows(y4.to(cdev))
+        if rank == 0:
+            ok4 = bool(torch.equal(g.to(dev), device.apply(T(full.rgb)[None], t4)))
+    out["config4"] = {"workload": f"one 3x4320x7680 fp32 image, row strip {y0}:{y1} per rank "
+                                  f"((y0, H_total=4320), strong scaling over {world})",
+                      "value": round(4320 * 7680 / (ms4 * 1e-3) / 1e6, 3), "unit": UNIT,
+                      "ms_per_step": round(ms4, 5), "scaling": "strong",
+                      "bitwise_vs_1gpu": ok4 if world > 1 else "n/a (1 GPU)"}
+    return out
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -218,6 +404,9 @@ def main():
     a = parse()
     if a.impl == "reference":
         return run_reference_arm(a)
+    rc = relaunch(a)
+    if rc is not None:
+        return rc
     if a.config == 1:
         return run_config1(a)
     if a.config != 2:
@@ -444,6 +633,8 @@ def main():
                          "oracle/svdlut_oracle.c (op-for-op restatement of the reference "
                          "kernel, bit-identical output) on pthreads"}
 
+    extras = {} if a.no_extra else extra_configs(a, rank, world, dev)
+
     if world > 1:
         torch.distributed.barrier()
     if rank == 0:
@@ -454,7 +645,7 @@ def main():
             "data": "synthetic (seeded smooth field, SURVEY.md §8d recipe)",
             "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "e2e_pnm_u8": e2e_u8, "gpu_launches": 2 * a.steps, "clocks": sampler.summary(),
-            "launch": "cuda graphs of 4 steps" if step_graphs else "eager",
+            "launch": "cuda graphs of 4 steps" if step_graphs else "eager", **extras,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
