@@ -205,8 +205,6 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + tables_bytes);
   const float tdm1 = (float)(dt - 1);
   const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
-  // inputs and tables may come from the previous kernel in the stream (PDL)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const uint32_t cst = (uint32_t)L.cst;
   const uint32_t cst16 = cst * 16u;
@@ -225,6 +223,20 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
   const long long g_end = (long long)(blockIdx.x + 1) * chunks_total / gridDim.x;
   const long long pl = p.pl_in, opl = p.pl_out;  // plane strides (floats)
   const long long plane_len = (long long)p.h * p.w;
+  // Programmatic dependent launch: the table-packing kernel before this one
+  // releases it early.  The input image is not written by that kernel, so the
+  // first rows of this CTA's range stream into L2 while the tables are
+  // packed; every read of the tables comes after griddepcontrol.wait.
+  if (threadIdx.x == blockDim.x - 32 && g_begin < g_end) {
+    const long long r0 = g_begin / cpr;
+    const int b0 = (int)(r0 / p.h), y0r = (int)(r0 - (long long)b0 * p.h);
+    const int y_end = (int)min((long long)p.h, (long long)y0r + kL2Rows + 2);
+    for (int yy = y0r; yy < y_end; ++yy) {
+      Src<IN>::prefetch_row(Src<IN>::image(p.in, b0, pl), pl, plane_len, yy, p.w);
+      if (LOSS) Src<kF32>::prefetch_row(Src<kF32>::image(p.target, b0, pl), pl, plane_len, yy, p.w);
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const bool vec_in = ((p.w & 3) == 0) && Src<IN>::aligned(p.in, pl);
   const bool vec_out = ((p.w & 3) == 0) && Dst<OUTF>::aligned(p.out, opl) &&
                        (!LOSS || Src<kF32>::aligned(p.target, pl));
@@ -529,9 +541,9 @@ static cudaError_t launch_dims(const FwdParams& p, bool check, int grid, size_t 
   cfg.blockDim = dim3(kFwdWarps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  // Programmatic dependent launch: the kernel's prologue (barriers, column
-  // table) may overlap the tail of the table-packing kernel before it; every
-  // global access comes after griddepcontrol.wait.
+  // Programmatic dependent launch: the kernel's prologue (barriers, L2
+  // prefetch of its first input rows) may overlap the table-packing kernel
+  // before it; every table read comes after griddepcontrol.wait.
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;

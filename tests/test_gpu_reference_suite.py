@@ -35,8 +35,10 @@ def _run(module, generator=False, extra=()):
            "-rfE", os.path.join(TESTS, module), *extra]
     res = subprocess.run(cmd, cwd=TESTS, env=env, capture_output=True, text=True, timeout=1800)
     tail = (res.stdout + res.stderr)[-4000:]
-    assert "paper_2508_16121_b200" in res.stdout, "drop-in not active:\n" + tail
     assert res.returncode == 0, tail
+    summary = [ln for ln in res.stdout.splitlines() if ln.startswith("[b200-dropin]")]
+    assert summary and "paper_2508_16121_b200" in summary[0], "drop-in not active:\n" + tail
+    assert "fused_enhance=" in summary[0] or "run_model=" in summary[0] or "reconstruct_lut=" in summary[0], tail
     return res.stdout
 
 
