@@ -39,6 +39,13 @@ def _stream(t):
     return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
 
 
+def _call(t, name, *args):
+    """C-ABI call with t's device current (the library launches on, and
+    creates texture objects for, the current device)."""
+    with torch.cuda.device(t.device):
+        _lib.call(name, *args)
+
+
 def _f32(t, name, ndim):
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
@@ -80,7 +87,7 @@ def reconstruct(u, s, vt):
         raise DimensionMismatch(f"inconsistent factor shapes {tuple(u.shape)} {tuple(s.shape)} "
                                 f"{tuple(vt.shape)}")
     planes = torch.empty((b, 3, 3, d, d), dtype=torch.float32, device=u.device)
-    _lib.call("svdlut_reconstruct", _p(u), _p(s), _p(vt), b, d, n, _p(planes), _stream(u))
+    _call(u, "svdlut_reconstruct", _p(u), _p(s), _p(vt), b, d, n, _p(planes), _stream(u))
     return planes
 
 
@@ -109,7 +116,7 @@ def pack_tables(lut_planes, lw, lb, grid_planes, gw, gb):
     lp, lw, lb, gp, gw, gb, b, d_t, k, d_s = _check_tables(lut_planes, lw, lb, grid_planes, gw, gb)
     nbytes = table_bytes(d_t, d_s)
     buf = torch.empty(b * nbytes // 4, dtype=torch.float32, device=lp.device)
-    _lib.call("svdlut_pack_tables", _p(lp), _p(lw), _p(lb), d_t, _p(gp), _p(gw), _p(gb), k, d_s,
+    _call(lp, "svdlut_pack_tables", _p(lp), _p(lw), _p(lb), d_t, _p(gp), _p(gw), _p(gb), k, d_s,
               b, _p(buf), _stream(lp))
     return PackedTables(buf, b, d_t, d_s)
 
@@ -131,7 +138,7 @@ def pack_tables_factors(u, s, vt, lw, lb, grid_planes, gw, gb):
         raise DimensionMismatch(f"{k} grids but weights shaped {tuple(gw.shape)} {tuple(gb.shape)}")
     nbytes = table_bytes(d, d_s)
     buf = torch.empty(b * nbytes // 4, dtype=torch.float32, device=u.device)
-    _lib.call("svdlut_pack_tables_factors", _p(u), _p(s), _p(vt), n, _p(lw), _p(lb), d, _p(gp),
+    _call(u, "svdlut_pack_tables_factors", _p(u), _p(s), _p(vt), n, _p(lw), _p(lb), d, _p(gp),
               _p(gw), _p(gb), k, d_s, b, _p(buf), _stream(u))
     return PackedTables(buf, b, d, d_s)
 
@@ -158,7 +165,7 @@ def apply(rgb, tables, out=None, y0=0, h_total=None, nonfinite=None):
         out = torch.empty_like(rgb)
     elif out.shape != rgb.shape or not out.is_contiguous() or out.dtype != torch.float32:
         raise DimensionMismatch("out must be a contiguous float32 tensor shaped like rgb")
-    _lib.call("svdlut_fused_fwd_packed_ex", _p(rgb), b, h, w, y0, h_total, _p(tables.buf),
+    _call(rgb, "svdlut_fused_fwd_packed_ex", _p(rgb), b, h, w, y0, h_total, _p(tables.buf),
               tables.d_t, tables.d_s, _p(out), _p(None), 0, _p(nonfinite), _stream(rgb))
     return out
 
@@ -208,7 +215,7 @@ def apply_io(x, tables, in_fmt="f32", out_fmt="f32", out=None, y0=0, h_total=Non
         out, bo, ho, wo = _io_image(out, fo, tables.batch)
         if (bo, ho, wo) != (b, h, w):
             raise DimensionMismatch("out does not match the input image size")
-    _lib.call("svdlut_fused_fwd_io", _p(x), fi, b, h, w, y0, h_total, _p(tables.buf), tables.d_t,
+    _call(x, "svdlut_fused_fwd_io", _p(x), fi, b, h, w, y0, h_total, _p(tables.buf), tables.d_t,
               tables.d_s, _p(out), fo, _p(nonfinite), _stream(x))
     return out
 
@@ -224,7 +231,7 @@ def slice_grids(rgb, grid_planes, gw, gb, y0=0, h_total=None):
     if gw.shape[1] != k or gb.shape[1] != k:
         raise DimensionMismatch(f"{k} grids but {gw.shape[1]} weight rows")
     fs = torch.empty((b, k, h, w), dtype=torch.float32, device=rgb.device)
-    _lib.call("svdlut_slice_grids", _p(rgb), b, h, w, y0, h if h_total is None else h_total, _p(gp),
+    _call(rgb, "svdlut_slice_grids", _p(rgb), b, h, w, y0, h if h_total is None else h_total, _p(gp),
               _p(gw), _p(gb), k, d_s, _p(fs), _stream(rgb))
     return fs
 
@@ -235,7 +242,7 @@ def apply_lut2d(rgb, lut_planes, lw, lb):
     rgb = _image(rgb, lp.shape[0])
     b, _, h, w = rgb.shape
     out = torch.empty_like(rgb)
-    _lib.call("svdlut_apply_lut2d", _p(rgb), b, h, w, _p(lp), _p(lw), _p(lb), lp.shape[3], _p(out),
+    _call(rgb, "svdlut_apply_lut2d", _p(rgb), b, h, w, _p(lp), _p(lw), _p(lb), lp.shape[3], _p(out),
               _stream(rgb))
     return out
 
@@ -248,7 +255,7 @@ def combine_slices(base, fs):
         raise DimensionMismatch("feature map size differs from image size")
     b, _, h, w = base.shape
     out = torch.empty_like(base)
-    _lib.call("svdlut_combine_slices", _p(base), _p(fs), b, h, w, fs.shape[1], _p(out),
+    _call(base, "svdlut_combine_slices", _p(base), _p(fs), b, h, w, fs.shape[1], _p(out),
               _stream(base))
     return out
 
@@ -259,7 +266,7 @@ def apply_lut3d(rgb, cubes):
     rgb = _image(rgb, cubes.shape[0])
     b, _, h, w = rgb.shape
     out = torch.empty_like(rgb)
-    _lib.call("svdlut_apply_lut3d", _p(rgb), b, h, w, _p(cubes), cubes.shape[2], _p(out),
+    _call(rgb, "svdlut_apply_lut3d", _p(rgb), b, h, w, _p(cubes), cubes.shape[2], _p(out),
               _stream(rgb))
     return out
 
@@ -272,7 +279,7 @@ def apply_exact(rgb, lut_planes, lw, lb, grid_planes, gw, gb, out=None, y0=0, h_
     h_total = h if h_total is None else h_total
     if out is None:
         out = torch.empty_like(rgb)
-    _lib.call("svdlut_fused_fwd_exact", _p(rgb), b, h, w, y0, h_total, _p(lp), _p(lw), _p(lb), d_t,
+    _call(rgb, "svdlut_fused_fwd_exact", _p(rgb), b, h, w, y0, h_total, _p(lp), _p(lw), _p(lb), d_t,
               _p(gp), _p(gw), _p(gb), k, d_s, _p(out), _stream(rgb))
     return out
 
@@ -292,7 +299,7 @@ def indices(rgb, d_t, d_s, y0=0, h_total=None):
     b, _, h, w = rgb.shape
     h_total = h if h_total is None else h_total
     idx = torch.empty((b, 8, h, w), dtype=torch.int32, device=rgb.device)
-    _lib.call("svdlut_indices", _p(rgb), b, h, w, y0, h_total, d_t, d_s, _p(idx), _stream(rgb))
+    _call(rgb, "svdlut_indices", _p(rgb), b, h, w, y0, h_total, d_t, d_s, _p(idx), _stream(rgb))
     return idx
 
 
@@ -313,7 +320,7 @@ def apply_l2(rgb, target, tables, gscale=None, y0=0, h_total=None):
     gy = torch.empty_like(rgb)
     loss = torch.empty(b, dtype=torch.float64, device=rgb.device)
     gmax = torch.empty(b, dtype=torch.float32, device=rgb.device)
-    _lib.call("svdlut_fused_fwd_l2", _p(rgb), _p(target), b, h, w, y0, h if h_total is None else h_total,
+    _call(rgb, "svdlut_fused_fwd_l2", _p(rgb), _p(target), b, h, w, y0, h if h_total is None else h_total,
               _p(tables.buf), tables.d_t, tables.d_s, _p(gy), _p(loss), _p(gmax),
               ctypes.c_float(gscale), _stream(rgb))
     return gy, loss, gmax
@@ -356,7 +363,7 @@ def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None,
         raise DimensionMismatch("gmax must be a float32 tensor with one entry per image")
     if gsumsq is not None and (gsumsq.dtype != torch.float64 or gsumsq.numel() != b or gmax is None):
         raise DimensionMismatch("gsumsq must be a float64 tensor with one entry per image (with gmax)")
-    _lib.call("svdlut_fused_bwd_packed", _p(rgb), _p(gy), b, h, w, y0, h_total,
+    _call(rgb, "svdlut_fused_bwd_packed", _p(rgb), _p(gy), b, h, w, y0, h_total,
               _p(tables.buf if tables is not None else None), _p(gmax), _p(gsumsq), _p(lp), _p(lw), d_t,
               _p(gp), _p(gw), k, d_s, _p(g["gx"]), _p(g["dlut_planes"]), _p(g["dlw"]),
               _p(g["dlb"]), _p(g["dgrid_planes"]), _p(g["dgw"]), _p(g["dgb"]), _p(ws), ws_bytes,
@@ -369,6 +376,6 @@ def reconstruct_backward(u, s, vt, dplanes):
     dplanes = _f32(dplanes, "dplanes", 5)
     b, _, _, d, n = u.shape
     du, ds, dvt = torch.empty_like(u), torch.empty_like(s), torch.empty_like(vt)
-    _lib.call("svdlut_reconstruct_bwd", _p(u), _p(s), _p(vt), _p(dplanes), b, d, n, _p(du),
+    _call(u, "svdlut_reconstruct_bwd", _p(u), _p(s), _p(vt), _p(dplanes), b, d, n, _p(du),
               _p(ds), _p(dvt), _stream(u))
     return du, ds, dvt

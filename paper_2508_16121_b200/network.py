@@ -260,17 +260,18 @@ class Generator:
         shape = tuple(int(v) for v in shape)
         x = torch.zeros(shape, dtype=torch.float32, device=self.device)
         out = torch.empty_like(x)
-        side = torch.cuda.Stream(self.device)
-        side.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(side):
-            for _ in range(2):  # allocations, kernel attributes, texture objects
+        with torch.cuda.device(self.device):  # capture on the generator's device
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):
+                for _ in range(2):  # allocations, kernel attributes, texture objects
+                    self.enhance(x, out=out)
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            # relaxed: the apply may create a texture object over the graph pool's
+            # table buffer while capturing (not a stream operation)
+            with torch.cuda.graph(graph, capture_error_mode="relaxed"):
                 self.enhance(x, out=out)
-        torch.cuda.current_stream(self.device).wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        # relaxed: the apply may create a texture object over the graph pool's
-        # table buffer while capturing (not a stream operation)
-        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
-            self.enhance(x, out=out)
 
         def run(rgb):
             if tuple(rgb.shape) != shape:

@@ -135,11 +135,14 @@ def fused_enhance(img, luts, lut_weights, grids, grid_weights, threads: int = 1,
               planes.shape[2], _ptr(gp), _ptr(gw), _ptr(gb), gp.shape[0], gp.shape[2], _ptr(out),
               int(bool(exact)), ctypes.byref(flag))
     cls = _image_type(img)
-    if not exact and issubclass(cls, _Image):
+    # the non-finite flag is only produced by the fast kernel; the exact kernel
+    # also serves dims beyond shared memory (svdlut_fast_supported)
+    fast = not exact and bool(_lib.load().svdlut_fast_supported(planes.shape[2], gp.shape[2]))
+    if fast and issubclass(cls, _Image):
         if flag.value:
             raise NonFiniteValue("image data contains a NaN or infinite entry")
         return cls._trusted(w, h, out)
-    return cls(w, h, out)  # exact mode / foreign Image type: the constructor validates
+    return cls(w, h, out)  # exact kernel / foreign Image type: the constructor validates
 
 
 def enhance_payload(payload, luts, lut_weights, grids, grid_weights, out_bits=None, out=None):

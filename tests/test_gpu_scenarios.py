@@ -106,3 +106,27 @@ def test_random_small_models_fused_vs_multistage(ops):
         naive = transform.naive_enhance(img, *_model(c, ct))
         worst = max(worst, float(np.abs(fused.data - naive.data).max()))
     assert worst <= 1e-5
+
+
+def test_graph_replay_after_wider_eager_launch(ops):
+    """a CUDA graph captured at 720x480, then an eager 4K launch of
+    the same kernel instantiation, then the graph replayed: the kernel's
+    dynamic shared-memory limit is set once to the maximum, so the replay
+    still launches and reproduces its first output bit for bit."""
+    import torch
+
+    from paper_2508_16121_b200 import device, network, synth
+
+    gen = network.Generator(network.random_init(0), device="cuda")
+    x = torch.from_numpy(np.random.default_rng(0).random((1, 3, 480, 720), dtype=np.float32)).cuda()
+    run = gen.graphed(x.shape)
+    first = run(x).clone()
+    case = synth.make_case(1)
+    t = {k: torch.from_numpy(np.ascontiguousarray(getattr(case, k))).cuda()
+         for k in ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")}
+    tables = device.pack_tables_factors(*(t[k] for k in ("u", "s", "vt", "lw", "lb", "grid_planes", "gw", "gb")))
+    device.apply(torch.from_numpy(case.rgb).cuda()[None], tables)  # eager, 3840 wide
+    torch.cuda.synchronize()
+    again = run(x)
+    torch.cuda.synchronize()
+    assert torch.equal(first, again)
