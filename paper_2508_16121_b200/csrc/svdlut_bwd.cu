@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       for (int e = threadIdx.x; e < nent; e += blockDim.x) {
         const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
         const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
+        SVDLUT_CHECK(jyp >= 0 && jyp <= ds - 2);
         S[e] = bgrid_entry(gsm, L, ch, jx, jc, jyp, eyp);
       }
     };
@@ -355,6 +356,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           const uint32_t sr = bbracket(qr, sdm1, sdm2, er);
           const uint32_t sg = bbracket(qg, sdm1, sdm2, eg);
           const uint32_t sb = bbracket(qb, sdm1, sdm2, eb);
+          SVDLUT_CHECK(br - kMagic <= (uint32_t)(dt - 2) && bg - kMagic <= (uint32_t)(dt - 2) &&
+                       bb - kMagic <= (uint32_t)(dt - 2) && jx >= 0 && jx <= ds - 2 &&
+                       sr - kMagic <= (uint32_t)(ds - 2) && sg - kMagic <= (uint32_t)(ds - 2) &&
+                       sb - kMagic <= (uint32_t)(ds - 2) && jy >= 0 && jy <= ds - 2);
           // ---- input gradient from the coefficient cells ----
           float gar = 0.f, gag = 0.f, gab = 0.f;
           // chunks {A0 A1 B0 B1} {C0 C1 D0 D1} {A2 C2 B2 D2} (svdlut_common.cuh):
@@ -401,6 +406,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
               const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
               int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
+              SVDLUT_CHECK(((pr * dt + ia + 1) * (dt + 1) + ibb + 1) * 3 + 2 < A.grid_off);
               // lane-rotated corner and channel order: lanes of one instruction
               // that share a cell hit up to 12 different words (distinct banks,
               // see AccLayout) instead of one address (ATOMS serializes them)

@@ -18,6 +18,21 @@
 
 namespace svdlut {
 
+// Debug builds (-DSVDLUT_BOUNDS_CHECK, tests/test_gpu_bounds.py) check every
+// table / slot / accumulator index the kernels form and trap on a violation;
+// release builds compile the checks away.  (compute-sanitizer is not
+// available on the GPU pool.)
+#ifdef SVDLUT_BOUNDS_CHECK
+#define SVDLUT_CHECK(cond)   \
+  do {                       \
+    if (!(cond)) __trap();   \
+  } while (0)
+#else
+#define SVDLUT_CHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
+
 constexpr int kMaxSmemBytes = 232448;       // sharedMemPerBlockOptin on B200 (measured)
 constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 

@@ -17,7 +17,9 @@ namespace svdlut {
 
 // interp.py:35-45 in f64 (p is an f32 sample promoted to f64).
 __device__ __forceinline__ void bracket_f64(double p, int d, int& i, double& delta) {
-  if (p < 0.0) {
+  // interp.py:37-40 (strict compares); a NaN, which the reference's Image
+  // rejects before any compute, is taken as 0 so the cell index stays in range
+  if (!(p >= 0.0)) {  // p < 0 or NaN
     p = 0.0;
   } else if (p > 1.0) {
     p = 1.0;

@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
       for (int e = warp * 32 + lane; e < nent; e += NW * 32) {
         const int jx = e / (3 * ds), rem = e - jx * 3 * ds;
         const int ch = rem / ds, jc = rem - ch * ds;
+        SVDLUT_CHECK(jx >= 0 && jx <= ds - 2 && jy >= 0 && jy <= ds - 2 && (int)(n % kRing) < kRing);
         S[e] = grid_slot(gsm, L, ds, ch, jx, jc, jy, ey);
       }
       __syncwarp();
@@ -331,6 +332,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
       // ---- this warp's chunks of row y ----
       while (cy == y && in_seg(cy, ck)) {
         const int xl = ck * kChunk + kPx * lane;
+        SVDLUT_CHECK(cy >= 0 && cy < p.h && ck >= 0 && ck < cpr);
         int ny = cy, nk = ck + NW;  // this warp's next chunk
         while (nk >= cpr) {
           nk -= cpr;
@@ -391,6 +393,12 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
             tex_issue(2, tq, 0u);
           }
           const uint32_t br = bits(mcr[u >> 1], u), bg = bits(mcg[u >> 1], u), bb = bits(mcb[u >> 1], u);
+          SVDLUT_CHECK(br - kMagicBits <= (uint32_t)(dt - 2) && bg - kMagicBits <= (uint32_t)(dt - 2) &&
+                       bb - kMagicBits <= (uint32_t)(dt - 2));
+          SVDLUT_CHECK(bits(mx[u >> 1], u) - kMagicBits <= (uint32_t)(ds - 2) &&
+                       bits(msr[u >> 1], u) - kMagicBits <= (uint32_t)(ds - 1) &&
+                       bits(msg[u >> 1], u) - kMagicBits <= (uint32_t)(ds - 1) &&
+                       bits(msb[u >> 1], u) - kMagicBits <= (uint32_t)(ds - 1));
           const float a_r = lo(dr[u >> 1], u), a_g = lo(dg[u >> 1], u), a_b = lo(db[u >> 1], u);
           // shared-memory planes
           float4 c[9];

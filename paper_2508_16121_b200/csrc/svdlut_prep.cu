@@ -136,6 +136,7 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
         q[3] = (p11 - p10) - (p01 - p00);      // D
       }
       const int cell = i * L.cst + j;
+      SVDLUT_CHECK(i < dt - 1 && j < L.cst && cell < L.plane_floats / 4);
       P0[(sA >> 2) * L.plane_floats + cell * 4 + (sA & 3)] = (float)q[0];
       P0[(sB >> 2) * L.plane_floats + cell * 4 + (sB & 3)] = (float)q[1];
       P0[(sC >> 2) * L.plane_floats + cell * 4 + (sC & 3)] = (float)q[2];
