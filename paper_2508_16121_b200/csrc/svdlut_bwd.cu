@@ -134,19 +134,6 @@ __device__ __forceinline__ int to_fixed(float v, float S) {
   return __float_as_int(__fmaf_rn(v, S, 12582912.0f)) - 0x4B400000;
 }
 
-// Direct flush of one lane's closed xc/yc run (divergent: only lanes whose
-// guide cell changed mid-chunk come here).
-__device__ __forceinline__ void grid_flush(int key, const float (&v)[8], int c, int jy, int ds,
-                                           float S, int* E_xc, int* E_yc) {
-  const int jx = key >> 8, jc = key & 0xff;
-  int* xc = E_xc + c * ds * ds + jx * ds + jc;
-  atomicAdd(xc, to_fixed(v[0], S)); atomicAdd(xc + ds, to_fixed(v[1], S));
-  atomicAdd(xc + 1, to_fixed(v[2], S)); atomicAdd(xc + ds + 1, to_fixed(v[3], S));
-  int* yc = E_yc + c * ds * ds + jy * ds + jc;
-  atomicAdd(yc, to_fixed(v[4], S)); atomicAdd(yc + ds, to_fixed(v[5], S));
-  atomicAdd(yc + 1, to_fixed(v[6], S)); atomicAdd(yc + ds + 1, to_fixed(v[7], S));
-}
-
 // Merged grid coefficients of channel c at (row jy/ey, x-cell jx, guide cell
 // jc) from the grid block `gsm` (xc first, svdlut_common.cuh).
 __device__ __forceinline__ float4 bgrid_entry(const float* gsm, const TableLayout& L, int c, int jx,
@@ -203,7 +190,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
   const int rc0 = lane % 3, rc1 = (lane + 1) % 3, rc2 = (lane + 2) % 3;  // lane's channel order
-  const int rt = (lane / 3) & 3;                                           // lane's corner order
 
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1) : "memory");
@@ -228,6 +214,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
   const uint32_t slotK0 = bsmem_addr(slots) - kMagic * 16u;
   int* Ei = reinterpret_cast<int*>(Es);
+  int* Rrow = Ei + A.total;  // 2 rows x [Rx 3*ds | Rc 3*ds]
   int* E_lut = Ei + A.lut_off;
   int* E_xy = Ei + A.grid_off;
   int* E_xc = E_xy + 3 * ds * ds;
@@ -264,7 +251,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       copy(sbase, reinterpret_cast<const char*>(tb + L.plane_off(1, 0)), 3u * plane_bytes);
       copy(sbase + 3u * plane_bytes, reinterpret_cast<const char*>(tb + L.xc_off), grid_bytes);
     }
-    for (int i = threadIdx.x; i < A.total; i += blockDim.x) Ei[i] = 0;
+    for (int i = threadIdx.x; i < A.total + 12 * ds; i += blockDim.x) Ei[i] = 0;
     float gm = p.gmax[b];
     if (p.gss) gm = fminf(gm, kOutlierSigmas * (float)sqrt(p.gss[b] / (3.0 * (double)pl)));
     const float S = gm > 0.f ? kFixedOne / gm : 1.0f;  // fixed-point scale of this image
@@ -319,20 +306,40 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // ~10 lanes on the same address, which ATOMS serializes (measured cost:
       // max lanes per bank, same-address lanes not merged).
       const int slots4 = (p.w + 3) >> 2;
+      // per-row guide / x-vertex sums of this row (fixed point, parity buffer):
+      //   Rx[c][vx] = sum g_c wx   (xy plane: folded with wy(b) at the row's end)
+      //   Rc[c][vc] = sum g_c wc   (yc plane: likewise)
+      int* Rx = Rrow + (y & 1) * 6 * ds;
+      int* Rc = Rx + 3 * ds;
       for (int s0 = 0; s0 < slots4; s0 += kBwdWarps * 32) {
         const int xl = 4 * (s0 + lane * kBwdWarps + warp);
         if (xl >= p.w) continue;
         BChunk cur;
         bload_chunk(X, GY, pl, y, xl - 4 * lane, p.w, lane, vec, cur);
         float oxr[kBPx], oxg[kBPx], oxb[kBPx];
-        // xy accumulators of this lane for the x-cell of its first pixel
-        float exy = 0.f;
-        const int jx_first = (int)(col_bracket(min(xl, p.w - 1), p.rcp_w, sdm1, sdm2, exy) - kMagic);
-        float axy[12];
+        // lane-local runs: xc (4) + yc (2) sums per channel keyed by (x-cell,
+        // guide cell); xy (2) sums per channel keyed by the x-cell
+        int run_key[3] = {-1, -1, -1};
+        float rxc[3][4] = {}, ryc[3][2] = {};
+        int xkey = -1;
+        float rxy[3][2] = {};
+        auto flush_run = [&](int c) {
+          const int jx = run_key[c] >> 8, jc = run_key[c] & 0xff;
+          int* xc = E_xc + c * ds * ds + jx * ds + jc;
+          atomicAdd(xc, to_fixed(rxc[c][0], S));
+          atomicAdd(xc + ds, to_fixed(rxc[c][1], S));
+          atomicAdd(xc + 1, to_fixed(rxc[c][2], S));
+          atomicAdd(xc + ds + 1, to_fixed(rxc[c][3], S));
+          atomicAdd(Rc + c * ds + jc, to_fixed(ryc[c][0], S));
+          atomicAdd(Rc + c * ds + jc + 1, to_fixed(ryc[c][1], S));
+        };
+        auto flush_xy = [&]() {
 #pragma unroll
-        for (int i = 0; i < 12; ++i) axy[i] = 0.f;
-        int run_key[3] = {-1, -1, -1};  // open xc/yc run per channel
-        float run[3][8];
+          for (int c = 0; c < 3; ++c) {
+            atomicAdd(Rx + c * ds + xkey, to_fixed(rxy[c][0], S));
+            atomicAdd(Rx + c * ds + xkey + 1, to_fixed(rxy[c][1], S));
+          }
+        };
 #pragma unroll
         for (int u = 0; u < kBPx; ++u) {
           const bool valid = xl + u < p.w;
@@ -395,30 +402,35 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           oxg[u] = (Xg < 0.f || Xg > 1.f) ? 0.f : __fmaf_rn(gag, tdm1, gsg * sdm1);
           oxb[u] = (Xb < 0.f || Xb > 1.f) ? 0.f : __fmaf_rn(gab, tdm1, gsb * sdm1);
 
-          // ---- scatter: LUT pairs, one fixed-point atomic per value ----
+          // ---- scatter: LUT pairs, one fixed-point atomic per (corner, channel) ----
+          // The lane writes channel (k + lane % 3) % 3 at its k-th atomic of a
+          // corner, so lanes of one instruction that share a cell hit three
+          // different words; corner offsets are immediates (AccLayout).
           if (valid) {
+            const float fs[3] = {f0 * S, f1 * S, f2 * S};
+            const float s0v = fs[rc0 == 0 ? 0 : rc0 == 1 ? 1 : 2];
+            const float s1v = rc1 == 0 ? fs[0] : rc1 == 1 ? fs[1] : fs[2];
+            const float s2v = rc2 == 0 ? fs[0] : rc2 == 1 ? fs[1] : fs[2];
             const int ir = (int)(br - kMagic), ig = (int)(bg - kMagic), ib = (int)(bb - kMagic);
-            const float q0 = rc0 == 0 ? f0 : (rc0 == 1 ? f1 : f2);  // gY in this lane's channel order
-            const float q1 = rc1 == 0 ? f0 : (rc1 == 1 ? f1 : f2);
-            const float q2 = rc2 == 0 ? f0 : (rc2 == 1 ? f1 : f2);
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
               const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
               const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
               int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
               SVDLUT_CHECK(((pr * dt + ia + 1) * (dt + 1) + ibb + 1) * 3 + 2 < A.grid_off);
-              // lane-rotated corner and channel order: lanes of one instruction
-              // that share a cell hit up to 12 different words (distinct banks,
-              // see AccLayout) instead of one address (ATOMS serializes them)
               const float ea = 1.f - da, eb = 1.f - dbb;
+              const float w[4] = {ea * eb, da * eb, ea * dbb, da * dbb};  // corners (0,0) (1,0) (0,1) (1,1)
+              int* e0 = e + rc0;
+              int* e1 = e + rc1;
+              int* e2 = e + rc2;
 #pragma unroll
-              for (int jslot = 0; jslot < 4; ++jslot) {
-                const int kc = (jslot + rt) & 3;  // corner (a, b) = (kc & 1, kc >> 1)
-                const float wgt = ((kc & 1) ? da : ea) * ((kc & 2) ? dbb : eb);
-                int* ec = e + ((kc & 1) ? (dt + 1) * 3 : 0) + ((kc & 2) ? 3 : 0);
-                atomicAdd(ec + rc0, to_fixed(q0 * wgt, S));
-                atomicAdd(ec + rc1, to_fixed(q1 * wgt, S));
-                atomicAdd(ec + rc2, to_fixed(q2 * wgt, S));
+              for (int q = 0; q < 4; ++q) {
+                const int off = ((q & 1) ? (dt + 1) * 3 : 0) + ((q & 2) ? 3 : 0);
+                const float2 v01 = __ffma2_rn(make_float2(s0v, s1v), make_float2(w[q], w[q]),
+                                              make_float2(12582912.0f, 12582912.0f));
+                atomicAdd(e0 + off, __float_as_int(v01.x) - 0x4B400000);
+                atomicAdd(e1 + off, __float_as_int(v01.y) - 0x4B400000);
+                atomicAdd(e2 + off, __float_as_int(__fmaf_rn(s2v, w[q], 12582912.0f)) - 0x4B400000);
               }
             }
           }
@@ -459,64 +471,44 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               atomicAdd(yc + ds + 1, gg[c] * ey * ecs[c]);
             }
           }
-          // ---- grids: xc + yc runs per channel (key = guide cell; x-cell checked) ----
+          // ---- grids: runs per channel (x-cell, guide cell) and per x-cell ----
+          if (valid) {
+            if (jx != xkey) {
+              if (xkey >= 0) flush_xy();
+              xkey = jx;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const float gc = c == 0 ? f0 : (c == 1 ? f1 : f2);
-            const int jc = (int)((c == 0 ? sr : (c == 1 ? sg : sb)) - kMagic);
-            const float ec = c == 0 ? er : (c == 1 ? eg : eb);
-            const int key = valid ? (jx << 8) | jc : -1;
-            if (key != run_key[c]) {
-              if (run_key[c] >= 0) grid_flush(run_key[c], run[c], c, jy, ds, S, E_xc, E_yc);
-              run_key[c] = key;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) run[c][i] = 0.f;
+              for (int c = 0; c < 3; ++c) rxy[c][0] = rxy[c][1] = 0.f;
             }
-            if (valid) {
-              run[c][0] += gc * (1.f - ex) * (1.f - ec);
-              run[c][1] += gc * ex * (1.f - ec);
-              run[c][2] += gc * (1.f - ex) * ec;
-              run[c][3] += gc * ex * ec;
-              run[c][4] += gc * (1.f - ey) * (1.f - ec);
-              run[c][5] += gc * ey * (1.f - ec);
-              run[c][6] += gc * (1.f - ey) * ec;
-              run[c][7] += gc * ey * ec;
-            }
-          }
-          // ---- xy: summed in registers for the lane's first x-cell ----
-          {
-            const float w00 = (1.f - ex) * (1.f - ey), w10 = ex * (1.f - ey);
-            const float w01 = (1.f - ex) * ey, w11 = ex * ey;
-            if (jx == jx_first) {
-              axy[0] += f0 * w00; axy[1] += f1 * w00; axy[2] += f2 * w00;
-              axy[3] += f0 * w10; axy[4] += f1 * w10; axy[5] += f2 * w10;
-              axy[6] += f0 * w01; axy[7] += f1 * w01; axy[8] += f2 * w01;
-              axy[9] += f0 * w11; axy[10] += f1 * w11; axy[11] += f2 * w11;
-            } else if (valid) {  // the lane's pixels straddle an x-cell boundary
-              const float gg[3] = {f0, f1, f2};
 #pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                int* e = E_xy + c * ds * ds + jx * ds + jy;
-                atomicAdd(e, to_fixed(gg[c] * w00, S)); atomicAdd(e + ds, to_fixed(gg[c] * w10, S));
-                atomicAdd(e + 1, to_fixed(gg[c] * w01, S)); atomicAdd(e + ds + 1, to_fixed(gg[c] * w11, S));
+            for (int c = 0; c < 3; ++c) {
+              const float gc = c == 0 ? f0 : (c == 1 ? f1 : f2);
+              const int jc = (int)((c == 0 ? sr : (c == 1 ? sg : sb)) - kMagic);
+              const float ec = c == 0 ? er : (c == 1 ? eg : eb);
+              const int key = (jx << 8) | jc;
+              if (key != run_key[c]) {
+                if (run_key[c] >= 0) flush_run(c);
+                run_key[c] = key;
+                rxc[c][0] = rxc[c][1] = rxc[c][2] = rxc[c][3] = 0.f;
+                ryc[c][0] = ryc[c][1] = 0.f;
               }
+              const float gx1 = gc * ex, gx0 = gc - gx1;  // g (1 - ex), g ex
+              const float gc1 = gc * ec;
+              rxc[c][0] = __fmaf_rn(-gx0, ec, rxc[c][0] + gx0);  // g (1-ex)(1-ec)
+              rxc[c][1] = __fmaf_rn(-gx1, ec, rxc[c][1] + gx1);  // g ex (1-ec)
+              rxc[c][2] = __fmaf_rn(gx0, ec, rxc[c][2]);         // g (1-ex) ec
+              rxc[c][3] = __fmaf_rn(gx1, ec, rxc[c][3]);         // g ex ec
+              ryc[c][0] += gc - gc1;
+              ryc[c][1] += gc1;
+              rxy[c][0] += gx0;
+              rxy[c][1] += gx1;
             }
           }
         }
-        // ---- end of the lane's 4 pixels: open grid runs and the xy sums ----
+        // ---- end of the lane's 4 pixels: open runs ----
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-          if (run_key[c] >= 0) grid_flush(run_key[c], run[c], c, jy, ds, S, E_xc, E_yc);
-        {
-          int* e = E_xy + jx_first * ds + jy;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            atomicAdd(e + c * ds * ds, to_fixed(axy[c], S));
-            atomicAdd(e + c * ds * ds + ds, to_fixed(axy[3 + c], S));
-            atomicAdd(e + c * ds * ds + 1, to_fixed(axy[6 + c], S));
-            atomicAdd(e + c * ds * ds + ds + 1, to_fixed(axy[9 + c], S));
-          }
-        }
+          if (run_key[c] >= 0) flush_run(c);
+        if (xkey >= 0) flush_xy();
         if (GX) {
           const long long ro = (long long)y * p.w;
           if (vec && xl + 4 <= p.w) {
@@ -537,7 +529,22 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       px_since_flush += p.w;
       if (y < y_last) produce_rows(y + 1);  // the other half of the ring
       __syncthreads();
+      // fold this row's Rx / Rc into the xy / yc planes with wy(b) of row y
+      // and zero them (rows y + 1 use the other buffer)
+      for (int i = threadIdx.x; i < 6 * ds; i += blockDim.x) {
+        const int v = Rx[i];
+        if (v != 0) {
+          const bool isx = i < 3 * ds;
+          const int c = (isx ? i : i - 3 * ds) / ds, t = (isx ? i : i - 3 * ds) - c * ds;
+          int* e = isx ? E_xy + (c * ds + t) * ds + jy : E_yc + (c * ds + jy) * ds + t;
+          const float fv = (float)v;
+          atomicAdd(e, __float2int_rn(fv * (1.f - ey)));
+          atomicAdd(e + (isx ? 1 : ds), __float2int_rn(fv * ey));
+          Rx[i] = 0;
+        }
+      }
       if (px_since_flush + p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
+        __syncthreads();  // the fold has landed
         for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
           const int v = Ei[i];
           if (v != 0) {
@@ -664,7 +671,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
   const size_t staged = (size_t)3 * L.plane_floats * 4 + (size_t)L.grid_floats() * 4;
-  const size_t smem = staged + 2 * (size_t)nent * 16 + (size_t)A.total * 4;
+  const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds) * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
   float* tables = (float*)wp;
