@@ -139,14 +139,14 @@ __device__ __forceinline__ int to_fixed(float v, float S) {
 __device__ __forceinline__ float4 bgrid_entry(const float* gsm, const TableLayout& L, int c, int jx,
                                               int jc, int jy, float ey) {
   const int ds = L.ds;
-  const float4 x = reinterpret_cast<const float4*>(gsm)[(c * (ds - 1) + jx) * (ds - 1) + jc];
+  const float4 x = __ldg(reinterpret_cast<const float4*>(gsm) + (c * (ds - 1) + jx) * (ds - 1) + jc);
   const float* Y = gsm + (L.gyc_off - L.xc_off) + c * ds * ds;
-  const float y00 = Y[jy * ds + jc], y01 = Y[jy * ds + jc + 1];
-  const float y10 = Y[(jy + 1) * ds + jc], y11 = Y[(jy + 1) * ds + jc + 1];
+  const float y00 = __ldg(Y + jy * ds + jc), y01 = __ldg(Y + jy * ds + jc + 1);
+  const float y10 = __ldg(Y + (jy + 1) * ds + jc), y11 = __ldg(Y + (jy + 1) * ds + jc + 1);
   const float q0 = __fmaf_rn(ey, y10 - y00, y00), q1 = __fmaf_rn(ey, y11 - y01, y01);
   const float* X = gsm + (L.gxy_off - L.xc_off);
-  const float v00 = X[(jx * ds + jy) * 3 + c], v01 = X[(jx * ds + jy + 1) * 3 + c];
-  const float v10 = X[((jx + 1) * ds + jy) * 3 + c], v11 = X[((jx + 1) * ds + jy + 1) * 3 + c];
+  const float v00 = __ldg(X + (jx * ds + jy) * 3 + c), v01 = __ldg(X + (jx * ds + jy + 1) * 3 + c);
+  const float v10 = __ldg(X + ((jx + 1) * ds + jy) * 3 + c), v11 = __ldg(X + ((jx + 1) * ds + jy + 1) * 3 + c);
   const float r0 = __fmaf_rn(ey, v01 - v00, v00), r1 = __fmaf_rn(ey, v11 - v10, v10);
   return make_float4(x.x + q0 + r0, x.z + (q1 - q0), x.y + (r1 - r0), x.w);  // {M, M', N, N'}
 }
@@ -197,9 +197,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   }
   // staged: pair rb's three chunk planes, then the grid block
   const uint32_t plane_bytes = (uint32_t)L.plane_floats * 4u;
-  const uint32_t grid_bytes = (uint32_t)L.grid_floats() * 4u;
-  const uint32_t table_bytes = 3u * plane_bytes + grid_bytes;
-  const float* gsm = smem + 3 * L.plane_floats;  // grid block
+  const uint32_t table_bytes = 6u * plane_bytes;  // pairs rg and rb (contiguous in the table)
   const int nent = (ds - 1) * 3 * (ds - 1);
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
   float* Es = reinterpret_cast<float*>(slots + 2 * nent);  // A.total floats
@@ -207,7 +205,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
   const uint32_t cst = (uint32_t)L.cst, cst16 = cst * 16u;
   const uint32_t ptex = (uint32_t)L.plane_floats / 4u;  // texels per plane
-  // smem address of pair rb's cell (bits_r, bits_b), chunk k: lutK + br*cst16 + bb*16 + k*plane_bytes
+  // smem address of pair rg / rb cell (bits_a, bits_b), chunk k: lutK + ba*cst16 + bb*16 + k*plane_bytes
+  // (+ 3 planes for rb)
   const uint32_t lutK = sbase - kMagic * (cst16 + 16u);
   const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;
   const uint32_t jx_bytes = 3u * chan_bytes;
@@ -248,8 +247,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               "l"(from + off), "r"(min(32768u, bytes - off)), "r"(bar)
               : "memory");
       };
-      copy(sbase, reinterpret_cast<const char*>(tb + L.plane_off(1, 0)), 3u * plane_bytes);
-      copy(sbase + 3u * plane_bytes, reinterpret_cast<const char*>(tb + L.xc_off), grid_bytes);
+      copy(sbase, reinterpret_cast<const char*>(tb + L.plane_off(0, 0)), 6u * plane_bytes);
     }
     for (int i = threadIdx.x; i < A.total + 12 * ds; i += blockDim.x) Ei[i] = 0;
     float gm = p.gmax[b];
@@ -263,6 +261,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     const float* GY = p.gy + (long long)b * 3 * pl;
     float* GX = p.gx ? p.gx + (long long)b * 3 * pl : nullptr;
     // texel of cell (bits_a, bits_b), chunk k of pair rg / gb: tex* + bits_a*cst + bits_b + k*ptex
+    const float* gsm = tb + L.xc_off;  // grid block (global, L1-cached; read by the slot production)
     const uint32_t texKrg = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
                             (uint32_t)(L.plane_off(0, 0) / 4) - kMagic * (cst + 1u);
     const uint32_t texK = texKrg + 6u * ptex;  // pair gb
@@ -372,14 +371,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // chunks {A0 A1 B0 B1} {C0 C1 D0 D1} {A2 C2 B2 D2} (svdlut_common.cuh):
           // d/da = B + D b, d/db = C + D a per channel
           {
-            const int ti = (int)(br * cst + bg + texKrg);  // rg via the texture path
-            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + (int)ptex),
-                         c2 = tex1Dfetch<float4>(p.tex, ti + 2 * (int)ptex);
+            const uint32_t a = br * cst16 + bg * 16u + lutK;  // rg (shared memory)
+            const float4 c0 = blds4(a), c1 = blds4(a + plane_bytes), c2 = blds4(a + 2u * plane_bytes);
             gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.z);
             gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            const uint32_t a = br * cst16 + bb * 16u + lutK;  // rb (shared memory)
+            const uint32_t a = br * cst16 + bb * 16u + lutK + 3u * plane_bytes;  // rb (shared memory)
             const float4 c0 = blds4(a), c1 = blds4(a + plane_bytes), c2 = blds4(a + 2u * plane_bytes);
             gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
@@ -670,7 +668,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
-  const size_t staged = (size_t)3 * L.plane_floats * 4 + (size_t)L.grid_floats() * 4;
+  const size_t staged = (size_t)6 * L.plane_floats * 4;
   const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds) * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
