@@ -41,7 +41,10 @@ namespace svdlut {
 constexpr int kFwdWarps = FWD_NW;
 constexpr int kPx = 4;                 // consecutive pixels per lane
 constexpr int kChunk = 32 * kPx;       // pixels per warp chunk
-constexpr int kRing = 3;               // per-row grid slot buffers (4: the smem carve-out steps up)
+#ifndef FWD_RING
+#define FWD_RING 3
+#endif
+constexpr int kRing = FWD_RING;        // per-row grid slot buffers
 constexpr int kAhead = kRing - 1;      // rows of slots produced ahead of the one consumed
 #ifndef FWD_L2ROWS
 #define FWD_L2ROWS 2
