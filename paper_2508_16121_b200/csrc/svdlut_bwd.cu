@@ -208,6 +208,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   // smem address of pair rg / rb cell (bits_a, bits_b), chunk k: lutK + ba*cst16 + bb*16 + k*plane_bytes
   // (+ 3 planes for rb)
   const uint32_t lutK = sbase - kMagic * (cst16 + 16u);
+  const uint32_t tiles = (uint32_t)L.tiles();
+  // the same for a 4x4-tiled plane: lutT + tiled(bits_a, bits_b) * 16
+  const uint32_t lutT = sbase - (((kMagic >> 2) * tiles + (kMagic >> 2)) << 8);
   const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;
   const uint32_t jx_bytes = 3u * chan_bytes;
   const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
@@ -262,9 +265,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     float* GX = p.gx ? p.gx + (long long)b * 3 * pl : nullptr;
     // texel of cell (bits_a, bits_b), chunk k of pair rg / gb: tex* + bits_a*cst + bits_b + k*ptex
     const float* gsm = tb + L.xc_off;  // grid block (global, L1-cached; read by the slot production)
-    const uint32_t texKrg = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
-                            (uint32_t)(L.plane_off(0, 0) / 4) - kMagic * (cst + 1u);
-    const uint32_t texK = texKrg + 6u * ptex;  // pair gb
+    const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
+                          (uint32_t)(L.plane_off(2, 0) / 4) - (((kMagic >> 2) * tiles + (kMagic >> 2)) << 4);  // pair gb
+    const uint32_t texKr = texK + (((kMagic >> 2) * tiles + (kMagic >> 2)) << 4) - kMagic * (cst + 1u);
     asm volatile(
         "{\n.reg .pred p;\nWAITB_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAITB_%=;\n}\n" ::"r"(bar),
         "r"(phase)
@@ -372,20 +375,30 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // d/da = B + D b, d/db = C + D a per channel
           {
             const uint32_t a = br * cst16 + bg * 16u + lutK;  // rg (shared memory)
-            const float4 c0 = blds4(a), c1 = blds4(a + plane_bytes), c2 = blds4(a + 2u * plane_bytes);
+            const uint32_t at = ((((br >> 2) * tiles + (bg >> 2)) << 4) + ((br & 3u) << 2) + (bg & 3u)) * 16u + lutT;
+            const float4 c0 = blds4(plane_tiled(0) ? at : a);
+            const float4 c1 = blds4((plane_tiled(1) ? at : a) + plane_bytes);
+            const float4 c2 = blds4((plane_tiled(2) ? at : a) + 2u * plane_bytes);
             gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.z);
             gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            const uint32_t a = br * cst16 + bb * 16u + lutK + 3u * plane_bytes;  // rb (shared memory)
-            const float4 c0 = blds4(a), c1 = blds4(a + plane_bytes), c2 = blds4(a + 2u * plane_bytes);
+            // rb (shared memory); a plane may be stored in 4x4 tiles (svdlut_common.cuh)
+            const uint32_t a = br * cst16 + bb * 16u + lutK;
+            const uint32_t at = ((((br >> 2) * tiles + (bb >> 2)) << 4) + ((br & 3u) << 2) + (bb & 3u)) * 16u + lutT;
+            const float4 c0 = blds4((plane_tiled(3) ? at : a) + 3u * plane_bytes);
+            const float4 c1 = blds4((plane_tiled(4) ? at : a) + 4u * plane_bytes);
+            const float4 c2 = blds4((plane_tiled(5) ? at : a) + 5u * plane_bytes);
             gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            const int ti = (int)(bg * cst + bb + texK);  // gb via the texture path
-            const float4 c0 = tex1Dfetch<float4>(p.tex, ti), c1 = tex1Dfetch<float4>(p.tex, ti + (int)ptex),
-                         c2 = tex1Dfetch<float4>(p.tex, ti + 2 * (int)ptex);
+            // gb via the texture path (row-stride or 4x4-tiled cells, svdlut_common.cuh)
+            const uint32_t tt = (((bg >> 2) * tiles + (bb >> 2)) << 4) + ((bg & 3u) << 2) + (bb & 3u) + texK;
+            const uint32_t tr = bg * cst + bb + texKr;
+            const float4 c0 = tex1Dfetch<float4>(p.tex, (int)(plane_tiled(6) ? tt : tr)),
+                         c1 = tex1Dfetch<float4>(p.tex, (int)((plane_tiled(7) ? tt : tr) + ptex)),
+                         c2 = tex1Dfetch<float4>(p.tex, (int)((plane_tiled(8) ? tt : tr) + 2u * ptex));
             gag += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dg, c1.x) + g1 * __fmaf_rn(c1.w, dg, c1.y) + g2 * __fmaf_rn(c2.w, dg, c2.y);
           }

@@ -45,10 +45,14 @@ constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 //     k = 0  {A0 A1 B0 B1}     channels 0/1 as float2 pairs for FFMA2
 //     k = 1  {C0 C1 D0 D1}
 //     k = 2  {A2 C2 B2 D2}     so {A2 + B2 a, C2 + D2 a} is one FFMA2
-// Each plane is (dt-1) cell rows x cst cell columns, cst >= dt-1 (cst % 8 ==
-// 3): cell (i, j) at index i*cst + j.  With cst % 8 == 3 the 3x3 cell
-// neighbourhood a run of pixels touches maps to distinct 16-byte bank groups
-// except the two opposite diagonals.
+// Planes gathered from shared memory store cell (i, j) at index i*cst + j,
+// cst >= dt-1 with cst % 8 == 3: the 3x3 cell neighbourhood a run of pixels
+// touches maps to distinct 16-byte bank groups except the two opposite
+// diagonals.  Planes gathered through the texture path (kTiledPlanes: pair
+// gb and chunk 1 of pair rb) store their cells in 4x4 tiles, index
+// ((i/4)*T + j/4)*16 + (i%4)*4 + j%4 with T = ceil((dt-1)/4): the cells a
+// warp's pixels touch then share a few 128-byte cache lines (a texture gather
+// costs a cycle per distinct line beyond four).
 //
 // Grid block (K grids merged per output channel c: grid k feeds output and
 // guide channel k%3, transform.py:269-297):
@@ -60,10 +64,16 @@ constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 // The fused kernel interpolates xy / yc along y once per row into merged
 // per-(row, jx, c, jc) slots {M, M', N, N'} (term M + N ex + (M' + N' ex) ec).
 __host__ __device__ constexpr int cst_for(int dt) { return (dt - 1) + ((3 - (dt - 1)) & 7); }
+// chunk planes (bit 3*pair + chunk) stored in the 4x4-tiled cell order
+#ifndef SVDLUT_TILED_PLANES
+#define SVDLUT_TILED_PLANES 0x1D0u
+#endif
+constexpr unsigned kTiledPlanes = SVDLUT_TILED_PLANES;  // rb chunk 1, gb chunks 0-2
+__host__ __device__ constexpr bool plane_tiled(int idx) { return (kTiledPlanes >> idx) & 1u; }
 
 struct TableLayout {
   int dt, ds, cst;
-  int plane_floats;                  // one LUT float4 plane: (dt-1) * cst * 4
+  int plane_floats;                  // one LUT float4 plane (the larger of the two cell orders)
   int lut_off;                       // 9 planes [pair][chunk]
   int xc_off, gxy_off, gyc_off;      // grid block
   int total_floats;                  // rounded up to 32 floats (128 B)
@@ -72,7 +82,8 @@ struct TableLayout {
     L.dt = dt;
     L.ds = ds;
     L.cst = cst_for(dt);
-    L.plane_floats = (dt - 1) * L.cst * 4;
+    const int T = (dt + 2) / 4;  // ceil((dt-1)/4) tiles per side
+    L.plane_floats = ((dt - 1) * L.cst > T * T * 16 ? (dt - 1) * L.cst : T * T * 16) * 4;
     L.lut_off = 0;
     L.xc_off = L.lut_off + 9 * L.plane_floats;
     L.gxy_off = L.xc_off + 3 * (ds - 1) * (ds - 1) * 4;
@@ -81,6 +92,11 @@ struct TableLayout {
     return L;
   }
   __host__ __device__ int plane_off(int p, int k) const { return lut_off + (3 * p + k) * plane_floats; }
+  __host__ __device__ int tiles() const { return (dt + 2) / 4; }
+  // cell (i, j) within chunk plane idx = 3*pair + chunk (in float4 units)
+  __host__ __device__ int cell_index(int idx, int i, int j) const {
+    return !plane_tiled(idx) ? i * cst + j : ((i >> 2) * tiles() + (j >> 2)) * 16 + ((i & 3) << 2) + (j & 3);
+  }
   __host__ __device__ size_t bytes() const { return (size_t)total_floats * 4; }
   __host__ __device__ int grid_floats() const { return total_floats - xc_off; }
   // merged grid slots of one row: [jx ds-1][c 3][jc ds] float4, the last jc

@@ -35,8 +35,8 @@ namespace svdlut {
 #endif
 #ifndef FWD_PLANES
 // LUT chunk planes staged in shared memory (bit 3*pair + chunk; pairs rg, rb,
-// gb); the others go through the texture path
-#define FWD_PLANES 0x3F
+// gb); the others (chunk 1 of rb, pair gb) go through the texture path
+#define FWD_PLANES 0x2F
 #endif
 constexpr int kFwdWarps = FWD_NW;
 constexpr int kPx = 4;                 // consecutive pixels per lane
@@ -284,6 +284,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
     const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) -
                           kMagicBits * (cst + 1u);
     const uint32_t ptex = (uint32_t)L.plane_floats / 4u;  // texels per plane
+    const uint32_t tiles = (uint32_t)L.tiles();
+    // tiled index of the biased bits minus the row-stride bias already in texK
+    const uint32_t texT = kMagicBits * (cst + 1u) - (((kMagicBits >> 2) * tiles + (kMagicBits >> 2)) << 4);
 
     // this warp's chunks: global chunk g_seg + warp + NW*i (< g_img_end), as
     // (row cy, chunk ck) advanced in 32-bit
@@ -375,15 +378,21 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
 
         // texture-path planes of pixel u: issued one pixel ahead
         float4 tq[9];
+        // cell index of (bits_a, bits_b) in plane idx (svdlut_common.cuh): row
+        // stride or 4x4 tiles; the 2^23 biases of the index bits fold into
+        // texK / lutK (texT moves a tiled index onto the row-stride bias)
+        auto cell_of = [&](int idx, uint32_t ba, uint32_t bbv) -> uint32_t {
+          return plane_tiled(idx) ? (((ba >> 2) * tiles + (bbv >> 2)) << 4) + ((ba & 3u) << 2) + (bbv & 3u) + texT
+                                  : ba * cst + bbv;
+        };
         auto tex_issue = [&](int u, float4 (&tq_)[9], uint32_t dep) {
           const uint32_t br = bits(mcr[u >> 1], u), bg = bits(mcg[u >> 1], u), bb = bits(mcb[u >> 1], u);
 #pragma unroll
-          for (int pr = 0; pr < 3; ++pr) {
+          for (int idx = 0; idx < 9; ++idx) {
+            if (plane_in_smem(idx)) continue;
+            const int pr = idx / 3;
             const uint32_t ba = pr == 2 ? bg : br, bbv = pr == 0 ? bg : bb;
-            const uint32_t t0 = ba * cst + bbv + texK + (uint32_t)(L.plane_off(pr, 0) / 4) + dep;
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk)
-              if (!plane_in_smem(3 * pr + kk)) tq_[3 * pr + kk] = texv4(p.tex, (int)(t0 + kk * ptex));
+            tq_[idx] = texv4(p.tex, (int)(cell_of(idx, ba, bbv) + texK + (uint32_t)(L.plane_off(pr, idx % 3) / 4) + dep));
           }
         };
         tex_issue(0, tq, 0u);
@@ -405,11 +414,17 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
           const float a_r = lo(dr[u >> 1], u), a_g = lo(dg[u >> 1], u), a_b = lo(db[u >> 1], u);
           // shared-memory planes
           float4 c[9];
-          const uint32_t ur = br * cst16 + lutK, ug = bg * cst16 + lutK;
-          const uint32_t cell_a[3] = {ur + bg * 16u, ur + bb * 16u, ug + bb * 16u};
+          const uint32_t ur = br * cst16 + lutK;
+          const uint32_t row_a[3] = {ur + bg * 16u, ur + bb * 16u, bg * cst16 + bb * 16u + lutK};
 #pragma unroll
-          for (int idx = 0; idx < 9; ++idx)
-            if (plane_in_smem(idx)) c[idx] = lds4(cell_a[idx / 3] + (uint32_t)smem_plane_slot(idx) * plane_bytes);
+          for (int idx = 0; idx < 9; ++idx) {
+            if (!plane_in_smem(idx)) continue;
+            const int pr = idx / 3;
+            const uint32_t a = plane_tiled(idx)
+                                   ? cell_of(idx, pr == 2 ? bg : br, pr == 0 ? bg : bb) * 16u + lutK
+                                   : row_a[pr];
+            c[idx] = lds4(a + (uint32_t)smem_plane_slot(idx) * plane_bytes);
+          }
           const uint32_t sa = slotK + bits(mx[u >> 1], u) * jx_bytes;
           const float4 s0 = lds4(sa + bits(msr[u >> 1], u) * 16u);
           const float4 s1 = lds4(sa + chan_bytes + bits(msg[u >> 1], u) * 16u);

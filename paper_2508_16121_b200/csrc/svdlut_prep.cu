@@ -135,12 +135,15 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
         q[2] = p01 - p00;                      // C
         q[3] = (p11 - p10) - (p01 - p00);      // D
       }
-      const int cell = i * L.cst + j;
-      SVDLUT_CHECK(i < dt - 1 && j < L.cst && cell < L.plane_floats / 4);
-      P0[(sA >> 2) * L.plane_floats + cell * 4 + (sA & 3)] = (float)q[0];
-      P0[(sB >> 2) * L.plane_floats + cell * 4 + (sB & 3)] = (float)q[1];
-      P0[(sC >> 2) * L.plane_floats + cell * 4 + (sC & 3)] = (float)q[2];
-      P0[(sD >> 2) * L.plane_floats + cell * 4 + (sD & 3)] = (float)q[3];
+      const int sl[4] = {sA, sB, sC, sD};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int idx = 3 * p + (sl[t] >> 2);
+        if (plane_tiled(idx) && j >= dt - 1) continue;  // tiled planes have no padding columns
+        const int cell = L.cell_index(idx, i, j);
+        SVDLUT_CHECK(i < dt - 1 && j < L.cst && cell < L.plane_floats / 4);
+        P0[(sl[t] >> 2) * L.plane_floats + cell * 4 + (sl[t] & 3)] = (float)q[t];
+      }
     }
     return;
   }
@@ -149,7 +152,8 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
   const int n_gxy = ds * ds;  // vertices (3 floats each)
   const int n_gyc = 3 * ds * ds;
   const int n_tail = L.total_floats - (L.gyc_off + n_gyc);
-  const int total = n_xc + n_gxy + n_gyc + n_tail;
+  const int n_gbpad = L.plane_floats / 4;  // tiled planes: zero the positions that hold no cell
+  const int total = n_xc + n_gxy + n_gyc + n_tail + n_gbpad;
   const int gb0 = 9 * nbands;
   for (int e = (blockIdx.x - gb0) * blockDim.x + threadIdx.x; e < total;
        e += (gridDim.x - gb0) * blockDim.x) {
@@ -197,7 +201,20 @@ __global__ void pack_kernel(const float* __restrict__ lp, const float* __restric
       continue;
     }
     r -= n_gyc;
-    T[L.gyc_off + n_gyc + r] = 0.f;  // tail padding
+    if (r < n_tail) {
+      T[L.gyc_off + n_gyc + r] = 0.f;  // tail padding
+      continue;
+    }
+    r -= n_tail;
+    {  // position r of every tiled plane: zero unless it holds a cell (i, j)
+      const int tile = r >> 4, tr = (r >> 2) & 3, tc = r & 3;
+      const int ti = tile / L.tiles(), tj = tile - ti * L.tiles();
+      const int i = ti * 4 + tr, j = tj * 4 + tc;
+      if (tile < L.tiles() * L.tiles() && i < dt - 1 && j < dt - 1) continue;
+      for (int idx = 0; idx < 9; ++idx)
+        if (plane_tiled(idx))
+          reinterpret_cast<float4*>(T + L.plane_off(idx / 3, idx % 3))[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
 }
 
@@ -213,7 +230,7 @@ cudaError_t launch_pack(const float* lp, const float* fu, const float* fs, const
                         const float* gb, int k, const TableLayout& L, int batch, float* tables,
                         cudaStream_t st) {
   // 9 planes x row bands + enough grid blocks for one item per thread
-  const int grid_items = 3 * (L.ds - 1) * (L.ds - 1) + 4 * L.ds * L.ds + 64;
+  const int grid_items = 3 * (L.ds - 1) * (L.ds - 1) + 4 * L.ds * L.ds + 64 + L.plane_floats / 4;
   const int nbands = (L.dt - 1 + kPackBand - 1) / kPackBand;
   dim3 grid(9 * nbands + (grid_items + 255) / 256, batch);
   size_t smem = (size_t)(kPackBand + 1) * L.dt * sizeof(float);

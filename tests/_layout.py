@@ -16,7 +16,8 @@ class Layout:
     def __init__(self, dt, ds):
         self.dt, self.ds = dt, ds
         self.cst = cst_for(dt)
-        self.plane_floats = (dt - 1) * self.cst * 4
+        self.tiles = (dt + 2) // 4
+        self.plane_floats = max((dt - 1) * self.cst, self.tiles * self.tiles * 16) * 4
         self.lut_off = 0
         self.xc_off = self.lut_off + 9 * self.plane_floats
         self.gxy_off = self.xc_off + 3 * (ds - 1) * (ds - 1) * 4
@@ -39,15 +40,27 @@ def coef_slot(c, q):
     return (8, 10, 9, 11)[q]
 
 
+TILED_PLANES = {4, 6, 7, 8}  # svdlut_common.cuh kTiledPlanes: rb chunk 1, gb chunks 0-2
+
+
+def cell_index(L, idx, i, j):
+    """Cell (i, j) within chunk plane idx = 3*pair + chunk: row stride cst, or
+    4x4 tiles for the texture-path planes (svdlut_common.cuh)."""
+    if idx not in TILED_PLANES:
+        return i * L.cst + j
+    return ((i >> 2) * L.tiles + (j >> 2)) * 16 + ((i & 3) << 2) + (j & 3)
+
+
 def write_cells(table, L, p, c, coef):
     """Write coefficient arrays coef (4, dt-1, dt-1) = (A, B, C, D) of channel
     c, pair p (cells (i, j)), into a flat table."""
     n = L.dt - 1
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
     for q in range(4):
         slot = coef_slot(c, q)
         base = L.plane_off(p, slot // 4)
-        plane = table[base:base + L.plane_floats].reshape(n, L.cst, 4)
-        plane[:, :n, slot % 4] = coef[q]
+        plane = table[base:base + L.plane_floats].reshape(-1, 4)
+        plane[cell_index(L, 3 * p + slot // 4, i, j), slot % 4] = coef[q]
 
 
 def empty_table(L):

@@ -24,8 +24,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHECKED = os.path.join(ROOT, "paper_2508_16121_b200", "_lib", "variants", "libchecked.so")
 
 
+def _stale(lib):
+    import glob
+
+    if not os.path.exists(lib):
+        return True
+    srcs = glob.glob(os.path.join(ROOT, "paper_2508_16121_b200", "csrc", "*"))
+    return any(os.path.getmtime(f) > os.path.getmtime(lib) for f in srcs)
+
+
 def test_bounds_checked_build_runs_clean():
-    if not os.path.exists(CHECKED):
+    if _stale(CHECKED):
         res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "build_variant.py"), "checked",
                               "-DSVDLUT_BOUNDS_CHECK"], cwd=ROOT, capture_output=True, text=True, timeout=1800)
         assert res.returncode == 0, res.stderr[-3000:]
