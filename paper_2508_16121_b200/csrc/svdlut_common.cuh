@@ -49,7 +49,7 @@ constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 // cst >= dt-1 with cst % 8 == 3: the 3x3 cell neighbourhood a run of pixels
 // touches maps to distinct 16-byte bank groups except the two opposite
 // diagonals.  Planes gathered through the texture path (kTiledPlanes: pair
-// gb and chunk 1 of pair rb) store their cells in 4x4 tiles, index
+// gb and chunks 1-2 of pair rb) store their cells in 4x4 tiles, index
 // ((i/4)*T + j/4)*16 + (i%4)*4 + j%4 with T = ceil((dt-1)/4): the cells a
 // warp's pixels touch then share a few 128-byte cache lines (a texture gather
 // costs a cycle per distinct line beyond four).
@@ -66,9 +66,9 @@ constexpr int kSmemReserve = 1024;           // mbarrier + scratch
 __host__ __device__ constexpr int cst_for(int dt) { return (dt - 1) + ((3 - (dt - 1)) & 7); }
 // chunk planes (bit 3*pair + chunk) stored in the 4x4-tiled cell order
 #ifndef SVDLUT_TILED_PLANES
-#define SVDLUT_TILED_PLANES 0x1D0u
+#define SVDLUT_TILED_PLANES 0x1F0u
 #endif
-constexpr unsigned kTiledPlanes = SVDLUT_TILED_PLANES;  // rb chunk 1, gb chunks 0-2
+constexpr unsigned kTiledPlanes = SVDLUT_TILED_PLANES;  // rb chunks 1-2, gb chunks 0-2
 __host__ __device__ constexpr bool plane_tiled(int idx) { return (kTiledPlanes >> idx) & 1u; }
 
 struct TableLayout {

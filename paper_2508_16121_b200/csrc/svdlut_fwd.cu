@@ -35,8 +35,8 @@ namespace svdlut {
 #endif
 #ifndef FWD_PLANES
 // LUT chunk planes staged in shared memory (bit 3*pair + chunk; pairs rg, rb,
-// gb); the others (chunk 1 of rb, pair gb) go through the texture path
-#define FWD_PLANES 0x2F
+// gb); the others (chunks 1-2 of rb, pair gb) go through the texture path
+#define FWD_PLANES 0x0F
 #endif
 constexpr int kFwdWarps = FWD_NW;
 constexpr int kPx = 4;                 // consecutive pixels per lane

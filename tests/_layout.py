@@ -40,7 +40,7 @@ def coef_slot(c, q):
     return (8, 10, 9, 11)[q]
 
 
-TILED_PLANES = {4, 6, 7, 8}  # svdlut_common.cuh kTiledPlanes: rb chunk 1, gb chunks 0-2
+TILED_PLANES = {4, 5, 6, 7, 8}  # svdlut_common.cuh kTiledPlanes: rb chunks 1-2, gb chunks 0-2
 
 
 def cell_index(L, idx, i, j):
