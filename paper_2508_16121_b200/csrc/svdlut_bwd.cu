@@ -23,16 +23,57 @@
 //         pass 2^31, and at the end of each image.
 // finalize_kernel: dlut = lw * E, dlw = <T, E>, dgrid[k,q] = gw[k,q] * E[q][k%3],
 // dgw = <G, E>, dlb / dgb from the per-image gY sums.
+#include <atomic>
 #include <cstdint>
 #include "svdlut_common.cuh"
 #include "svdlut_internal.h"
 
 namespace svdlut {
 
-constexpr int kBwdWarps = 15;
+#ifndef BWD_NW
+#define BWD_NW 15
+#endif
+constexpr int kBwdWarps = BWD_NW;
 constexpr int kBPx = 4;
 constexpr uint32_t kMagic = 0x4B000000u;
 constexpr int kBwdL2Rows = 2;  // rows of L2 prefetch distance (X and gY planes)
+
+// LUT chunk planes (bit 3*pair + chunk) staged in shared memory by TMA; the
+// others are gathered through the texture path.  Only the input gradient gX
+// reads them (B, C, D coefficients of the pixel's cells).
+#ifndef BWD_PLANES
+#define BWD_PLANES 0x3Fu
+#endif
+constexpr unsigned kBwdPlanes = BWD_PLANES;
+constexpr int bpopc(unsigned m) { return m ? (int)(m & 1u) + bpopc(m >> 1) : 0; }
+constexpr int kBwdStaged = bpopc(kBwdPlanes & 0x1FFu);
+
+// Addressing of the chunk planes from 2^23-biased cell index bits
+// (ba = kMagic + i): shared-memory byte addresses or texel indices.
+struct BAddr {
+  uint32_t lutK;   // smem, row-stride cell order: lutK + ba*cst16 + bb*16 + slot*plane_bytes
+  uint32_t lutT;   // smem, 4x4-tiled order:      lutT + tiled(ba, bb)*16 + slot*plane_bytes
+  uint32_t texR;   // texel, row-stride:          texR + ba*cst + bb + idx*ptex
+  uint32_t texT;   // texel, tiled:               texT + tiled(ba, bb) + idx*ptex
+  uint32_t cst, cst16, tiles, plane_bytes, ptex;
+  cudaTextureObject_t tex;
+};
+
+template <int IDX>
+__device__ __forceinline__ float4 bfetch(const BAddr& a, uint32_t ba, uint32_t bb) {
+  constexpr bool kSmem = (kBwdPlanes >> IDX) & 1u;
+  constexpr bool kTiled = plane_tiled(IDX);
+  const uint32_t tcell = (((ba >> 2) * a.tiles + (bb >> 2)) << 4) + ((ba & 3u) << 2) + (bb & 3u);
+  if constexpr (kSmem) {
+    constexpr int kSlot = bpopc(kBwdPlanes & ((1u << IDX) - 1u));
+    const uint32_t addr = (kTiled ? tcell * 16u + a.lutT : ba * a.cst16 + bb * 16u + a.lutK) +
+                          (uint32_t)kSlot * a.plane_bytes;
+    return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(addr));
+  } else {
+    const uint32_t t = (kTiled ? tcell + a.texT : ba * a.cst + bb + a.texR) + (uint32_t)IDX * a.ptex;
+    return tex1Dfetch<float4>(a.tex, (int)t);
+  }
+}
 
 // Bulk L2 prefetch of row y of three planes (16-byte aligned cover, clipped
 // to each plane), no completion tracking.
@@ -190,33 +231,49 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
   const int rc0 = lane % 3, rc1 = (lane + 1) % 3, rc2 = (lane + 2) % 3;  // lane's channel order
+  // lane's corner order: k-th corner = (k + lane/3) % 4, bit 0 the first
+  // axis (LUT a / grid x), bit 1 the second (LUT b / grid guide)
+  bool kqa[4], kqb[4];
+  int kcoff[4], kxoff[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = (k + lane / 3) & 3;
+    kqa[k] = q & 1;
+    kqb[k] = q & 2;
+    kcoff[k] = ((q & 1) ? (dt + 1) * 3 : 0) + ((q & 2) ? 3 : 0);
+    kxoff[k] = ((q & 1) ? ds : 0) + ((q & 2) ? 1 : 0);
+  }
 
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // staged: pair rb's three chunk planes, then the grid block
+  // staged: the kBwdPlanes chunk planes (in plane order), then the slot rows
+  // and the accumulators
   const uint32_t plane_bytes = (uint32_t)L.plane_floats * 4u;
-  const uint32_t table_bytes = 6u * plane_bytes;  // pairs rg and rb (contiguous in the table)
+  const uint32_t table_bytes = (uint32_t)kBwdStaged * plane_bytes;
   const int nent = (ds - 1) * 3 * (ds - 1);
   float4* slots = reinterpret_cast<float4*>(reinterpret_cast<char*>(smem) + table_bytes);
   float* Es = reinterpret_cast<float*>(slots + 2 * nent);  // A.total floats
   const float tdm1 = (float)(dt - 1), tdm2 = (float)(dt - 2);
   const float sdm1 = (float)(ds - 1), sdm2 = (float)(ds - 2);
-  const uint32_t cst = (uint32_t)L.cst, cst16 = cst * 16u;
-  const uint32_t ptex = (uint32_t)L.plane_floats / 4u;  // texels per plane
-  // smem address of pair rg / rb cell (bits_a, bits_b), chunk k: lutK + ba*cst16 + bb*16 + k*plane_bytes
-  // (+ 3 planes for rb)
-  const uint32_t lutK = sbase - kMagic * (cst16 + 16u);
-  const uint32_t tiles = (uint32_t)L.tiles();
-  // the same for a 4x4-tiled plane: lutT + tiled(bits_a, bits_b) * 16
-  const uint32_t lutT = sbase - (((kMagic >> 2) * tiles + (kMagic >> 2)) << 8);
+  BAddr ad;
+  ad.cst = (uint32_t)L.cst;
+  ad.cst16 = ad.cst * 16u;
+  ad.ptex = (uint32_t)L.plane_floats / 4u;  // texels per plane
+  ad.tiles = (uint32_t)L.tiles();
+  ad.plane_bytes = plane_bytes;
+  ad.lutK = sbase - kMagic * (ad.cst16 + 16u);
+  ad.lutT = sbase - (((kMagic >> 2) * ad.tiles + (kMagic >> 2)) << 8);
+  ad.tex = p.tex;
   const uint32_t chan_bytes = (uint32_t)(ds - 1) * 16u;
   const uint32_t jx_bytes = 3u * chan_bytes;
   const uint32_t slot_row_bytes = (uint32_t)nent * 16u;
   const uint32_t slotK0 = bsmem_addr(slots) - kMagic * 16u;
   int* Ei = reinterpret_cast<int*>(Es);
-  int* Rrow = Ei + A.total;  // 2 rows x [Rx 3*ds | Rc 3*ds]
+  int* Rrow = Ei + A.total;         // 2 rows x [Rx 3*ds | Rc 3*ds]
+  int* XRrow = Rrow + 12 * ds;      // 2 rows x xc plane [c 3][vx ds][vc ds] of the row
+  const int xr_size = 3 * ds * ds;
   int* E_lut = Ei + A.lut_off;
   int* E_xy = Ei + A.grid_off;
   int* E_xc = E_xy + 3 * ds * ds;
@@ -241,7 +298,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(table_bytes)
                    : "memory");
-      // pair rb's planes are contiguous in the table; the grid block follows them in smem
       auto copy = [&](uint32_t dst, const char* from, uint32_t bytes) {
         for (uint32_t off = 0; off < bytes; off += 32768u)
           asm volatile(
@@ -250,9 +306,15 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               "l"(from + off), "r"(min(32768u, bytes - off)), "r"(bar)
               : "memory");
       };
-      copy(sbase, reinterpret_cast<const char*>(tb + L.plane_off(0, 0)), 6u * plane_bytes);
+      uint32_t dst = sbase;
+#pragma unroll
+      for (int idx = 0; idx < 9; ++idx)
+        if ((kBwdPlanes >> idx) & 1u) {
+          copy(dst, reinterpret_cast<const char*>(tb + L.lut_off + idx * L.plane_floats), plane_bytes);
+          dst += plane_bytes;
+        }
     }
-    for (int i = threadIdx.x; i < A.total + 12 * ds; i += blockDim.x) Ei[i] = 0;
+    for (int i = threadIdx.x; i < A.total + 12 * ds + 2 * xr_size; i += blockDim.x) Ei[i] = 0;
     float gm = p.gmax[b];
     if (p.gss) gm = fminf(gm, kOutlierSigmas * (float)sqrt(p.gss[b] / (3.0 * (double)pl)));
     const float S = gm > 0.f ? kFixedOne / gm : 1.0f;  // fixed-point scale of this image
@@ -263,11 +325,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     const float* X = p.rgb + (long long)b * 3 * pl;
     const float* GY = p.gy + (long long)b * 3 * pl;
     float* GX = p.gx ? p.gx + (long long)b * 3 * pl : nullptr;
-    // texel of cell (bits_a, bits_b), chunk k of pair rg / gb: tex* + bits_a*cst + bits_b + k*ptex
     const float* gsm = tb + L.xc_off;  // grid block (global, L1-cached; read by the slot production)
-    const uint32_t texK = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
-                          (uint32_t)(L.plane_off(2, 0) / 4) - (((kMagic >> 2) * tiles + (kMagic >> 2)) << 4);  // pair gb
-    const uint32_t texKr = texK + (((kMagic >> 2) * tiles + (kMagic >> 2)) << 4) - kMagic * (cst + 1u);
+    {
+      const uint32_t t0 = (uint32_t)p.tex_base + (uint32_t)b * (uint32_t)(L.total_floats / 4) +
+                          (uint32_t)(L.lut_off / 4);
+      ad.texT = t0 - (((kMagic >> 2) * ad.tiles + (kMagic >> 2)) << 4);
+      ad.texR = t0 - kMagic * (ad.cst + 1u);
+    }
     asm volatile(
         "{\n.reg .pred p;\nWAITB_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAITB_%=;\n}\n" ::"r"(bar),
         "r"(phase)
@@ -288,6 +352,25 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     produce_rows(y_first);
     __syncthreads();
     float gsum0 = 0.f, gsum1 = 0.f, gsum2 = 0.f;
+    // Rrow[par] = [Rx[c][vx] = sum g_c wx | Rc[c][vc] = sum g_c wc] of one row
+    // into the xy / yc planes with that row's y weights, then zeroed
+    auto fold_rows = [&](int par, int jyr, float eyr) {
+      int* R = Rrow + par * 6 * ds;
+      for (int i = threadIdx.x; i < 6 * ds; i += blockDim.x) {
+        const int v = R[i];
+        if (v != 0) {
+          const bool isx = i < 3 * ds;
+          const int c = (isx ? i : i - 3 * ds) / ds, t = (isx ? i : i - 3 * ds) - c * ds;
+          int* e = isx ? E_xy + (c * ds + t) * ds + jyr : E_yc + (c * ds + jyr) * ds + t;
+          const float fv = (float)v;
+          atomicAdd(e, __float2int_rn(fv * (1.f - eyr)));
+          atomicAdd(e + (isx ? 1 : ds), __float2int_rn(fv * eyr));
+          R[i] = 0;
+        }
+      }
+    };
+    int jy_prev = 0;
+    float ey_prev = 0.f;
 
     for (int y = y_first; y <= y_last; ++y) {
       const int buf = (y - y_first) & 1;
@@ -300,48 +383,19 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       float ey;
       const int jy = (int)(row_bracket(p.y0 + y, p.rcp_h, sdm1, sdm2, ey) - kMagic);
       const uint32_t slotK = slotK0 + (uint32_t)buf * slot_row_bytes;
-      // Spread lane mapping: the CTA walks the row in 4-pixel slots; lane l of
-      // warp w takes slot s0 + l * kBwdWarps + w, so the 32 lanes of one warp
-      // instruction sit kBwdWarps * 4 = 60 px apart.  On smooth images that
-      // makes their LUT cells (and so the shared atomics' addresses) nearly
-      // independent; with neighbouring lanes 4 px apart a warp instruction had
-      // ~10 lanes on the same address, which ATOMS serializes (measured cost:
-      // max lanes per bank, same-address lanes not merged).
-      const int slots4 = (p.w + 3) >> 2;
-      // per-row guide / x-vertex sums of this row (fixed point, parity buffer):
-      //   Rx[c][vx] = sum g_c wx   (xy plane: folded with wy(b) at the row's end)
-      //   Rc[c][vc] = sum g_c wc   (yc plane: likewise)
-      int* Rx = Rrow + (y & 1) * 6 * ds;
-      int* Rc = Rx + 3 * ds;
-      for (int s0 = 0; s0 < slots4; s0 += kBwdWarps * 32) {
-        const int xl = 4 * (s0 + lane * kBwdWarps + warp);
+      // Lane mapping as in the forward: warp chunks of 128 consecutive
+      // pixels, lane = 4 consecutive pixels.  Neighbouring lanes then share
+      // cells, which keeps the table gathers cheap (4.5 instead of 8.7
+      // cycles per LDS.128, tools/microbench/bwd_lds.txt); the atomics of
+      // lanes that share a cell are spread over twelve words by the lane's
+      // corner x channel rotation (3.6 cycles per ATOMS instead of 10).
+      int* XR = XRrow + (y & 1) * xr_size;
+      for (int x0 = warp * 128; x0 < p.w; x0 += kBwdWarps * 128) {
+        const int xl = x0 + 4 * lane;
         if (xl >= p.w) continue;
         BChunk cur;
-        bload_chunk(X, GY, pl, y, xl - 4 * lane, p.w, lane, vec, cur);
+        bload_chunk(X, GY, pl, y, x0, p.w, lane, vec, cur);
         float oxr[kBPx], oxg[kBPx], oxb[kBPx];
-        // lane-local runs: xc (4) + yc (2) sums per channel keyed by (x-cell,
-        // guide cell); xy (2) sums per channel keyed by the x-cell
-        int run_key[3] = {-1, -1, -1};
-        float rxc[3][4] = {}, ryc[3][2] = {};
-        int xkey = -1;
-        float rxy[3][2] = {};
-        auto flush_run = [&](int c) {
-          const int jx = run_key[c] >> 8, jc = run_key[c] & 0xff;
-          int* xc = E_xc + c * ds * ds + jx * ds + jc;
-          atomicAdd(xc, to_fixed(rxc[c][0], S));
-          atomicAdd(xc + ds, to_fixed(rxc[c][1], S));
-          atomicAdd(xc + 1, to_fixed(rxc[c][2], S));
-          atomicAdd(xc + ds + 1, to_fixed(rxc[c][3], S));
-          atomicAdd(Rc + c * ds + jc, to_fixed(ryc[c][0], S));
-          atomicAdd(Rc + c * ds + jc + 1, to_fixed(ryc[c][1], S));
-        };
-        auto flush_xy = [&]() {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            atomicAdd(Rx + c * ds + xkey, to_fixed(rxy[c][0], S));
-            atomicAdd(Rx + c * ds + xkey + 1, to_fixed(rxy[c][1], S));
-          }
-        };
 #pragma unroll
         for (int u = 0; u < kBPx; ++u) {
           const bool valid = xl + u < p.w;
@@ -374,31 +428,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // chunks {A0 A1 B0 B1} {C0 C1 D0 D1} {A2 C2 B2 D2} (svdlut_common.cuh):
           // d/da = B + D b, d/db = C + D a per channel
           {
-            const uint32_t a = br * cst16 + bg * 16u + lutK;  // rg (shared memory)
-            const uint32_t at = ((((br >> 2) * tiles + (bg >> 2)) << 4) + ((br & 3u) << 2) + (bg & 3u)) * 16u + lutT;
-            const float4 c0 = blds4(plane_tiled(0) ? at : a);
-            const float4 c1 = blds4((plane_tiled(1) ? at : a) + plane_bytes);
-            const float4 c2 = blds4((plane_tiled(2) ? at : a) + 2u * plane_bytes);
+            const float4 c0 = bfetch<0>(ad, br, bg), c1 = bfetch<1>(ad, br, bg), c2 = bfetch<2>(ad, br, bg);  // rg
             gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.z);
             gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            // rb (shared memory); a plane may be stored in 4x4 tiles (svdlut_common.cuh)
-            const uint32_t a = br * cst16 + bb * 16u + lutK;
-            const uint32_t at = ((((br >> 2) * tiles + (bb >> 2)) << 4) + ((br & 3u) << 2) + (bb & 3u)) * 16u + lutT;
-            const float4 c0 = blds4((plane_tiled(3) ? at : a) + 3u * plane_bytes);
-            const float4 c1 = blds4((plane_tiled(4) ? at : a) + 4u * plane_bytes);
-            const float4 c2 = blds4((plane_tiled(5) ? at : a) + 5u * plane_bytes);
+            const float4 c0 = bfetch<3>(ad, br, bb), c1 = bfetch<4>(ad, br, bb), c2 = bfetch<5>(ad, br, bb);  // rb
             gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            // gb via the texture path (row-stride or 4x4-tiled cells, svdlut_common.cuh)
-            const uint32_t tt = (((bg >> 2) * tiles + (bb >> 2)) << 4) + ((bg & 3u) << 2) + (bb & 3u) + texK;
-            const uint32_t tr = bg * cst + bb + texKr;
-            const float4 c0 = tex1Dfetch<float4>(p.tex, (int)(plane_tiled(6) ? tt : tr)),
-                         c1 = tex1Dfetch<float4>(p.tex, (int)((plane_tiled(7) ? tt : tr) + ptex)),
-                         c2 = tex1Dfetch<float4>(p.tex, (int)((plane_tiled(8) ? tt : tr) + 2u * ptex));
+            const float4 c0 = bfetch<6>(ad, bg, bb), c1 = bfetch<7>(ad, bg, bb), c2 = bfetch<8>(ad, bg, bb);  // gb
             gag += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dg, c1.x) + g1 * __fmaf_rn(c1.w, dg, c1.y) + g2 * __fmaf_rn(c2.w, dg, c2.y);
           }
@@ -414,14 +454,15 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           oxb[u] = (Xb < 0.f || Xb > 1.f) ? 0.f : __fmaf_rn(gab, tdm1, gsb * sdm1);
 
           // ---- scatter: LUT pairs, one fixed-point atomic per (corner, channel) ----
-          // The lane writes channel (k + lane % 3) % 3 at its k-th atomic of a
-          // corner, so lanes of one instruction that share a cell hit three
-          // different words; corner offsets are immediates (AccLayout).
+          // Lane l issues corner (k + l/3) % 4 at its k-th corner and channel
+          // (j + l) % 3 at its j-th channel (lane-constant offsets kcoff /
+          // kqa / kqb, rc*): up to twelve lanes that share a cell hit twelve
+          // different words.
+          const float fs[3] = {f0 * S, f1 * S, f2 * S};
+          const float s0v = rc0 == 0 ? fs[0] : rc0 == 1 ? fs[1] : fs[2];
+          const float s1v = rc1 == 0 ? fs[0] : rc1 == 1 ? fs[1] : fs[2];
+          const float s2v = rc2 == 0 ? fs[0] : rc2 == 1 ? fs[1] : fs[2];
           if (valid) {
-            const float fs[3] = {f0 * S, f1 * S, f2 * S};
-            const float s0v = fs[rc0 == 0 ? 0 : rc0 == 1 ? 1 : 2];
-            const float s1v = rc1 == 0 ? fs[0] : rc1 == 1 ? fs[1] : fs[2];
-            const float s2v = rc2 == 0 ? fs[0] : rc2 == 1 ? fs[1] : fs[2];
             const int ir = (int)(br - kMagic), ig = (int)(bg - kMagic), ib = (int)(bb - kMagic);
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
@@ -430,18 +471,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
               SVDLUT_CHECK(((pr * dt + ia + 1) * (dt + 1) + ibb + 1) * 3 + 2 < A.grid_off);
               const float ea = 1.f - da, eb = 1.f - dbb;
-              const float w[4] = {ea * eb, da * eb, ea * dbb, da * dbb};  // corners (0,0) (1,0) (0,1) (1,1)
               int* e0 = e + rc0;
               int* e1 = e + rc1;
               int* e2 = e + rc2;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int off = ((q & 1) ? (dt + 1) * 3 : 0) + ((q & 2) ? 3 : 0);
-                const float2 v01 = __ffma2_rn(make_float2(s0v, s1v), make_float2(w[q], w[q]),
+              for (int k = 0; k < 4; ++k) {
+                const float wk = (kqa[k] ? da : ea) * (kqb[k] ? dbb : eb);
+                const float2 v01 = __ffma2_rn(make_float2(s0v, s1v), make_float2(wk, wk),
                                               make_float2(12582912.0f, 12582912.0f));
-                atomicAdd(e0 + off, __float_as_int(v01.x) - 0x4B400000);
-                atomicAdd(e1 + off, __float_as_int(v01.y) - 0x4B400000);
-                atomicAdd(e2 + off, __float_as_int(__fmaf_rn(s2v, w[q], 12582912.0f)) - 0x4B400000);
+                atomicAdd(e0 + kcoff[k], __float_as_int(v01.x) - 0x4B400000);
+                atomicAdd(e1 + kcoff[k], __float_as_int(v01.y) - 0x4B400000);
+                atomicAdd(e2 + kcoff[k], __float_as_int(__fmaf_rn(s2v, wk, 12582912.0f)) - 0x4B400000);
               }
             }
           }
@@ -482,44 +522,31 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               atomicAdd(yc + ds + 1, gg[c] * ey * ecs[c]);
             }
           }
-          // ---- grids: runs per channel (x-cell, guide cell) and per x-cell ----
+          // ---- grid xc plane of this row: XR[c][vx][vc] += g_c wx wc, with the
+          // same corner x channel rotation ----
           if (valid) {
-            if (jx != xkey) {
-              if (xkey >= 0) flush_xy();
-              xkey = jx;
+            const int jcr = (int)(sr - kMagic), jcg = (int)(sg - kMagic), jcb = (int)(sb - kMagic);
+            const int j0 = rc0 == 0 ? jcr : rc0 == 1 ? jcg : jcb;
+            const int j1 = rc1 == 0 ? jcr : rc1 == 1 ? jcg : jcb;
+            const int j2 = rc2 == 0 ? jcr : rc2 == 1 ? jcg : jcb;
+            const float c0e = rc0 == 0 ? er : rc0 == 1 ? eg : eb;
+            const float c1e = rc1 == 0 ? er : rc1 == 1 ? eg : eb;
+            const float c2e = rc2 == 0 ? er : rc2 == 1 ? eg : eb;
+            int* x0p = XR + rc0 * ds * ds + jx * ds + j0;
+            int* x1p = XR + rc1 * ds * ds + jx * ds + j1;
+            int* x2p = XR + rc2 * ds * ds + jx * ds + j2;
+            const float wx0 = 1.f - ex;
 #pragma unroll
-              for (int c = 0; c < 3; ++c) rxy[c][0] = rxy[c][1] = 0.f;
-            }
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const float gc = c == 0 ? f0 : (c == 1 ? f1 : f2);
-              const int jc = (int)((c == 0 ? sr : (c == 1 ? sg : sb)) - kMagic);
-              const float ec = c == 0 ? er : (c == 1 ? eg : eb);
-              const int key = (jx << 8) | jc;
-              if (key != run_key[c]) {
-                if (run_key[c] >= 0) flush_run(c);
-                run_key[c] = key;
-                rxc[c][0] = rxc[c][1] = rxc[c][2] = rxc[c][3] = 0.f;
-                ryc[c][0] = ryc[c][1] = 0.f;
-              }
-              const float gx1 = gc * ex, gx0 = gc - gx1;  // g (1 - ex), g ex
-              const float gc1 = gc * ec;
-              rxc[c][0] = __fmaf_rn(-gx0, ec, rxc[c][0] + gx0);  // g (1-ex)(1-ec)
-              rxc[c][1] = __fmaf_rn(-gx1, ec, rxc[c][1] + gx1);  // g ex (1-ec)
-              rxc[c][2] = __fmaf_rn(gx0, ec, rxc[c][2]);         // g (1-ex) ec
-              rxc[c][3] = __fmaf_rn(gx1, ec, rxc[c][3]);         // g ex ec
-              ryc[c][0] += gc - gc1;
-              ryc[c][1] += gc1;
-              rxy[c][0] += gx0;
-              rxy[c][1] += gx1;
+            for (int k = 0; k < 4; ++k) {
+              const float wx = kqa[k] ? ex : wx0;
+              const float w0 = kqb[k] ? c0e : 1.f - c0e, w1 = kqb[k] ? c1e : 1.f - c1e,
+                          w2 = kqb[k] ? c2e : 1.f - c2e;
+              atomicAdd(x0p + kxoff[k], __float_as_int(__fmaf_rn(s0v * wx, w0, 12582912.0f)) - 0x4B400000);
+              atomicAdd(x1p + kxoff[k], __float_as_int(__fmaf_rn(s1v * wx, w1, 12582912.0f)) - 0x4B400000);
+              atomicAdd(x2p + kxoff[k], __float_as_int(__fmaf_rn(s2v * wx, w2, 12582912.0f)) - 0x4B400000);
             }
           }
         }
-        // ---- end of the lane's 4 pixels: open runs ----
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (run_key[c] >= 0) flush_run(c);
-        if (xkey >= 0) flush_xy();
         if (GX) {
           const long long ro = (long long)y * p.w;
           if (vec && xl + 4 <= p.w) {
@@ -540,20 +567,24 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       px_since_flush += p.w;
       if (y < y_last) produce_rows(y + 1);  // the other half of the ring
       __syncthreads();
-      // fold this row's Rx / Rc into the xy / yc planes with wy(b) of row y
-      // and zero them (rows y + 1 use the other buffer)
-      for (int i = threadIdx.x; i < 6 * ds; i += blockDim.x) {
-        const int v = Rx[i];
+      // the previous row's x-vertex / guide-vertex sums (complete since the
+      // barrier) into the xy / yc planes with that row's y weights
+      if (y > y_first) fold_rows((y - 1) & 1, jy_prev, ey_prev);
+      // this row's xc sums into E_xc and its x-vertex / guide-vertex sums;
+      // the buffer is zeroed for row y + 2 (rows y + 1 use the other one)
+      for (int i = threadIdx.x; i < xr_size; i += blockDim.x) {
+        const int v = XR[i];
         if (v != 0) {
-          const bool isx = i < 3 * ds;
-          const int c = (isx ? i : i - 3 * ds) / ds, t = (isx ? i : i - 3 * ds) - c * ds;
-          int* e = isx ? E_xy + (c * ds + t) * ds + jy : E_yc + (c * ds + jy) * ds + t;
-          const float fv = (float)v;
-          atomicAdd(e, __float2int_rn(fv * (1.f - ey)));
-          atomicAdd(e + (isx ? 1 : ds), __float2int_rn(fv * ey));
-          Rx[i] = 0;
+          const int c = i / (ds * ds), r2 = i - c * ds * ds, vx = r2 / ds, vc = r2 - vx * ds;
+          E_xc[i] += v;  // one writer per entry in this phase
+          int* R = Rrow + (y & 1) * 6 * ds;
+          atomicAdd(R + c * ds + vx, v);
+          atomicAdd(R + 3 * ds + c * ds + vc, v);
+          XR[i] = 0;
         }
       }
+      jy_prev = jy;
+      ey_prev = ey;
       if (px_since_flush + p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
         __syncthreads();  // the fold has landed
         for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
@@ -563,10 +594,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
             Ei[i] = 0;
           }
         }
-        px_since_flush = 0;
+        px_since_flush = p.w;  // row y's xy / yc sums are still pending
         __syncthreads();
       }
     }
+    __syncthreads();
+    fold_rows(y_last & 1, jy_prev, ey_prev);
     // ---- per-image gY sums and flush of the shared accumulators ----
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -681,8 +714,8 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
-  const size_t staged = (size_t)6 * L.plane_floats * 4;
-  const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds) * 4;
+  const size_t staged = (size_t)kBwdStaged * L.plane_floats * 4;
+  const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds + 6 * ds * ds) * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
   float* tables = (float*)wp;
@@ -740,16 +773,25 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     long long grid = sms < rows ? sms : rows;
-    auto kern = (dt == 33 && ds == 17) ? fused_bwd_kernel<33, 17> : fused_bwd_kernel<0, 0>;
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
-    // smallest carve-out that fits: the rest of the 256 KB array is L1 for the
-    // texture-path LUT pairs
-    const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  pct > 100 ? 100 : pct)) != cudaSuccess)
-      return e;
+    const bool spec = dt == 33 && ds == 17;
+    auto kern = spec ? fused_bwd_kernel<33, 17> : fused_bwd_kernel<0, 0>;
+    // Attributes set once per (instantiation, device) to the largest request
+    // any launch may make, so concurrent launches never see the limit lowered
+    // under them (as for the forward kernel).
+    constexpr int kMaxDev = 64;
+    static std::atomic<int> configured[kMaxDev][2];
+    if (dev >= kMaxDev || configured[dev][spec].load(std::memory_order_acquire) == 0) {
+      if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    fwd_max_smem_bytes())) != cudaSuccess)
+        return e;
+      // smallest carve-out that fits the specialised layout: the rest of the
+      // 256 KB array is L1 for the texture-path planes
+      const int pct = (int)((smem + 2048 + (228 * 1024 - 1)) * 100 / (228 * 1024)) + 1;
+      if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    pct > 100 ? 100 : pct)) != cudaSuccess)
+        return e;
+      if (dev < kMaxDev) configured[dev][spec].store(1, std::memory_order_release);
+    }
     kern<<<(int)grid, kBwdWarps * 32, smem, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = table_texture_used(p.tex, st)) != cudaSuccess) return e;
