@@ -142,6 +142,10 @@ __device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
 __device__ __forceinline__ float4 blds4(uint32_t a) {
   return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(a));
 }
+// Shared-memory fixed-point add at a byte address (ATOMS.ADD, no return).
+__device__ __forceinline__ void ared(uint32_t addr, int v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, float& delta) {
   const float t = fminf(__fmul_rz(q, dm1), dm2);
   const float m = __fadd_rz(t, 8388608.0f);
@@ -234,14 +238,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   // lane's corner order: k-th corner = (k + lane/3) % 4, bit 0 the first
   // axis (LUT a / grid x), bit 1 the second (LUT b / grid guide)
   bool kqa[4], kqb[4];
-  int kcoff[4], kxoff[4];
+  uint32_t kcoff[4], kxoff[4];  // byte offsets of the k-th corner (LUT / grid xc)
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int q = (k + lane / 3) & 3;
     kqa[k] = q & 1;
     kqb[k] = q & 2;
-    kcoff[k] = ((q & 1) ? (dt + 1) * 3 : 0) + ((q & 2) ? 3 : 0);
-    kxoff[k] = ((q & 1) ? ds : 0) + ((q & 2) ? 1 : 0);
+    kcoff[k] = (uint32_t)(((q & 1) ? (dt + 1) * 3 : 0) + ((q & 2) ? 3 : 0)) * 4u;
+    kxoff[k] = (uint32_t)(((q & 1) ? ds : 0) + ((q & 2) ? 1 : 0)) * 4u;
   }
 
   if (threadIdx.x == 0) {
@@ -272,8 +276,20 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const uint32_t slotK0 = bsmem_addr(slots) - kMagic * 16u;
   int* Ei = reinterpret_cast<int*>(Es);
   int* Rrow = Ei + A.total;         // 2 rows x [Rx 3*ds | Rc 3*ds]
-  int* XRrow = Rrow + 12 * ds;      // 2 rows x xc plane [c 3][vx ds][vc ds] of the row
+  // 2 rows x 3 lane-group copies (lanes 0-11, 12-23, 24-31: lanes with the
+  // same corner x channel rotation never share a copy) x the row's xc plane
+  // [c 3][vx ds][vc ds]
+  int* XRrow = Rrow + 12 * ds;
   const int xr_size = 3 * ds * ds;
+  const uint32_t sXR = bsmem_addr(XRrow) + (uint32_t)((lane / 12) * xr_size) * 4u;
+  // byte address of LUT pair pr's cell from 2^23-biased index bits:
+  // lutE[pr] + bits_a * (dt+1)*12 + bits_b * 12
+  const uint32_t rowB = (uint32_t)(dt + 1) * 12u;
+  uint32_t lutE[3];
+#pragma unroll
+  for (int pr = 0; pr < 3; ++pr)
+    lutE[pr] = bsmem_addr(Ei) + (uint32_t)(A.lut_off + pr * dt * (dt + 1) * 3) * 4u - kMagic * (rowB + 12u);
+  const uint32_t rcb0 = (uint32_t)rc0 * 4u, rcb1 = (uint32_t)rc1 * 4u, rcb2 = (uint32_t)rc2 * 4u;
   int* E_lut = Ei + A.lut_off;
   int* E_xy = Ei + A.grid_off;
   int* E_xc = E_xy + 3 * ds * ds;
@@ -314,7 +330,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           dst += plane_bytes;
         }
     }
-    for (int i = threadIdx.x; i < A.total + 12 * ds + 2 * xr_size; i += blockDim.x) Ei[i] = 0;
+    for (int i = threadIdx.x; i < A.total + 12 * ds + 6 * xr_size; i += blockDim.x) Ei[i] = 0;
     float gm = p.gmax[b];
     if (p.gss) gm = fminf(gm, kOutlierSigmas * (float)sqrt(p.gss[b] / (3.0 * (double)pl)));
     const float S = gm > 0.f ? kFixedOne / gm : 1.0f;  // fixed-point scale of this image
@@ -389,7 +405,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // cycles per LDS.128, tools/microbench/bwd_lds.txt); the atomics of
       // lanes that share a cell are spread over twelve words by the lane's
       // corner x channel rotation (3.6 cycles per ATOMS instead of 10).
-      int* XR = XRrow + (y & 1) * xr_size;
+      int* XR = XRrow + (y & 1) * 3 * xr_size;
+      const uint32_t sXRy = sXR + (uint32_t)((y & 1) * 3 * xr_size) * 4u;
       for (int x0 = warp * 128; x0 < p.w; x0 += kBwdWarps * 128) {
         const int xl = x0 + 4 * lane;
         if (xl >= p.w) continue;
@@ -462,26 +479,23 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           const float s0v = rc0 == 0 ? fs[0] : rc0 == 1 ? fs[1] : fs[2];
           const float s1v = rc1 == 0 ? fs[0] : rc1 == 1 ? fs[1] : fs[2];
           const float s2v = rc2 == 0 ? fs[0] : rc2 == 1 ? fs[1] : fs[2];
-          if (valid) {
-            const int ir = (int)(br - kMagic), ig = (int)(bg - kMagic), ib = (int)(bb - kMagic);
+          {  // pixels past the row end carry g = 0: their adds are zeros at clamped cells
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
-              const int ia = pr == 2 ? ig : ir, ibb = pr == 0 ? ig : ib;
+              const uint32_t ba = pr == 2 ? bg : br, bbq = pr == 0 ? bg : bb;
               const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
-              int* e = E_lut + ((pr * dt + ia) * (dt + 1) + ibb) * 3;
-              SVDLUT_CHECK(((pr * dt + ia + 1) * (dt + 1) + ibb + 1) * 3 + 2 < A.grid_off);
+              const uint32_t e = lutE[pr] + ba * rowB + bbq * 12u;
+              SVDLUT_CHECK(((pr * dt + (int)(ba - kMagic) + 1) * (dt + 1) + (int)(bbq - kMagic) + 1) * 3 + 2 <
+                           A.grid_off);
               const float ea = 1.f - da, eb = 1.f - dbb;
-              int* e0 = e + rc0;
-              int* e1 = e + rc1;
-              int* e2 = e + rc2;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const float wk = (kqa[k] ? da : ea) * (kqb[k] ? dbb : eb);
                 const float2 v01 = __ffma2_rn(make_float2(s0v, s1v), make_float2(wk, wk),
                                               make_float2(12582912.0f, 12582912.0f));
-                atomicAdd(e0 + kcoff[k], __float_as_int(v01.x) - 0x4B400000);
-                atomicAdd(e1 + kcoff[k], __float_as_int(v01.y) - 0x4B400000);
-                atomicAdd(e2 + kcoff[k], __float_as_int(__fmaf_rn(s2v, wk, 12582912.0f)) - 0x4B400000);
+                ared(e + kcoff[k] + rcb0, __float_as_int(v01.x) - 0x4B400000);
+                ared(e + kcoff[k] + rcb1, __float_as_int(v01.y) - 0x4B400000);
+                ared(e + kcoff[k] + rcb2, __float_as_int(__fmaf_rn(s2v, wk, 12582912.0f)) - 0x4B400000);
               }
             }
           }
@@ -524,26 +538,27 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           }
           // ---- grid xc plane of this row: XR[c][vx][vc] += g_c wx wc, with the
           // same corner x channel rotation ----
-          if (valid) {
-            const int jcr = (int)(sr - kMagic), jcg = (int)(sg - kMagic), jcb = (int)(sb - kMagic);
-            const int j0 = rc0 == 0 ? jcr : rc0 == 1 ? jcg : jcb;
-            const int j1 = rc1 == 0 ? jcr : rc1 == 1 ? jcg : jcb;
-            const int j2 = rc2 == 0 ? jcr : rc2 == 1 ? jcg : jcb;
+          {
+            const uint32_t jcr = sr - kMagic, jcg = sg - kMagic, jcb = sb - kMagic;
+            const uint32_t j0 = rc0 == 0 ? jcr : rc0 == 1 ? jcg : jcb;
+            const uint32_t j1 = rc1 == 0 ? jcr : rc1 == 1 ? jcg : jcb;
+            const uint32_t j2 = rc2 == 0 ? jcr : rc2 == 1 ? jcg : jcb;
             const float c0e = rc0 == 0 ? er : rc0 == 1 ? eg : eb;
             const float c1e = rc1 == 0 ? er : rc1 == 1 ? eg : eb;
             const float c2e = rc2 == 0 ? er : rc2 == 1 ? eg : eb;
-            int* x0p = XR + rc0 * ds * ds + jx * ds + j0;
-            int* x1p = XR + rc1 * ds * ds + jx * ds + j1;
-            int* x2p = XR + rc2 * ds * ds + jx * ds + j2;
+            const uint32_t xb = sXRy + (uint32_t)(jx * ds) * 4u;
+            const uint32_t x0p = xb + ((uint32_t)(rc0 * ds * ds) + j0) * 4u;
+            const uint32_t x1p = xb + ((uint32_t)(rc1 * ds * ds) + j1) * 4u;
+            const uint32_t x2p = xb + ((uint32_t)(rc2 * ds * ds) + j2) * 4u;
             const float wx0 = 1.f - ex;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float wx = kqa[k] ? ex : wx0;
               const float w0 = kqb[k] ? c0e : 1.f - c0e, w1 = kqb[k] ? c1e : 1.f - c1e,
                           w2 = kqb[k] ? c2e : 1.f - c2e;
-              atomicAdd(x0p + kxoff[k], __float_as_int(__fmaf_rn(s0v * wx, w0, 12582912.0f)) - 0x4B400000);
-              atomicAdd(x1p + kxoff[k], __float_as_int(__fmaf_rn(s1v * wx, w1, 12582912.0f)) - 0x4B400000);
-              atomicAdd(x2p + kxoff[k], __float_as_int(__fmaf_rn(s2v * wx, w2, 12582912.0f)) - 0x4B400000);
+              ared(x0p + kxoff[k], __float_as_int(__fmaf_rn(s0v * wx, w0, 12582912.0f)) - 0x4B400000);
+              ared(x1p + kxoff[k], __float_as_int(__fmaf_rn(s1v * wx, w1, 12582912.0f)) - 0x4B400000);
+              ared(x2p + kxoff[k], __float_as_int(__fmaf_rn(s2v * wx, w2, 12582912.0f)) - 0x4B400000);
             }
           }
         }
@@ -573,14 +588,16 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // this row's xc sums into E_xc and its x-vertex / guide-vertex sums;
       // the buffer is zeroed for row y + 2 (rows y + 1 use the other one)
       for (int i = threadIdx.x; i < xr_size; i += blockDim.x) {
-        const int v = XR[i];
+        const int v = XR[i] + XR[i + xr_size] + XR[i + 2 * xr_size];
+        XR[i] = 0;
+        XR[i + xr_size] = 0;
+        XR[i + 2 * xr_size] = 0;
         if (v != 0) {
           const int c = i / (ds * ds), r2 = i - c * ds * ds, vx = r2 / ds, vc = r2 - vx * ds;
           E_xc[i] += v;  // one writer per entry in this phase
           int* R = Rrow + (y & 1) * 6 * ds;
           atomicAdd(R + c * ds + vx, v);
           atomicAdd(R + 3 * ds + c * ds + vc, v);
-          XR[i] = 0;
         }
       }
       jy_prev = jy;
@@ -715,7 +732,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
   const size_t staged = (size_t)kBwdStaged * L.plane_floats * 4;
-  const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds + 6 * ds * ds) * 4;
+  const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds + 18 * ds * ds) * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
   float* tables = (float*)wp;
