@@ -142,6 +142,18 @@ __device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
 __device__ __forceinline__ float4 blds4(uint32_t a) {
   return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(a));
 }
+// Cyclic rotation of a channel triple by the lane's channel offset r (rot1:
+// r == 1, rot2: r == 2) with selects: (a, b, c) -> (b, c, a) / (c, a, b).
+template <typename T>
+__device__ __forceinline__ void rot3(bool rot1, bool rot2, T& a, T& b, T& c) {
+  const T a1 = rot1 ? b : (rot2 ? c : a);
+  const T b1 = rot1 ? c : (rot2 ? a : b);
+  const T c1 = rot1 ? a : (rot2 ? b : c);
+  a = a1;
+  b = b1;
+  c = c1;
+}
+
 // Shared-memory fixed-point add at a byte address (ATOMS.ADD, no return).
 __device__ __forceinline__ void ared(uint32_t addr, int v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -235,6 +247,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
   const int rc0 = lane % 3, rc1 = (lane + 1) % 3, rc2 = (lane + 2) % 3;  // lane's channel order
+  const bool rot1 = rc0 == 1, rot2 = rc0 == 2;  // (x0, x1, x2) -> (x_rc0, x_rc1, x_rc2)
   // lane's corner order: k-th corner = (k + lane/3) % 4, bit 0 the first
   // axis (LUT a / grid x), bit 1 the second (LUT b / grid guide)
   bool kqa[4], kqb[4];
@@ -476,9 +489,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // kqa / kqb, rc*): up to twelve lanes that share a cell hit twelve
           // different words.
           const float fs[3] = {f0 * S, f1 * S, f2 * S};
-          const float s0v = rc0 == 0 ? fs[0] : rc0 == 1 ? fs[1] : fs[2];
-          const float s1v = rc1 == 0 ? fs[0] : rc1 == 1 ? fs[1] : fs[2];
-          const float s2v = rc2 == 0 ? fs[0] : rc2 == 1 ? fs[1] : fs[2];
+          float s0v = fs[0], s1v = fs[1], s2v = fs[2];
+          rot3(rot1, rot2, s0v, s1v, s2v);
           {  // pixels past the row end carry g = 0: their adds are zeros at clamped cells
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
@@ -540,12 +552,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           // same corner x channel rotation ----
           {
             const uint32_t jcr = sr - kMagic, jcg = sg - kMagic, jcb = sb - kMagic;
-            const uint32_t j0 = rc0 == 0 ? jcr : rc0 == 1 ? jcg : jcb;
-            const uint32_t j1 = rc1 == 0 ? jcr : rc1 == 1 ? jcg : jcb;
-            const uint32_t j2 = rc2 == 0 ? jcr : rc2 == 1 ? jcg : jcb;
-            const float c0e = rc0 == 0 ? er : rc0 == 1 ? eg : eb;
-            const float c1e = rc1 == 0 ? er : rc1 == 1 ? eg : eb;
-            const float c2e = rc2 == 0 ? er : rc2 == 1 ? eg : eb;
+            uint32_t j0 = jcr, j1 = jcg, j2 = jcb;
+            rot3(rot1, rot2, j0, j1, j2);
+            float c0e = er, c1e = eg, c2e = eb;
+            rot3(rot1, rot2, c0e, c1e, c2e);
             const uint32_t xb = sXRy + (uint32_t)(jx * ds) * 4u;
             const uint32_t x0p = xb + ((uint32_t)(rc0 * ds * ds) + j0) * 4u;
             const uint32_t x1p = xb + ((uint32_t)(rc1 * ds * ds) + j1) * 4u;
