@@ -3,6 +3,10 @@
 // the two pipes overlap.  Throughput-bound loop (16 independent fetches per
 // iteration, the table fits in L1).
 //
+// With 2 or 3 LDS.128 (4 cycles each) per TLD: if the two pipes have
+// separate data paths the loop costs max(8, 4k) cycles per TLD, if they share
+// the L1 data SRAM port 4 + 4k.
+//
 // Question: is the texture path's cost per instruction fixed (~10 cycles, the
 // round-1 estimate) or does it drop when a warp's 32 lanes hit few cells
 // (decides where LUT pair gb lives).
@@ -27,7 +31,7 @@ constexpr int TEXELS = 4096;  // 64 KB
 __global__ void kern(cudaTextureObject_t t, const int* __restrict__ idx, int with_lds, float* out,
                      long long* cyc) {
   extern __shared__ float4 sm[];
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) sm[i] = make_float4(i, i, i, i);
+  for (int i = threadIdx.x; i < 1024 * 3; i += blockDim.x) sm[i] = make_float4(i, i, i, i);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int base = idx[lane];
@@ -43,13 +47,15 @@ __global__ void kern(cudaTextureObject_t t, const int* __restrict__ idx, int wit
                    : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                    : "l"(t), "r"(w + j * 64));
       acc += v.x;
-      if (with_lds) {
-        float x, y, z, q;
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(x), "=f"(y), "=f"(z), "=f"(q)
-                     : "r"(sb + (uint32_t)j * 512u));
-        acc += x;
-      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (k < with_lds) {  // with_lds LDS.128 (4 cycles each, distinct chunks) per TLD
+          float x, y, z, q;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(x), "=f"(y), "=f"(z), "=f"(q)
+                       : "r"(sb + (uint32_t)(j * 3 + k) * 512u));
+          acc += x + y + z + q;
+        }
     }
   }
   __syncthreads();
@@ -92,15 +98,16 @@ int main() {
   CK(cudaMalloc(&didx, 32 * sizeof(int)));
   CK(cudaMalloc(&out, sizeof(float) * nsm * threads));
   CK(cudaMalloc(&cyc, sizeof(long long) * nsm));
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384));
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 49152));
   long long* hc = new long long[nsm];
   for (auto& p : pats) {
     int h[32];
     for (int l = 0; l < 32; ++l) h[l] = p.f(l);
     CK(cudaMemcpy(didx, h, sizeof(h), cudaMemcpyHostToDevice));
-    for (int lds = 0; lds < 2; ++lds) {
+    for (int lds = 0; lds < 4; ++lds) {
+      if (lds > 1 && p.f != pats[0].f) continue;
       for (int rep = 0; rep < 2; ++rep) {
-        kern<<<nsm, threads, 16384>>>(tex, didx, lds, out, cyc);
+        kern<<<nsm, threads, 49152>>>(tex, didx, lds, out, cyc);
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
       }
@@ -108,7 +115,7 @@ int main() {
       double avg = 0;
       for (int s = 0; s < nsm; ++s) avg += (double)hc[s];
       avg /= nsm;
-      printf("%-36s %s cycles per warp TLD.128 per SM = %.3f\n", p.name, lds ? "+LDS.128" : "        ",
+      printf("%-36s +%d LDS.128  cycles per warp TLD.128 per SM = %.3f\n", p.name, lds,
              avg / ((double)ITERS * 8 * (threads / 32)));
     }
   }
