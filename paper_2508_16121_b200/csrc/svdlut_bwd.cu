@@ -5,20 +5,24 @@
 //
 // fused_bwd_kernel mirrors the forward kernel's structure (svdlut_fwd.cu):
 // persistent CTA per SM over a contiguous row range, the same packed
-// coefficient tables (LUT pair rb's chunk planes + the grid block staged in
-// shared memory by TMA, pairs rg and gb gathered through the texture path),
-// per-row merged grid slots.
+// coefficient tables (BWD_PLANES chunk planes staged in shared memory by TMA,
+// the others gathered through the texture path), per-row merged grid slots
+// (double buffered, one CTA barrier per row), warps on 128-pixel chunks with
+// lane = 4 consecutive pixels.
 //   gX    from the coefficient form: d/da (A + B a + C b + D a b) = B + D b,
 //         d/db = C + D a; grid slot d/dec = M' + N' ex; the strict clamp of
 //         interp.py:37-40 zeroes the gradient outside [0, 1].
 //   E     UNWEIGHTED scatter sums  E_lut[p][i][j][c] = sum gY_c w_ij and
 //         E_grid[q][c][a][b], accumulated per CTA in shared memory as 32-bit
-//         fixed point (native ATOMS.ADD; shared f32 atomics are CAS loops).
-//         A warp's lanes sit 60 px apart (unrelated cells on smooth images)
-//         and each lane issues its 36 LUT atomics in a lane-rotated corner /
-//         channel order, so lanes sharing a cell hit different banks; the xc
-//         / yc grid planes are summed in per-lane registers over runs of
-//         equal (x-cell, guide cell) and the xy plane per chunk.
+//         fixed point (native ATOMS.ADD; shared f32 / u64 atomics are CAS
+//         loops).  Per pixel: 36 LUT atomics (3 pairs x 4 corners x 3
+//         channels) and 12 into the row's xc plane; each lane issues them in
+//         a lane-rotated corner x channel order, so up to twelve neighbouring
+//         lanes that share a cell hit twelve different words (an ATOMS warp
+//         instruction costs ~3.1 cycles conflict-free and one more per extra
+//         lane on a word, tools/microbench/atomspat.cu).  The xy and yc
+//         planes are derived at the row's end from the row's xc sums
+//         (sum_vc wc = sum_vx wx = 1) and take the row's y weights.
 //   flush to the global f32 accumulators before any fixed-point partial can
 //         pass 2^31, and at the end of each image.
 // finalize_kernel: dlut = lw * E, dlw = <T, E>, dgrid[k,q] = gw[k,q] * E[q][k%3],
@@ -172,14 +176,7 @@ __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, floa
 // that bound or, with B = max|gY|, leave the rest of the image with too
 // coarse a resolution; they scatter through global f32 atomics instead
 // (rare by construction).  Conversion is an add of 1.5*2^23
-// (round to nearest even on the FMA pipe).  Shared integer atomics are native
-// (ATOMS.ADD, ~2 cycles per warp instruction with distinct addresses, measured
-// in tools/microbench/atomicbench.cu) whereas shared f32 atomics are CAS loops
-// (7 cycles, and ~multiplicity x worse under sharing).
-//   LUT   one atomic per value per pixel (lanes hold pixels 4 apart, so a warp
-//         instruction's cells rarely collide);
-//   grids per-lane runs over the lane's 4 consecutive pixels, then one loop
-//         over the distinct keys of the warp with full-mask REDUX sums.
+// (round to nearest even on the FMA pipe).
 // Shared sums are flushed to the global f32 accumulators at least every
 // row that could take one partial past 2^31: every shared partial is a sum
 // of at most one contribution (|v| <= 2^16) per pixel, so at most

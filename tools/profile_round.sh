@@ -18,10 +18,11 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:fuse
   -o gpurun_out/fwd_$R -f python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-extra > gpurun_out/fwd_ncu.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:fused_bwd_kernel -c 1 \
   -o gpurun_out/bwd_$R -f python tools/bwd_once.py > gpurun_out/bwd_ncu.log 2>&1
-for m in ldsclean texphase atomswidth shfllds; do
-  [ -x tools/microbench/$m ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench/$m tools/microbench/$m.cu
+for m in ldsclean texphase atomswidth atomspat shfllds; do
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench/$m tools/microbench/$m.cu
 done
 { ./tools/microbench/ldsclean tools/microbench/clean.txt; ./tools/microbench/ldsclean tools/microbench/clean2.txt;
-  ./tools/microbench/texphase; ./tools/microbench/atomswidth; ./tools/microbench/shfllds; } > gpurun_out/microbench_$R.txt 2>&1
+  ./tools/microbench/texphase; ./tools/microbench/atomswidth; ./tools/microbench/atomspat tools/microbench/bwd_atoms.txt;
+  ./tools/microbench/ldsclean tools/microbench/bwd_lds.txt; ./tools/microbench/shfllds; } > gpurun_out/microbench_$R.txt 2>&1
 timeout 600 python tools/runtime_table.py > gpurun_out/runtime_table_$R.txt 2>&1
 ls -la gpurun_out
