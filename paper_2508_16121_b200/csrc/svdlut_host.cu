@@ -103,6 +103,7 @@ struct svdlut_ctx {
   cudaEvent_t ev_in[kMaxStrips] = {};
   cudaEvent_t ev_k[kMaxStrips] = {};
   cudaEvent_t ev_out[kMaxStrips] = {};
+  cudaEvent_t ev_par = nullptr;  // parameters on the device
   void* d_img = nullptr;  // input strips followed by output strips
   size_t d_img_bytes = 0;
   void* d_par = nullptr;  // parameters + packed tables + workspaces
@@ -165,6 +166,7 @@ svdlut_ctx* svdlut_ctx_create(int device) {
     ok &= cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming) == cudaSuccess;
   }
+  ok &= cudaEventCreateWithFlags(&c->ev_par, cudaEventDisableTiming) == cudaSuccess;
   ok &= cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault) == cudaSuccess;
   if (!ok) {
     svdlut_ctx_destroy(c);
@@ -187,6 +189,7 @@ void svdlut_ctx_destroy(svdlut_ctx* c) {
   delete c->pool;
   for (int i = 0; i < 3; ++i)
     if (c->st[i]) cudaStreamDestroy(c->st[i]);
+  if (c->ev_par) cudaEventDestroy(c->ev_par);
   for (int i = 0; i < kMaxStrips; ++i) {
     if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
     if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
@@ -241,19 +244,6 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
   int* d_flag = (int*)(d_tables + rup(tb));
 
   cudaStream_t s_in = ctx->st[0], s_k = ctx->st[1], s_out = ctx->st[2];
-  // ---- parameters + table prologue on the compute stream --------------------
-  float* dst[6] = {d_lut, d_lw, d_lb, d_grid, d_gw, d_gb};
-  const float* src[6] = {lut_planes, lw, lb, grid_planes, gw, gb};
-  const size_t cnt[6] = {n_lut, 9, 3, n_grid, 3ull * k, (size_t)k};
-  for (int i = 0; i < 6; ++i)
-    if (cudaMemcpyAsync(dst[i], src[i], cnt[i] * 4, cudaMemcpyHostToDevice, s_k) != cudaSuccess)
-      return SVDLUT_ERR_CUDA;
-  if (cudaMemsetAsync(d_flag, 0, sizeof(int), s_k) != cudaSuccess) return SVDLUT_ERR_CUDA;
-  if (fast) {
-    int rc = svdlut_pack_tables(d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb, k, d_s, 1, d_tables, s_k);
-    if (rc != SVDLUT_OK) return rc;
-  }
-
   // ---- strip pipeline: H2D (s_in) -> kernel (s_k) -> D2H (s_out) ------------
   // ~12 MB strips at 4K: every copy has a fixed setup cost of several
   // microseconds, so fewer, larger copies win; the first strip is a quarter
@@ -307,9 +297,10 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
   // SVDLUT_TRACE=1 (development): per-strip H2D / kernel / D2H completion
   // times relative to the start of the call, printed to stderr
   static const bool trace = getenv("SVDLUT_TRACE") != nullptr;
-  cudaEvent_t tev[3 * kMaxStrips + 1];
+  cudaEvent_t tev[3 * kMaxStrips + 1], tks[kMaxStrips];
   if (trace) {
     for (auto& e : tev) cudaEventCreate(&e);
+    for (auto& e : tks) cudaEventCreate(&e);
     cudaEventRecord(tev[3 * kMaxStrips], s_k);
     cudaPointerAttributes ai, ao;
     const bool oki = cudaPointerGetAttributes(&ai, rgb) == cudaSuccess;
@@ -389,13 +380,10 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
       memcpy(parts[i].dst + off, parts[i].src + off, n);
     });
   };
-  for (int s = 0; s < n_strips; ++s) {
-    const int r0 = bounds[s], r1 = bounds[s + 1];
-    const int hs = r1 - r0;
-    // device layout: f32 strip-major (3, hs, w) at the strip's offset; HWC
-    // rows [r0, r1) contiguous, as on the host
+  // H2D of strip s on the copy-in stream, then its ev_in event
+  auto issue_h2d = [&](int s) -> int {
+    const int r0 = bounds[s], hs = bounds[s + 1] - bounds[s];
     char* din = d_in + (size_t)3 * r0 * w * ib;
-    char* dout = d_out + (size_t)3 * r0 * w * ob;
     if (stage_in) {  // slot s % 2 is free once the H2D of strip s - 2 is done
       if (s >= 2 && cudaEventSynchronize(ctx->ev_in[s - 2]) != cudaSuccess) return SVDLUT_ERR_CUDA;
       strip_copy(r0, hs, slot_in[s & 1], true);
@@ -412,7 +400,57 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     }
     if (trace) cudaEventRecord(tev[3 * s], s_in);
     if (cudaEventRecord(ctx->ev_in[s], s_in) != cudaSuccess) return SVDLUT_ERR_CUDA;
+    return SVDLUT_OK;
+  };
+  // ---- parameters + table prologue --------------------------------------------
+  // One async copy from the context's page-locked staging (a cudaMemcpyAsync
+  // from pageable memory blocks the host while the driver stages it), queued
+  // on the copy-in stream ahead of the first strip: copies share the H2D
+  // engine, and one queued on another stream behind the strips would hold the
+  // first kernel back until all of the input has arrived.
+  {
+    const size_t need = par_floats * 4;
+    if (ctx->h_stage_bytes < need) {
+      if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+      ctx->h_stage = nullptr;
+      ctx->h_stage_bytes = 0;
+      if (cudaHostAlloc((void**)&ctx->h_stage, need, cudaHostAllocDefault) != cudaSuccess)
+        return SVDLUT_ERR_CUDA;
+      ctx->h_stage_bytes = need;
+    }
+    const float* src[6] = {lut_planes, lw, lb, grid_planes, gw, gb};
+    const size_t cnt[6] = {n_lut, 9, 3, n_grid, 3ull * k, (size_t)k};
+    float* hp = ctx->h_stage;
+    for (int i = 0; i < 6; ++i) {
+      memcpy(hp, src[i], cnt[i] * 4);
+      hp += cnt[i];
+    }
+    if (cudaMemcpyAsync(d_lut, ctx->h_stage, need, cudaMemcpyHostToDevice, s_in) != cudaSuccess ||
+        cudaEventRecord(ctx->ev_par, s_in) != cudaSuccess || cudaStreamWaitEvent(s_k, ctx->ev_par, 0) != cudaSuccess)
+      return SVDLUT_ERR_CUDA;
+  }
+  if (!stage_in) {  // a page-locked input starts streaming right behind the parameters
+    const int rc = issue_h2d(0);
+    if (rc != SVDLUT_OK) return rc;
+  }
+  if (cudaMemsetAsync(d_flag, 0, sizeof(int), s_k) != cudaSuccess) return SVDLUT_ERR_CUDA;
+  if (fast) {
+    int rc = svdlut_pack_tables(d_lut, d_lw, d_lb, d_t, d_grid, d_gw, d_gb, k, d_s, 1, d_tables, s_k);
+    if (rc != SVDLUT_OK) return rc;
+  }
+  for (int s = 0; s < n_strips; ++s) {
+    const int r0 = bounds[s], r1 = bounds[s + 1];
+    const int hs = r1 - r0;
+    // device layout: f32 strip-major (3, hs, w) at the strip's offset; HWC
+    // rows [r0, r1) contiguous, as on the host
+    char* din = d_in + (size_t)3 * r0 * w * ib;
+    char* dout = d_out + (size_t)3 * r0 * w * ob;
+    if (s > 0 || stage_in) {
+      const int rc = issue_h2d(s);
+      if (rc != SVDLUT_OK) return rc;
+    }
     if (cudaStreamWaitEvent(s_k, ctx->ev_in[s], 0) != cudaSuccess) return SVDLUT_ERR_CUDA;
+    if (trace) cudaEventRecord(tks[s], s_k);
     if (fast) {
       if (launch_fused_fwd_io(din, in_fmt, dout, out_fmt, 1, hs, w, r0, h, (const float*)d_tables, L,
                               d_flag, s_k) != cudaSuccess)
@@ -450,11 +488,14 @@ static int enhance_host_impl(svdlut_ctx* ctx, const void* rgb, int in_fmt, int h
     cudaStreamSynchronize(s_out);
     fprintf(stderr, "host enqueue %.3f ms\n", enq_ms);
     for (int s = 0; s < n_strips; ++s) {
-      float t[3];
+      float t[4];
       for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], tev[3 * kMaxStrips], tev[3 * s + i]);
-      fprintf(stderr, "strip %2d  h2d done %7.3f  kernel done %7.3f  d2h done %7.3f ms\n", s, t[0], t[1], t[2]);
+      cudaEventElapsedTime(&t[3], tev[3 * kMaxStrips], tks[s]);
+      fprintf(stderr, "strip %2d  h2d done %7.3f  kernel start %7.3f done %7.3f  d2h done %7.3f ms\n", s, t[0],
+              t[3], t[1], t[2]);
     }
     for (auto& e : tev) cudaEventDestroy(e);
+    for (auto& e : tks) cudaEventDestroy(e);
   }
   if (stage_out) {
     for (int s = std::max(0, n_strips - 2); s < n_strips; ++s) {

@@ -29,7 +29,16 @@ for _ in range(10):
     t0 = time.perf_counter()
     transform.fused_enhance(img, svd.reconstruct_lut(f), lw, g, gw)
     ts.append(1e3 * (time.perf_counter() - t0))
-print("fused_enhance ms: " + " ".join(f"{t:.2f}" for t in ts), file=sys.stderr)
+print("reconstruct_lut + fused_enhance ms: " + " ".join(f"{t:.2f}" for t in ts), file=sys.stderr)
+luts = svd.reconstruct_lut(f)
+for name, fn in (("reconstruct_lut", lambda: svd.reconstruct_lut(f)),
+                 ("fused_enhance", lambda: transform.fused_enhance(img, luts, lw, g, gw))):
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(1e3 * (time.perf_counter() - t0))
+    print(f"{name} alone ms: " + " ".join(f"{t:.3f}" for t in sorted(ts)[:5]), file=sys.stderr)
 os.environ["SVDLUT_TRACE"] = "1"
 # bare duplex copies of the same bytes
 d_in = torch.empty((3, H, W), dtype=torch.float32, device="cuda")
