@@ -400,10 +400,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
 #pragma unroll
         for (int u = 0; u < kPx; ++u) {
           if ((u & 1) == 0) grid_brackets(u >> 1);
-          if (u == 2) {
-            colour_brackets(1);
-            tex_issue(2, tq, 0u);
-          }
+          if (u == 1) colour_brackets(1);  // pixel 2's texture gathers are issued during pixel 1
           const uint32_t br = bits(mcr[u >> 1], u), bg = bits(mcg[u >> 1], u), bb = bits(mcb[u >> 1], u);
           SVDLUT_CHECK(br - kMagicBits <= (uint32_t)(dt - 2) && bg - kMagicBits <= (uint32_t)(dt - 2) &&
                        bb - kMagicBits <= (uint32_t)(dt - 2));
@@ -432,7 +429,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
 #pragma unroll
           for (int idx = 0; idx < 9; ++idx)
             if (!plane_in_smem(idx)) c[idx] = tq[idx];
-          if (u + 1 < kPx && u != 1) {
+          if (u + 1 < kPx) {
             // next pixel's texture gathers, after this pixel's shared gathers;
             // the (never taken) dependency on the last LDS stops ptxas from
             // hoisting all of the chunk's TLDs to its top
