@@ -27,6 +27,7 @@
  *                             baseline, bitwise equal to the reference)
  *   svdlut_fused_fwd_l2       forward + L2 loss epilogue (training step, config 5)
  *   svdlut_fused_bwd_packed   svdlut_fused_bwd reusing the forward's tables / max|gY|
+ *   svdlut_fused_l2_step      forward + L2 loss + backward in one pass (training step)
  *   svdlut_occurrence         analysis.occurrence_stats (analysis.py:109-122), the
  *                             source of utilization_rate (analysis.py:74-106)
  *
@@ -231,6 +232,20 @@ int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h,
                             float* dlut_planes, float* dlw, float* dlb, float* dgrid_planes,
                             float* dgw, float* dgb, void* workspace, size_t workspace_bytes,
                             void* stream);
+
+/* One training step of mean((Y - target)^2) in a single pass over the pixels:
+ * Y from the forward's packed `tables` (svdlut_pack_tables, biases included),
+ * gy = gscale (Y - target) per pixel, then the backward of svdlut_fused_bwd
+ * (gx may be NULL).  loss_sum[b] = sum (Y - target)^2 over image b (f64,
+ * written).  The fixed-point bound of each CTA's rows comes from a probe of
+ * its first row and grows with the running min(max |gy|, 6 rms gy); pixels
+ * above it scatter through f32 atomics.  Workspace: svdlut_bwd_workspace_bytes. */
+int svdlut_fused_l2_step(const float* rgb, const float* target, int batch, int h, int w, int y0,
+                         int h_total, const void* tables, float gscale, const float* lut_planes,
+                         const float* lw, int d_t, const float* grid_planes, const float* gw, int k,
+                         int d_s, float* gx, float* dlut_planes, float* dlw, float* dlb,
+                         float* dgrid_planes, float* dgw, float* dgb, double* loss_sum, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* cube (d, d, d) u64, zeroed then filled: how often each cube vertex is a
  * corner of some pixel's bracketing cell, over a batch of (B, 3, H, W) images

@@ -56,6 +56,8 @@ _SIGS = {
                                  ctypes.c_float, _vp]),
     "svdlut_fused_bwd_packed": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp,
                                      _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "svdlut_fused_l2_step": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, ctypes.c_float, _vp, _vp, _i, _vp, _vp,
+                                  _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "svdlut_occurrence": (_i, [_vp, _i, _i, _i, _i, _vp, _vp]),
     "svdlut_fused_fwd_io": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _i, _i, _vp, _i, _vp, _vp]),
     "svdlut_enhance_host_io": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _i,

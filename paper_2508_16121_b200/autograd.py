@@ -52,22 +52,28 @@ def svdlut_apply(rgb, u, s, vt, lw, lb, grid_planes, gw, gb, y0=0, h_total=None)
     return SvdLutApply.apply(rgb, u, s, vt, lw, lb, grid_planes, gw, gb, y0, h_total)
 
 
-def l2_step(rgb, target, u, s, vt, lw, lb, grid_planes, gw, gb, need_gx=True):
+def l2_step(rgb, target, u, s, vt, lw, lb, grid_planes, gw, gb, need_gx=True, fused=True):
     """One training step of mean((Y - target)^2) without autograd overhead
-    (BASELINE config 5): tables from the factors, the forward with the loss
-    fused into its epilogue (Y never hits HBM; gY and max|gY| come out of the
-    same kernel), the backward reusing the forward's tables and max|gY|, and
+    (BASELINE config 5): tables from the factors, then the pixel work in one
+    pass (``fused=True``, svdlut_fused_l2_step: Y, the loss and gY are formed
+    per pixel and feed the backward directly, so neither Y nor gY touches
+    HBM), or as two kernels (``fused=False``: the forward with the loss fused
+    into its epilogue writes gY and max|gY|, the backward reads them), and
     the factor gradients.  Returns a dict with the scalar ``loss`` (float64
     tensor) and the gradients keyed like SvdLutApply's inputs.
     """
     planes = device.reconstruct(u, s, vt)
     tables = device.pack_tables(planes, lw, lb, grid_planes, gw, gb)
     gscale = 2.0 / rgb.numel()
-    gy, loss_sum, gmax = device.apply_l2(rgb, target, tables, gscale=gscale)
-    # sum gY^2 per image = gscale^2 * sum (Y - T)^2: sets the scatter's
-    # fixed-point bound (outlier residuals take the f32 path)
-    g = device.fused_backward(rgb, gy, planes, lw, grid_planes, gw, need_gx=need_gx, tables=tables,
-                              gmax=gmax, gsumsq=loss_sum * (gscale * gscale))
+    if fused:
+        loss_sum, g = device.fused_l2_step(rgb, target, tables, planes, lw, grid_planes, gw, gscale=gscale,
+                                           need_gx=need_gx)
+    else:
+        gy, loss_sum, gmax = device.apply_l2(rgb, target, tables, gscale=gscale)
+        # sum gY^2 per image = gscale^2 * sum (Y - T)^2: sets the scatter's
+        # fixed-point bound (outlier residuals take the f32 path)
+        g = device.fused_backward(rgb, gy, planes, lw, grid_planes, gw, need_gx=need_gx, tables=tables,
+                                  gmax=gmax, gsumsq=loss_sum * (gscale * gscale))
     du, ds, dvt = device.reconstruct_backward(u, s, vt, g["dlut_planes"])
     return {"loss": loss_sum.sum() / rgb.numel(), "gx": g["gx"], "u": du, "s": ds, "vt": dvt,
             "lw": g["dlw"], "lb": g["dlb"], "grid_planes": g["dgrid_planes"], "gw": g["dgw"],

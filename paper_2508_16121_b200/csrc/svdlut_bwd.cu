@@ -138,7 +138,51 @@ struct BwdParams {
   float* E;            // global accumulators, batch * A.total
   const float* gmax;   // per image max|gY|
   const double* gss;   // per image sum of gY^2 (may be NULL): outlier bound
+  // fused L2 step (L2 = true): `gy` is the target T, gY = gscale (Y - T) is
+  // formed per pixel from the tables, and sum (Y - T)^2 goes to loss[b]
+  float gscale;
+  double* loss;
 };
+
+// Per-pixel front end shared by the backward and the fused L2 step: the
+// colour / spatial brackets and the gathered coefficient cells and slots.
+struct PixFront {
+  uint32_t br, bg, bb;  // 2^23-biased LUT cell bits
+  uint32_t sr, sg, sb;  // 2^23-biased guide cell bits
+  int jx;
+  float dr, dg, db, er, eg, eb, ex;
+  float4 q[9];  // chunk planes: pair rg 0-2, rb 3-5, gb 6-8
+  float4 s[3];  // merged grid slots {M, M', N, N'} per channel
+};
+
+// Y of one pixel from its cells, the forward kernel's arithmetic
+// (svdlut_fwd.cu): per pair (A + B a) + (C + D a) b, then the slot term
+// (M + N ex) + (M' + N' ex) ec per channel.
+__device__ __forceinline__ float3 pix_y(const PixFront& F) {
+  float2 acc01;
+  float acc2;
+#pragma unroll
+  for (int pr = 0; pr < 3; ++pr) {
+    const float da = pr == 2 ? F.dg : F.dr, dbv = pr == 0 ? F.dg : F.db;
+    const float4 k0 = F.q[3 * pr], k1 = F.q[3 * pr + 1], k2 = F.q[3 * pr + 2];
+    const float2 s01 = __ffma2_rn(make_float2(k1.z, k1.w), make_float2(da, da), make_float2(k1.x, k1.y));
+    const float2 ts2 = __ffma2_rn(make_float2(k2.z, k2.w), make_float2(da, da), make_float2(k2.x, k2.y));
+    if (pr == 0) {
+      acc01 = __ffma2_rn(s01, make_float2(dbv, dbv),
+                         __ffma2_rn(make_float2(k0.z, k0.w), make_float2(da, da), make_float2(k0.x, k0.y)));
+      acc2 = __fmaf_rn(ts2.y, dbv, ts2.x);
+    } else {
+      acc01 = __ffma2_rn(make_float2(k0.z, k0.w), make_float2(da, da), __fadd2_rn(acc01, make_float2(k0.x, k0.y)));
+      acc01 = __ffma2_rn(s01, make_float2(dbv, dbv), acc01);
+      acc2 = __fmaf_rn(ts2.y, dbv, acc2 + ts2.x);
+    }
+  }
+  const float2 p0 = __ffma2_rn(make_float2(F.s[0].z, F.s[0].w), make_float2(F.ex, F.ex), make_float2(F.s[0].x, F.s[0].y));
+  const float2 p1 = __ffma2_rn(make_float2(F.s[1].z, F.s[1].w), make_float2(F.ex, F.ex), make_float2(F.s[1].x, F.s[1].y));
+  const float2 p2 = __ffma2_rn(make_float2(F.s[2].z, F.s[2].w), make_float2(F.ex, F.ex), make_float2(F.s[2].x, F.s[2].y));
+  const float2 o01 = __fadd2_rn(acc01, make_float2(__fmaf_rn(p0.y, F.er, p0.x), __fmaf_rn(p1.y, F.eg, p1.x)));
+  return make_float3(o01.x, o01.y, acc2 + __fmaf_rn(p2.y, F.eb, p2.x));
+}
 
 __device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -184,6 +228,10 @@ __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, floa
 constexpr int kMaxFlushPx = 32767;
 constexpr float kFixedOne = 65536.0f;
 constexpr float kOutlierSigmas = 6.0f;
+#ifndef BWD_L2_HEADROOM
+#define BWD_L2_HEADROOM 1.5f
+#endif
+constexpr float kL2Headroom = BWD_L2_HEADROOM;  // fused L2 step: bound = headroom x the row statistic
 __device__ __forceinline__ int to_fixed(float v, float S) {
   return __float_as_int(__fmaf_rn(v, S, 12582912.0f)) - 0x4B400000;
 }
@@ -231,10 +279,14 @@ __device__ __forceinline__ void bload_chunk(const float* X, const float* GY, lon
   bload4(GY + 2 * pl + ro, c.y2, x, w, vec);
 }
 
-template <int DT, int DS>
+template <int DT, int DS, bool L2>
 __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams p) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar_storage;
+  // fused L2 step: max |gY|, sum gY^2 and the number of pixels above the
+  // bound, of the probe row and of each row (row parity)
+  __shared__ float s_max[3], s_ss[3];
+  __shared__ int s_nbig[3];
   const int dt = DT ? DT : p.L.dt;
   const int ds = DS ? DS : p.L.ds;
   const TableLayout L = TableLayout::make(dt, ds);
@@ -341,11 +393,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         }
     }
     for (int i = threadIdx.x; i < A.total + 12 * ds + 6 * xr_size; i += blockDim.x) Ei[i] = 0;
-    float gm = p.gmax[b];
-    if (p.gss) gm = fminf(gm, kOutlierSigmas * (float)sqrt(p.gss[b] / (3.0 * (double)pl)));
-    const float S = gm > 0.f ? kFixedOne / gm : 1.0f;  // fixed-point scale of this image
-    const float bound = gm > 0.f ? gm : 3.4e38f;       // |gY| above: global slow path
-    const float invS = 1.0f / S;
+    float gm = 0.f;
+    if (!L2) {
+      gm = p.gmax[b];
+      if (p.gss) gm = fminf(gm, kOutlierSigmas * (float)sqrt(p.gss[b] / (3.0 * (double)pl)));
+    }
+    float S = gm > 0.f ? kFixedOne / gm : 1.0f;  // fixed-point scale of this image (segment)
+    float bound = gm > 0.f ? gm : 3.4e38f;       // |gY| above: global slow path
+    float invS = 1.0f / S;
     float* Eg = p.E + (long long)b * A.total;
     int px_since_flush = 0;
     const float* X = p.rgb + (long long)b * 3 * pl;
@@ -378,6 +433,92 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     produce_rows(y_first);
     __syncthreads();
     float gsum0 = 0.f, gsum1 = 0.f, gsum2 = 0.f;
+    // brackets and gathers of the pixel at column xpix with samples (Xr, Xg, Xb)
+    auto front = [&](PixFront& F, float Xr, float Xg, float Xb, int xpix, uint32_t slotK) {
+      const float qr = __saturatef(Xr), qg = __saturatef(Xg), qb = __saturatef(Xb);
+      F.br = bbracket(qr, tdm1, tdm2, F.dr);
+      F.bg = bbracket(qg, tdm1, tdm2, F.dg);
+      F.bb = bbracket(qb, tdm1, tdm2, F.db);
+      F.jx = (int)(col_bracket(min(xpix, p.w - 1), p.rcp_w, sdm1, sdm2, F.ex) - kMagic);
+      F.sr = bbracket(qr, sdm1, sdm2, F.er);
+      F.sg = bbracket(qg, sdm1, sdm2, F.eg);
+      F.sb = bbracket(qb, sdm1, sdm2, F.eb);
+      SVDLUT_CHECK(F.br - kMagic <= (uint32_t)(dt - 2) && F.bg - kMagic <= (uint32_t)(dt - 2) &&
+                   F.bb - kMagic <= (uint32_t)(dt - 2) && F.jx >= 0 && F.jx <= ds - 2 &&
+                   F.sr - kMagic <= (uint32_t)(ds - 2) && F.sg - kMagic <= (uint32_t)(ds - 2) &&
+                   F.sb - kMagic <= (uint32_t)(ds - 2));
+      F.q[0] = bfetch<0>(ad, F.br, F.bg);
+      F.q[1] = bfetch<1>(ad, F.br, F.bg);
+      F.q[2] = bfetch<2>(ad, F.br, F.bg);
+      F.q[3] = bfetch<3>(ad, F.br, F.bb);
+      F.q[4] = bfetch<4>(ad, F.br, F.bb);
+      F.q[5] = bfetch<5>(ad, F.br, F.bb);
+      F.q[6] = bfetch<6>(ad, F.bg, F.bb);
+      F.q[7] = bfetch<7>(ad, F.bg, F.bb);
+      F.q[8] = bfetch<8>(ad, F.bg, F.bb);
+      const uint32_t sa = slotK + (uint32_t)F.jx * jx_bytes;
+      F.s[0] = blds4(sa + F.sr * 16u);
+      F.s[1] = blds4(sa + chan_bytes + F.sg * 16u);
+      F.s[2] = blds4(sa + 2u * chan_bytes + F.sb * 16u);
+    };
+    // Fused L2 step: the fixed-point bound of this CTA's image segment comes
+    // from its first row (a forward-only probe pass), B = 1.5 min(max |gY|,
+    // 6 rms gY) of that row; pixels above B take the f32 slow path.  When
+    // more than 1/64 of a row's pixels did, B is raised to max(2 B, 1.5 x the
+    // row's own min(max, 6 rms)) after the partials at the old scale are
+    // flushed — sparse outliers never move it, growing residuals do.
+    float loss_acc = 0.f;
+    auto set_bound = [&](float bnd) {
+      S = bnd > 0.f ? kFixedOne / bnd : 1.0f;
+      bound = bnd > 0.f ? bnd : 0.f;
+      invS = 1.0f / S;
+    };
+    auto warp_stats = [&](float m, float ss, int nbig, int slot) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        m = fmaxf(m, __shfl_xor_sync(full, m, off));
+        ss += __shfl_xor_sync(full, ss, off);
+        nbig += __shfl_xor_sync(full, nbig, off);
+      }
+      if (lane == 0) {
+        atomicMax(reinterpret_cast<int*>(&s_max[slot]), __float_as_int(m));  // m >= 0
+        atomicAdd(&s_ss[slot], ss);
+        atomicAdd(&s_nbig[slot], nbig);
+      }
+    };
+    auto row_bound = [&](int slot) {  // with headroom for the rows after it
+      return kL2Headroom * fminf(s_max[slot], kOutlierSigmas * sqrtf(s_ss[slot] / (3.f * (float)p.w)));
+    };
+    if (L2) {
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < 3; ++i) {
+          s_max[i] = s_ss[i] = 0.f;
+          s_nbig[i] = 0;
+        }
+      }
+      __syncthreads();
+      float pm = 0.f, ps = 0.f;
+      for (int x0 = warp * 128; x0 < p.w; x0 += kBwdWarps * 128) {
+        const int xl = x0 + 4 * lane;
+        BChunk cur;
+        bload_chunk(X, GY, pl, y_first, x0, p.w, lane, vec, cur);
+#pragma unroll
+        for (int u = 0; u < kBPx; ++u) {
+          PixFront F;
+          front(F, cur.r[u], cur.g[u], cur.b[u], xl + u, slotK0);
+          const float3 Y = pix_y(F);
+          const bool valid = xl + u < p.w;
+          const float g0 = valid ? (Y.x - cur.y0[u]) * p.gscale : 0.f;
+          const float g1 = valid ? (Y.y - cur.y1[u]) * p.gscale : 0.f;
+          const float g2 = valid ? (Y.z - cur.y2[u]) * p.gscale : 0.f;
+          pm = fmaxf(pm, fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))));
+          ps = __fmaf_rn(g0, g0, __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, ps)));
+        }
+      }
+      warp_stats(pm, ps, 0, 2);
+      __syncthreads();
+      set_bound(row_bound(2));
+    }
     // Rrow[par] = [Rx[c][vx] = sum g_c wx | Rc[c][vc] = sum g_c wc] of one row
     // into the xy / yc planes with that row's y weights, then zeroed
     auto fold_rows = [&](int par, int jyr, float eyr) {
@@ -417,6 +558,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // corner x channel rotation (3.6 cycles per ATOMS instead of 10).
       int* XR = XRrow + (y & 1) * 3 * xr_size;
       const uint32_t sXRy = sXR + (uint32_t)((y & 1) * 3 * xr_size) * 4u;
+      float row_max = 0.f, row_ss = 0.f;  // fused L2 step: this thread's |gY| statistics of row y
+      int row_big = 0;
       for (int x0 = warp * 128; x0 < p.w; x0 += kBwdWarps * 128) {
         const int xl = x0 + 4 * lane;
         if (xl >= p.w) continue;
@@ -426,56 +569,58 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
 #pragma unroll
         for (int u = 0; u < kBPx; ++u) {
           const bool valid = xl + u < p.w;
-          const float g0 = valid ? cur.y0[u] : 0.f, g1 = valid ? cur.y1[u] : 0.f,
-                      g2 = valid ? cur.y2[u] : 0.f;
+          const float Xr = cur.r[u], Xg = cur.g[u], Xb = cur.b[u];
+          PixFront F;
+          front(F, Xr, Xg, Xb, xl + u, slotK);
+          float g0, g1, g2;
+          if (L2) {  // gY = gscale (Y - T); the loss sums (Y - T)^2
+            const float3 Y = pix_y(F);
+            const float r0 = valid ? Y.x - cur.y0[u] : 0.f, r1 = valid ? Y.y - cur.y1[u] : 0.f,
+                        r2 = valid ? Y.z - cur.y2[u] : 0.f;
+            loss_acc = __fmaf_rn(r0, r0, __fmaf_rn(r1, r1, __fmaf_rn(r2, r2, loss_acc)));
+            g0 = r0 * p.gscale;
+            g1 = r1 * p.gscale;
+            g2 = r2 * p.gscale;
+            row_max = fmaxf(row_max, fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))));
+            row_ss = __fmaf_rn(g0, g0, __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, row_ss)));
+          } else {
+            g0 = valid ? cur.y0[u] : 0.f;
+            g1 = valid ? cur.y1[u] : 0.f;
+            g2 = valid ? cur.y2[u] : 0.f;
+          }
           // outliers take the f32 slow path; the fixed-point path sees zeros
           const bool big = fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))) > bound;
           const float f0 = big ? 0.f : g0, f1 = big ? 0.f : g1, f2 = big ? 0.f : g2;
+          if (L2) row_big += big ? 1 : 0;
           gsum0 += g0;
           gsum1 += g1;
           gsum2 += g2;
-          const float Xr = cur.r[u], Xg = cur.g[u], Xb = cur.b[u];
-          const float qr = __saturatef(Xr), qg = __saturatef(Xg), qb = __saturatef(Xb);
-          float dr, dg, db;
-          const uint32_t br = bbracket(qr, tdm1, tdm2, dr);
-          const uint32_t bg = bbracket(qg, tdm1, tdm2, dg);
-          const uint32_t bb = bbracket(qb, tdm1, tdm2, db);
-          float ex;
-          const int jx = (int)(col_bracket(min(xl + u, p.w - 1), p.rcp_w, sdm1, sdm2, ex) - kMagic);
-          float er, eg, eb;
-          const uint32_t sr = bbracket(qr, sdm1, sdm2, er);
-          const uint32_t sg = bbracket(qg, sdm1, sdm2, eg);
-          const uint32_t sb = bbracket(qb, sdm1, sdm2, eb);
-          SVDLUT_CHECK(br - kMagic <= (uint32_t)(dt - 2) && bg - kMagic <= (uint32_t)(dt - 2) &&
-                       bb - kMagic <= (uint32_t)(dt - 2) && jx >= 0 && jx <= ds - 2 &&
-                       sr - kMagic <= (uint32_t)(ds - 2) && sg - kMagic <= (uint32_t)(ds - 2) &&
-                       sb - kMagic <= (uint32_t)(ds - 2) && jy >= 0 && jy <= ds - 2);
+          const uint32_t br = F.br, bg = F.bg, bb = F.bb, sr = F.sr, sg = F.sg, sb = F.sb;
+          const int jx = F.jx;
+          const float dr = F.dr, dg = F.dg, db = F.db, er = F.er, eg = F.eg, eb = F.eb, ex = F.ex;
+          SVDLUT_CHECK(jy >= 0 && jy <= ds - 2);
           // ---- input gradient from the coefficient cells ----
-          float gar = 0.f, gag = 0.f, gab = 0.f;
           // chunks {A0 A1 B0 B1} {C0 C1 D0 D1} {A2 C2 B2 D2} (svdlut_common.cuh):
           // d/da = B + D b, d/db = C + D a per channel
+          float gar = 0.f, gag = 0.f, gab = 0.f;
           {
-            const float4 c0 = bfetch<0>(ad, br, bg), c1 = bfetch<1>(ad, br, bg), c2 = bfetch<2>(ad, br, bg);  // rg
+            const float4 c0 = F.q[0], c1 = F.q[1], c2 = F.q[2];  // rg
             gar += g0 * __fmaf_rn(c1.z, dg, c0.z) + g1 * __fmaf_rn(c1.w, dg, c0.w) + g2 * __fmaf_rn(c2.w, dg, c2.z);
             gag += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            const float4 c0 = bfetch<3>(ad, br, bb), c1 = bfetch<4>(ad, br, bb), c2 = bfetch<5>(ad, br, bb);  // rb
+            const float4 c0 = F.q[3], c1 = F.q[4], c2 = F.q[5];  // rb
             gar += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dr, c1.x) + g1 * __fmaf_rn(c1.w, dr, c1.y) + g2 * __fmaf_rn(c2.w, dr, c2.y);
           }
           {
-            const float4 c0 = bfetch<6>(ad, bg, bb), c1 = bfetch<7>(ad, bg, bb), c2 = bfetch<8>(ad, bg, bb);  // gb
+            const float4 c0 = F.q[6], c1 = F.q[7], c2 = F.q[8];  // gb
             gag += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dg, c1.x) + g1 * __fmaf_rn(c1.w, dg, c1.y) + g2 * __fmaf_rn(c2.w, dg, c2.y);
           }
-          const uint32_t sa = slotK + (uint32_t)jx * jx_bytes;
-          const float4 s0 = blds4(sa + sr * 16u);
-          const float4 s1 = blds4(sa + chan_bytes + sg * 16u);
-          const float4 s2 = blds4(sa + 2u * chan_bytes + sb * 16u);
-          const float gsr = g0 * __fmaf_rn(s0.w, ex, s0.y);  // slot {M, M', N, N'}
-          const float gsg = g1 * __fmaf_rn(s1.w, ex, s1.y);
-          const float gsb = g2 * __fmaf_rn(s2.w, ex, s2.y);
+          const float gsr = g0 * __fmaf_rn(F.s[0].w, ex, F.s[0].y);  // slot {M, M', N, N'}
+          const float gsg = g1 * __fmaf_rn(F.s[1].w, ex, F.s[1].y);
+          const float gsb = g2 * __fmaf_rn(F.s[2].w, ex, F.s[2].y);
           oxr[u] = (Xr < 0.f || Xr > 1.f) ? 0.f : __fmaf_rn(gar, tdm1, gsr * sdm1);
           oxg[u] = (Xg < 0.f || Xg > 1.f) ? 0.f : __fmaf_rn(gag, tdm1, gsg * sdm1);
           oxb[u] = (Xb < 0.f || Xb > 1.f) ? 0.f : __fmaf_rn(gab, tdm1, gsb * sdm1);
@@ -587,8 +732,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         }
       }
       px_since_flush += p.w;
+      if (L2) warp_stats(row_max, row_ss, row_big, y & 1);
       if (y < y_last) produce_rows(y + 1);  // the other half of the ring
       __syncthreads();
+      if (L2 && threadIdx.x == 0) {  // row y + 1's statistics slot (row y - 1's was read last row)
+        s_max[(y + 1) & 1] = 0.f;
+        s_ss[(y + 1) & 1] = 0.f;
+        s_nbig[(y + 1) & 1] = 0;
+      }
       // the previous row's x-vertex / guide-vertex sums (complete since the
       // barrier) into the xy / yc planes with that row's y weights
       if (y > y_first) fold_rows((y - 1) & 1, jy_prev, ey_prev);
@@ -609,6 +760,26 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       }
       jy_prev = jy;
       ey_prev = ey;
+      if (L2 && y < y_last && s_nbig[y & 1] * 64 > p.w) {
+        // every thread reads the same row statistics: raise the bound after
+        // moving every partial at the old scale to the global f32 sums
+        const float bnd = fmaxf(2.f * bound, row_bound(y & 1));
+        {
+          __syncthreads();                 // the xc fold of row y has landed
+          fold_rows(y & 1, jy, ey);        // row y's x / guide vertex sums, old scale
+          __syncthreads();
+          for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
+            const int v = Ei[i];
+            if (v != 0) {
+              atomicAdd(Eg + i, (float)v * invS);
+              Ei[i] = 0;
+            }
+          }
+          __syncthreads();
+          set_bound(bnd);
+          px_since_flush = 0;
+        }
+      }
       if (px_since_flush + p.w > kMaxFlushPx && y < y_last) {  // keep shared partials < 2^31
         __syncthreads();  // the fold has landed
         for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
@@ -635,6 +806,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       atomicAdd(Eg + A.gsum_off + 0, gsum0);
       atomicAdd(Eg + A.gsum_off + 1, gsum1);
       atomicAdd(Eg + A.gsum_off + 2, gsum2);
+    }
+    if (L2) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) loss_acc += __shfl_xor_sync(full, loss_acc, off);
+      if (lane == 0) atomicAdd(p.loss + b, (double)loss_acc);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < A.gsum_off; i += blockDim.x) {
@@ -728,13 +904,18 @@ __global__ void gy_stats_kernel(const float* __restrict__ gy, long long per_img,
   }
 }
 
-cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w, int y0,
-                             int h_total, const float* lp, const float* lw, int dt,
-                             const float* gp, const float* gw, int k, int ds, float* gx,
-                             float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
-                             float* dgb, void* ws, size_t ws_bytes, cudaStream_t st,
-                             const float* tables_in, const float* gmax_in, const double* gss_in) {
-  (void)ws_bytes;
+// The backward (target == NULL: gy given) or the fused L2 training step
+// (target != NULL: gy = gscale (Y - target) formed per pixel from
+// `tables_in`, which must be the forward's packed tables; loss[b] += sum
+// (Y - target)^2, zeroed here).
+static cudaError_t bwd_impl(const float* rgb, const float* gy, int batch, int h, int w, int y0,
+                            int h_total, const float* lp, const float* lw, int dt, const float* gp,
+                            const float* gw, int k, int ds, float* gx, float* dlp, float* dlw, float* dlb,
+                            float* dgp, float* dgw, float* dgb, void* ws, cudaStream_t st,
+                            const float* tables_in, const float* gmax_in, const double* gss_in,
+                            const float* target, float gscale, double* loss) {
+  const bool l2 = target != nullptr;
+  if (l2 && (!tables_in || !loss)) return cudaErrorInvalidValue;
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
@@ -753,7 +934,9 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   double* gss = (double*)wp;
   cudaError_t e;
   if ((e = cudaMemsetAsync(zb, 0, (size_t)batch * (3 + k) * 4, st)) != cudaSuccess) return e;
-  if (gmax_in) {
+  if (l2) {
+    if ((e = cudaMemsetAsync(loss, 0, (size_t)batch * 8, st)) != cudaSuccess) return e;
+  } else if (gmax_in) {
     gmax = const_cast<float*>(gmax_in);  // caller-provided max |gY| per image
     gss = const_cast<double*>(gss_in);   // and sum gY^2 (may be NULL: bound = max)
   } else {
@@ -776,7 +959,9 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   }
   BwdParams p;
   p.rgb = rgb;
-  p.gy = gy;
+  p.gy = l2 ? target : gy;
+  p.gscale = gscale;
+  p.loss = loss;
   p.gx = gx;
   p.batch = batch;
   p.h = h;
@@ -798,13 +983,15 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     long long grid = sms < rows ? sms : rows;
     const bool spec = dt == 33 && ds == 17;
-    auto kern = spec ? fused_bwd_kernel<33, 17> : fused_bwd_kernel<0, 0>;
+    auto kern = l2 ? (spec ? fused_bwd_kernel<33, 17, true> : fused_bwd_kernel<0, 0, true>)
+                   : (spec ? fused_bwd_kernel<33, 17, false> : fused_bwd_kernel<0, 0, false>);
+    const int inst = (spec ? 1 : 0) + (l2 ? 2 : 0);
     // Attributes set once per (instantiation, device) to the largest request
     // any launch may make, so concurrent launches never see the limit lowered
     // under them (as for the forward kernel).
     constexpr int kMaxDev = 64;
-    static std::atomic<int> configured[kMaxDev][2];
-    if (dev >= kMaxDev || configured[dev][spec].load(std::memory_order_acquire) == 0) {
+    static std::atomic<int> configured[kMaxDev][4];
+    if (dev >= kMaxDev || configured[dev][inst].load(std::memory_order_acquire) == 0) {
       if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     fwd_max_smem_bytes())) != cudaSuccess)
         return e;
@@ -814,7 +1001,7 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
       if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     pct > 100 ? 100 : pct)) != cudaSuccess)
         return e;
-      if (dev < kMaxDev) configured[dev][spec].store(1, std::memory_order_release);
+      if (dev < kMaxDev) configured[dev][inst].store(1, std::memory_order_release);
     }
     kern<<<(int)grid, kBwdWarps * 32, smem, st>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -823,6 +1010,26 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
   dim3 fg(9 + 3 * k, batch);
   finalize_kernel<<<fg, 256, 0, st>>>(lp, lw, gp, gw, k, A, E, dlp, dlw, dlb, dgp, dgw, dgb);
   return cudaGetLastError();
+}
+
+cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h, int w, int y0,
+                             int h_total, const float* lp, const float* lw, int dt,
+                             const float* gp, const float* gw, int k, int ds, float* gx,
+                             float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
+                             float* dgb, void* ws, size_t ws_bytes, cudaStream_t st,
+                             const float* tables_in, const float* gmax_in, const double* gss_in) {
+  (void)ws_bytes;
+  return bwd_impl(rgb, gy, batch, h, w, y0, h_total, lp, lw, dt, gp, gw, k, ds, gx, dlp, dlw, dlb, dgp, dgw,
+                  dgb, ws, st, tables_in, gmax_in, gss_in, nullptr, 0.f, nullptr);
+}
+
+cudaError_t launch_fused_l2_step(const float* rgb, const float* target, int batch, int h, int w, int y0,
+                                 int h_total, const float* tables, float gscale, const float* lp,
+                                 const float* lw, int dt, const float* gp, const float* gw, int k, int ds,
+                                 float* gx, float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
+                                 float* dgb, double* loss, void* ws, cudaStream_t st) {
+  return bwd_impl(rgb, nullptr, batch, h, w, y0, h_total, lp, lw, dt, gp, gw, k, ds, gx, dlp, dlw, dlb, dgp,
+                  dgw, dgb, ws, st, tables, nullptr, nullptr, target, gscale, loss);
 }
 
 // dU[i,m] = S[m] * sum_j dT[i,j] Vt[m,j]; dS[m] = sum_ij dT[i,j] U[i,m] Vt[m,j];

@@ -404,6 +404,35 @@ int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h,
   return SVDLUT_OK;
 }
 
+int svdlut_fused_l2_step(const float* rgb, const float* target, int batch, int h, int w, int y0,
+                         int h_total, const void* tables, float gscale, const float* lut_planes,
+                         const float* lw, int d_t, const float* grid_planes, const float* gw, int k,
+                         int d_s, float* gx, float* dlut_planes, float* dlw, float* dlb,
+                         float* dgrid_planes, float* dgw, float* dgb, double* loss_sum, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  int rc;
+  if ((rc = check_k(k)) != SVDLUT_OK) return rc;
+  if ((rc = check_image(batch, h, w, y0, h_total)) != SVDLUT_OK) return rc;
+  if ((rc = check_dims(d_t, d_s)) != SVDLUT_OK) return rc;
+  if (!svdlut_fast_supported(d_t, d_s))
+    return fail(SVDLUT_ERR_UNSUPPORTED, "tables for d_t=%d d_s=%d exceed shared memory", d_t, d_s);
+  if (w > 32767)
+    return fail(SVDLUT_ERR_UNSUPPORTED, "backward rows are limited to 32767 pixels (got %d)", w);
+  if (batch == 0) return SVDLUT_OK;
+  if (!rgb || !target || !tables || !lut_planes || !lw || !grid_planes || !gw || !dlut_planes || !dlw ||
+      !dlb || !dgrid_planes || !dgw || !dgb || !loss_sum)
+    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if (!aligned16(tables)) return fail(SVDLUT_ERR_INVALID_ARGUMENT, "tables must be 16-byte aligned");
+  const size_t need = bwd_workspace_bytes(batch, h, w, d_t, d_s, k);
+  if (!workspace || workspace_bytes < need)
+    return fail(SVDLUT_ERR_INVALID_ARGUMENT, "workspace too small (%zu < %zu)", workspace_bytes, need);
+  CUDA_TRY(launch_fused_l2_step(rgb, target, batch, h, w, y0, h_total, (const float*)tables, gscale, lut_planes,
+                                lw, d_t, grid_planes, gw, k, d_s, gx, dlut_planes, dlw, dlb, dgrid_planes, dgw,
+                                dgb, loss_sum, workspace, (cudaStream_t)stream),
+           "fused L2 step");
+  return SVDLUT_OK;
+}
+
 int svdlut_reconstruct_bwd(const float* u, const float* s, const float* vt,
                            const float* dplanes, int batch, int d_t, int n_s, float* du,
                            float* ds, float* dvt, void* stream) {

@@ -65,6 +65,11 @@ cudaError_t launch_fused_bwd(const float* rgb, const float* gy, int batch, int h
                              const float* tables_in = nullptr, const float* gmax_in = nullptr,
                              const double* gss_in = nullptr);
 size_t bwd_workspace_bytes(int batch, int h, int w, int dt, int ds, int k);
+cudaError_t launch_fused_l2_step(const float* rgb, const float* target, int batch, int h, int w, int y0,
+                                 int h_total, const float* tables, float gscale, const float* lp,
+                                 const float* lw, int dt, const float* gp, const float* gw, int k, int ds,
+                                 float* gx, float* dlp, float* dlw, float* dlb, float* dgp, float* dgw,
+                                 float* dgb, double* loss, void* ws, cudaStream_t st);
 
 cudaError_t launch_reconstruct_bwd(const float* u, const float* s, const float* vt,
                                    const float* dplanes, int batch, int dt, int ns, float* du,

@@ -27,7 +27,7 @@ __all__ = [
     "table_bytes", "fast_supported", "PackedTables", "reconstruct", "pack_tables",
     "pack_tables_factors", "apply",
     "apply_exact", "slice_grids", "apply_lut2d", "combine_slices", "apply_lut3d",
-    "fused_forward", "indices", "fused_backward", "reconstruct_backward",
+    "fused_forward", "indices", "fused_backward", "fused_l2_step", "reconstruct_backward",
 ]
 
 
@@ -369,6 +369,49 @@ def fused_backward(rgb, gy, lut_planes, lw, grid_planes, gw, y0=0, h_total=None,
               _p(g["dlb"]), _p(g["dgrid_planes"]), _p(g["dgw"]), _p(g["dgb"]), _p(ws), ws_bytes,
               _stream(rgb))
     return g
+
+
+def fused_l2_step(rgb, target, tables, lut_planes, lw, grid_planes, gw, gscale=None, y0=0, h_total=None,
+                  need_gx=True):
+    """One pass of the training step's pixel work: Y from ``tables`` (the
+    forward's PackedTables), gy = gscale (Y - target) (default 2/N, i.e.
+    d mean((Y-T)^2)/dY), and the backward of fused_backward — without gy or Y
+    touching HBM.  Returns (loss_sum (B,) float64 per-image sum of squared
+    residuals, dict(gx, dlut_planes, dlw, dlb, dgrid_planes, dgw, dgb)).
+    """
+    lp = _f32(lut_planes, "lut_planes", 5)
+    lw = _f32(lw, "lw", 3)
+    gp = _f32(grid_planes, "grid_planes", 5)
+    gw = _f32(gw, "gw", 3)
+    b, d_t = lp.shape[0], lp.shape[3]
+    k, d_s = gp.shape[1], gp.shape[3]
+    rgb = _image(rgb, b)
+    target = _image(target, b)
+    if target.shape != rgb.shape:
+        raise DimensionMismatch("target must be shaped like rgb")
+    if tables.batch != b or tables.d_t != d_t or tables.d_s != d_s:
+        raise DimensionMismatch("tables do not match the LUT / grid planes")
+    _, _, h, w = rgb.shape
+    h_total = h if h_total is None else h_total
+    gscale = 2.0 / rgb.numel() if gscale is None else float(gscale)
+    dev = rgb.device
+    g = dict(
+        gx=torch.empty_like(rgb) if need_gx else None,
+        dlut_planes=torch.empty_like(lp),
+        dlw=torch.empty((b, 3, 3), dtype=torch.float32, device=dev),
+        dlb=torch.empty((b, 3), dtype=torch.float32, device=dev),
+        dgrid_planes=torch.empty_like(gp),
+        dgw=torch.empty((b, k, 3), dtype=torch.float32, device=dev),
+        dgb=torch.empty((b, k), dtype=torch.float32, device=dev),
+    )
+    loss = torch.empty(b, dtype=torch.float64, device=dev)
+    ws_bytes = int(_lib.load().svdlut_bwd_workspace_bytes(b, h, w, d_t, d_s, k))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    _call(rgb, "svdlut_fused_l2_step", _p(rgb), _p(target), b, h, w, y0, h_total, _p(tables.buf),
+          ctypes.c_float(gscale), _p(lp), _p(lw), d_t, _p(gp), _p(gw), k, d_s, _p(g["gx"]),
+          _p(g["dlut_planes"]), _p(g["dlw"]), _p(g["dlb"]), _p(g["dgrid_planes"]), _p(g["dgw"]),
+          _p(g["dgb"]), _p(loss), _p(ws), ws_bytes, _stream(rgb))
+    return loss, g
 
 
 def reconstruct_backward(u, s, vt, dplanes):
