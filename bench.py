@@ -778,8 +778,8 @@ def run_secondary(a):
         case = synth.make_batch(list(range(lo, hi)), h=1080, w=1920)
         h, w, units = 1080, 1920, (hi - lo)
         desc = (f"config5: training step on 8 x 3x1080x1920 (per-image shards, {hi - lo} per rank): "
-                f"forward with the L2 loss vs X^0.8 fused in its epilogue + backward (gX, dU/dS/dVt, "
-                f"grids, weights; autograd.l2_step)")
+                f"one pass per pixel: Y, the L2 loss vs X^0.8 and gY formed inside the backward "
+                f"(gX, dU/dS/dVt, grids, weights; autograd.l2_step -> svdlut_fused_l2_step)")
     rgb = T(case.rgb)
     prm = {k: T(getattr(case, k)) for k in keys}
     y0_strip = parallel.strip_rows(4320, world, rank)[0] if a.config == 4 else 0
@@ -794,7 +794,7 @@ def run_secondary(a):
                                                 prm["grid_planes"], prm["gw"], prm["gb"])
             device.apply(rgb, tables, out=out, y0=y0_strip, h_total=h_total)
             return
-        # fused training step: the L2 loss lives in the forward's epilogue
+        # one-pass training step: Y, the loss and gY never touch HBM
         autograd.l2_step(rgb, target, prm["u"], prm["s"], prm["vt"], prm["lw"], prm["lb"],
                          prm["grid_planes"], prm["gw"], prm["gb"])
 
