@@ -18,6 +18,8 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:fuse
   -o gpurun_out/fwd_$R -f python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-extra > gpurun_out/fwd_ncu.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:fused_bwd_kernel -c 1 \
   -o gpurun_out/bwd_$R -f python tools/bwd_once.py > gpurun_out/bwd_ncu.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:fused_bwd_kernel -s 1 -c 1 \
+  -o gpurun_out/l2step_$R -f python tools/bwd_once.py > gpurun_out/l2step_ncu.log 2>&1
 for m in ldsclean texphase atomswidth atomspat shfllds; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench/$m tools/microbench/$m.cu
 done
