@@ -538,6 +538,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     };
     int jy_prev = 0;
     float ey_prev = 0.f;
+    BChunk cur_out;     // backward: this warp's chunk of samples and gY, loaded ahead
+    bool have = false;  // cur_out holds the chunk (loaded at the end of the previous one)
 
     for (int y = y_first; y <= y_last; ++y) {
       const int buf = (y - y_first) & 1;
@@ -561,10 +563,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       float row_max = 0.f, row_ss = 0.f;  // fused L2 step: this thread's |gY| statistics of row y
       int row_big = 0;
       for (int x0 = warp * 128; x0 < p.w; x0 += kBwdWarps * 128) {
+        // (backward: lanes past the row end run on clamped samples with gY = 0)
         const int xl = x0 + 4 * lane;
-        if (xl >= p.w) continue;
-        BChunk cur;
-        bload_chunk(X, GY, pl, y, x0, p.w, lane, vec, cur);
+        if (L2 && xl >= p.w) continue;
+        BChunk cur_in;
+        BChunk& cur = L2 ? cur_in : cur_out;  // (the L2 step loads in place: less live state)
+        if (L2 || !have) bload_chunk(X, GY, pl, y, x0, p.w, lane, vec, cur);
         float oxr[kBPx], oxg[kBPx], oxb[kBPx];
 #pragma unroll
         for (int u = 0; u < kBPx; ++u) {
@@ -729,6 +733,18 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
                 GX[2 * pl + ro + xl + u] = oxb[u];
               }
           }
+        }
+        // the warp's next chunk (this row or the next), loaded while this one
+        // ends: its latency hides behind the row's end and barrier (not in
+        // the L2 step, whose larger live state would spill)
+        if (!L2) {
+          int nx0 = x0 + kBwdWarps * 128, ny = y;
+          if (nx0 >= p.w) {
+            nx0 = warp * 128;
+            ++ny;
+          }
+          have = ny <= y_last && nx0 < p.w;
+          if (have) bload_chunk(X, GY, pl, ny, nx0, p.w, lane, vec, cur);
         }
       }
       px_since_flush += p.w;
