@@ -149,3 +149,28 @@ def test_fused_step_growing_residuals(dev, oracle_mod):
     assert abs(float(g["loss"]) - loss_ref) <= 1e-5 * loss_ref
     for k, want in refs[0].items():
         close(g[k][0].cpu().numpy(), want, k)
+
+
+def test_fused_step_on_a_row_strip(dev):
+    """A row strip (y0 > 0, normalised by the full height) through the
+    one-pass step equals the two-kernel step on the same strip."""
+    import torch
+
+    from paper_2508_16121_b200 import device
+
+    case = _case(11, 1, 200, 300)
+    st = {k: T(getattr(case, k), dev) for k in ("rgb",) + KEYS}
+    x = st["rgb"][:, :, 60:140].contiguous()
+    tgt = x.clamp_min(0) ** 0.8
+    planes = device.reconstruct(st["u"], st["s"], st["vt"])
+    tables = device.pack_tables(planes, st["lw"], st["lb"], st["grid_planes"], st["gw"], st["gb"])
+    gscale = 2.0 / x.numel()
+    loss1, g1 = device.fused_l2_step(x, tgt, tables, planes, st["lw"], st["grid_planes"], st["gw"],
+                                     gscale=gscale, y0=60, h_total=200)
+    gy, loss2, gmax = device.apply_l2(x, tgt, tables, gscale=gscale, y0=60, h_total=200)
+    g2 = device.fused_backward(x, gy, planes, st["lw"], st["grid_planes"], st["gw"], y0=60, h_total=200,
+                               tables=tables, gmax=gmax, gsumsq=loss2 * gscale * gscale)
+    torch.cuda.synchronize()
+    assert abs(float(loss1[0]) - float(loss2[0])) <= 1e-6 * float(loss2[0])
+    for k in g1:
+        close(g1[k].cpu().numpy(), g2[k].cpu().numpy(), k)
