@@ -29,6 +29,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .core_types import Image as _Image
 from .errors import DimensionMismatch, InvalidArgument
 
 __all__ = ["HyperParams", "ModelParams", "expected_shapes", "random_init", "param_count",
@@ -239,11 +240,12 @@ class Generator:
         return device.pack_tables_factors(p["u"], p["s"], p["vt"], p["lw"], p["lb"],
                                           p["grid_planes"], p["gw"], p["gb"])
 
-    def enhance(self, rgb, out=None):
-        """(B, 3, H, W) CUDA float32 -> enhanced image, all on device."""
+    def enhance(self, rgb, out=None, nonfinite=None):
+        """(B, 3, H, W) CUDA float32 -> enhanced image, all on device
+        (``nonfinite``: optional int32 flag OR-ed with 1 on a NaN/Inf output)."""
         from . import device
 
-        return device.apply(rgb, self.tables(rgb), out=out)
+        return device.apply(rgb, self.tables(rgb), out=out, nonfinite=nonfinite)
 
     def graphed(self, shape):
         """Enhance for a fixed (B, 3, H, W) as one CUDA-graph replay.
@@ -260,18 +262,20 @@ class Generator:
         shape = tuple(int(v) for v in shape)
         x = torch.zeros(shape, dtype=torch.float32, device=self.device)
         out = torch.empty_like(x)
+        flag = torch.zeros(1, dtype=torch.int32, device=self.device)  # NaN/Inf in the output
         with torch.cuda.device(self.device):  # capture on the generator's device
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.stream(side):
                 for _ in range(2):  # allocations, kernel attributes, texture objects
-                    self.enhance(x, out=out)
+                    self.enhance(x, out=out, nonfinite=flag)
             torch.cuda.current_stream(self.device).wait_stream(side)
             graph = torch.cuda.CUDAGraph()
             # relaxed: the apply may create a texture object over the graph pool's
             # table buffer while capturing (not a stream operation)
             with torch.cuda.graph(graph, capture_error_mode="relaxed"):
-                self.enhance(x, out=out)
+                flag.zero_()
+                self.enhance(x, out=out, nonfinite=flag)
 
         def run(rgb):
             if tuple(rgb.shape) != shape:
@@ -281,19 +285,23 @@ class Generator:
             return out
 
         run.graph = graph  # keeps the capture (and its memory pool) alive with the closure
+        run.nonfinite = flag  # set by each replay
         return run
 
-    def enhance_replayed(self, rgb):
+    def enhance_replayed(self, rgb, with_flag=False):
         """``enhance`` through a CUDA graph captured on the first call for
         each input shape (kept for the last four shapes).  The returned tensor
-        is the graph's static output: consume it before the next call."""
+        is the graph's static output: consume it before the next call.
+        ``with_flag``: also return the replay's int32 NaN/Inf output flag."""
         key = tuple(rgb.shape)
         cache = self.__dict__.setdefault("_graphs", {})
         if key not in cache:
             if len(cache) >= 4:
                 cache.pop(next(iter(cache)))
             cache[key] = self.graphed(key)
-        return cache[key](rgb)
+        run = cache[key]
+        out = run(rgb)
+        return (out, run.nonfinite) if with_flag else out
 
 
 def backbone_forward(img, params, device="cuda"):
@@ -331,20 +339,28 @@ def run_model(img, params, fused=True, threads=1, device="cuda"):
         y = gen.enhance(rgb)[0].cpu().numpy()
         return transform._image_type(img)(img.width, img.height, y)
     # A Generator reused across calls replays a per-shape CUDA graph (batch 1
-    # is launch-bound) between page-locked staging buffers it keeps per shape:
-    # one host copy into the pinned input, H2D, replay, D2H into a pinned
-    # output, one host copy out (the returned Image owns its array).
+    # is launch-bound): one host copy into a page-locked input it keeps per
+    # shape, H2D, replay, D2H straight into a fresh page-locked output that
+    # the returned Image owns (no copy out), plus the replay's NaN/Inf flag,
+    # so the host finiteness scan of the Image constructor is skipped when
+    # the device found none (as fused_enhance does).
     shape = (1, 3, img.height, img.width)
     st = gen.__dict__.setdefault("_host_staging", {})
     if shape not in st:
         if len(st) >= 4:
             st.pop(next(iter(st)))
         st[shape] = (torch.empty(shape, dtype=torch.float32, pin_memory=True),
-                     torch.empty(shape, dtype=torch.float32, pin_memory=True))
-    pin_in, pin_out = st[shape]
-    np.copyto(pin_in.numpy()[0], img.data, casting="same_kind")
+                     torch.zeros(1, dtype=torch.int32, pin_memory=True))
+    pin_in, pin_flag = st[shape]
+    pin_in[0].copy_(torch.from_numpy(np.asarray(img.data, np.float32)))
+    pin_out = torch.empty(shape, dtype=torch.float32, pin_memory=True)
     with torch.cuda.device(gen.device):
-        y = gen.enhance_replayed(pin_in)  # the graph copies it into its static input (H2D)
+        y, flag = gen.enhance_replayed(pin_in, with_flag=True)  # the graph copies the input in (H2D)
         pin_out.copy_(y, non_blocking=True)
+        pin_flag.copy_(flag, non_blocking=True)
         torch.cuda.current_stream(gen.device).synchronize()
-    return transform._image_type(img)(img.width, img.height, pin_out.numpy()[0].copy())
+    cls = transform._image_type(img)
+    data = pin_out.numpy()[0]
+    if int(pin_flag[0]) == 0 and issubclass(cls, _Image):
+        return cls._trusted(img.width, img.height, data)
+    return cls(img.width, img.height, data)  # validates (NonFiniteValue on NaN/Inf)

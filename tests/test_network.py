@@ -179,3 +179,30 @@ def test_run_model_with_reused_generator_replays_graph():
         got = network.run_model(img, gen)
         assert np.array_equal(got.data, want.data)
     assert len(gen._graphs) == 2
+
+
+@pytest.mark.gpu
+def test_run_model_reused_generator_flags_non_finite_output():
+    """The replayed path skips the Image finiteness scan only when the
+    device flag says the output is finite: a NaN in a head's weights still
+    raises NonFiniteValue, like the reference's Image constructor, and the
+    next finite call returns a valid Image again."""
+    import __graft_entry__
+    from paper_2508_16121_b200 import network
+    from paper_2508_16121_b200.core_types import Image
+    from paper_2508_16121_b200.errors import NonFiniteValue
+
+    __graft_entry__.build_library()
+    params = network.random_init(0)
+    img = Image(96, 64, np.random.default_rng(3).random((3, 64, 96), dtype=np.float32))
+    name = "lutw_gen.fc2.bias"
+    bad = dict(params.tensors)
+    bad[name] = bad[name].copy()
+    bad[name].flat[0] = np.nan
+    gen_bad = network.Generator(network.ModelParams(params.hyper, bad))
+    with pytest.raises(NonFiniteValue):
+        network.run_model(img, gen_bad)
+    gen = network.Generator(params)
+    for _ in range(2):
+        y = network.run_model(img, gen)
+        assert np.isfinite(y.data).all() and not y.data.flags.writeable
