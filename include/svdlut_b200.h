@@ -224,7 +224,10 @@ int svdlut_fused_fwd_l2(const float* rgb, const float* target, int batch, int h,
  * of gy: `gmax` (>= max |gy|, e.g. from svdlut_fused_fwd_l2) and `gsumsq`
  * (sum of gy^2, f64, may be NULL).  The vertex scatter is 32-bit fixed point
  * scaled by B = min(gmax, 6 rms(gy)); pixels with |gy| > B scatter through
- * f32 atomics instead.  NULL gmax recomputes both statistics. */
+ * f32 atomics instead.  With NULL gmax each CTA sets its own bound from a
+ * probe of its first row, B = 1.5 min(max |gy|, 6 rms gy) of that row, and
+ * raises it (flushing its partials) when more than 1/64 of a row's pixels
+ * exceed it. */
 int svdlut_fused_bwd_packed(const float* rgb, const float* gy, int batch, int h, int w, int y0,
                             int h_total, const void* tables, const float* gmax, const double* gsumsq,
                             const float* lut_planes, const float* lw, int d_t,

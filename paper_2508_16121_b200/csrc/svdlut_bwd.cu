@@ -279,7 +279,10 @@ __device__ __forceinline__ void bload_chunk(const float* X, const float* GY, lon
   bload4(GY + 2 * pl + ro, c.y2, x, w, vec);
 }
 
-template <int DT, int DS, bool L2>
+// L2: the fused training step (gY formed per pixel, implies DYN).  DYN: the
+// fixed-point bound comes per CTA from a probe of its first row (and is
+// raised on demand) instead of precomputed per-image statistics.
+template <int DT, int DS, bool L2, bool DYN>
 __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams p) {
   extern __shared__ __align__(128) float smem[];
   __shared__ __align__(8) uint64_t bar_storage;
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     }
     for (int i = threadIdx.x; i < A.total + 12 * ds + 6 * xr_size; i += blockDim.x) Ei[i] = 0;
     float gm = 0.f;
-    if (!L2) {
+    if (!DYN) {
       gm = p.gmax[b];
       if (p.gss) gm = fminf(gm, kOutlierSigmas * (float)sqrt(p.gss[b] / (3.0 * (double)pl)));
     }
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     auto row_bound = [&](int slot) {  // with headroom for the rows after it
       return kL2Headroom * fminf(s_max[slot], kOutlierSigmas * sqrtf(s_ss[slot] / (3.f * (float)p.w)));
     };
-    if (L2) {
+    if (DYN) {
       if (threadIdx.x == 0) {
         for (int i = 0; i < 3; ++i) {
           s_max[i] = s_ss[i] = 0.f;
@@ -504,13 +507,16 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         bload_chunk(X, GY, pl, y_first, x0, p.w, lane, vec, cur);
 #pragma unroll
         for (int u = 0; u < kBPx; ++u) {
-          PixFront F;
-          front(F, cur.r[u], cur.g[u], cur.b[u], xl + u, slotK0);
-          const float3 Y = pix_y(F);
           const bool valid = xl + u < p.w;
-          const float g0 = valid ? (Y.x - cur.y0[u]) * p.gscale : 0.f;
-          const float g1 = valid ? (Y.y - cur.y1[u]) * p.gscale : 0.f;
-          const float g2 = valid ? (Y.z - cur.y2[u]) * p.gscale : 0.f;
+          float g0 = valid ? cur.y0[u] : 0.f, g1 = valid ? cur.y1[u] : 0.f, g2 = valid ? cur.y2[u] : 0.f;
+          if (L2) {  // the forward of the probe row
+            PixFront F;
+            front(F, cur.r[u], cur.g[u], cur.b[u], xl + u, slotK0);
+            const float3 Y = pix_y(F);
+            g0 = valid ? (Y.x - cur.y0[u]) * p.gscale : 0.f;
+            g1 = valid ? (Y.y - cur.y1[u]) * p.gscale : 0.f;
+            g2 = valid ? (Y.z - cur.y2[u]) * p.gscale : 0.f;
+          }
           pm = fmaxf(pm, fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))));
           ps = __fmaf_rn(g0, g0, __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, ps)));
         }
@@ -585,17 +591,19 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
             g0 = r0 * p.gscale;
             g1 = r1 * p.gscale;
             g2 = r2 * p.gscale;
-            row_max = fmaxf(row_max, fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))));
-            row_ss = __fmaf_rn(g0, g0, __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, row_ss)));
           } else {
             g0 = valid ? cur.y0[u] : 0.f;
             g1 = valid ? cur.y1[u] : 0.f;
             g2 = valid ? cur.y2[u] : 0.f;
           }
+          if (DYN) {
+            row_max = fmaxf(row_max, fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))));
+            row_ss = __fmaf_rn(g0, g0, __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, row_ss)));
+          }
           // outliers take the f32 slow path; the fixed-point path sees zeros
           const bool big = fmaxf(fabsf(g0), fmaxf(fabsf(g1), fabsf(g2))) > bound;
           const float f0 = big ? 0.f : g0, f1 = big ? 0.f : g1, f2 = big ? 0.f : g2;
-          if (L2) row_big += big ? 1 : 0;
+          if (DYN) row_big += big ? 1 : 0;
           gsum0 += g0;
           gsum1 += g1;
           gsum2 += g2;
@@ -748,10 +756,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         }
       }
       px_since_flush += p.w;
-      if (L2) warp_stats(row_max, row_ss, row_big, y & 1);
+      if (DYN) warp_stats(row_max, row_ss, row_big, y & 1);
       if (y < y_last) produce_rows(y + 1);  // the other half of the ring
       __syncthreads();
-      if (L2 && threadIdx.x == 0) {  // row y + 1's statistics slot (row y - 1's was read last row)
+      if (DYN && threadIdx.x == 0) {  // row y + 1's statistics slot (row y - 1's was read last row)
         s_max[(y + 1) & 1] = 0.f;
         s_ss[(y + 1) & 1] = 0.f;
         s_nbig[(y + 1) & 1] = 0;
@@ -776,7 +784,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       }
       jy_prev = jy;
       ey_prev = ey;
-      if (L2 && y < y_last && s_nbig[y & 1] * 64 > p.w) {
+      if (DYN && y < y_last && s_nbig[y & 1] * 64 > p.w) {
         // every thread reads the same row statistics: raise the bound after
         // moving every partial at the old scale to the global f32 sums
         const float bnd = fmaxf(2.f * bound, row_bound(y & 1));
@@ -888,38 +896,6 @@ __global__ void finalize_kernel(const float* __restrict__ lp, const float* __res
   }
 }
 
-// max|gY| and sum gY^2 per image (positive floats order like their bit patterns).
-__global__ void gy_stats_kernel(const float* __restrict__ gy, long long per_img, float* gmax, double* gss) {
-  const long long b = blockIdx.y;
-  const float* base = gy + b * per_img;
-  float m = 0.f;
-  double sq = 0.0;
-  const bool vec = (per_img % 4 == 0) && ((reinterpret_cast<uintptr_t>(gy) & 15) == 0);
-  if (vec) {
-    const float4* g = reinterpret_cast<const float4*>(base);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_img / 4;
-         i += (long long)gridDim.x * blockDim.x) {
-      const float4 v = __ldcs(g + i);
-      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-      sq += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
-    }
-  } else {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_img;
-         i += (long long)gridDim.x * blockDim.x) {
-      m = fmaxf(m, fabsf(base[i]));
-      sq += (double)base[i] * base[i];
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    sq += __shfl_xor_sync(0xffffffffu, sq, off);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMax(reinterpret_cast<int*>(gmax + b), __float_as_int(m));
-    atomicAdd(gss + b, sq);
-  }
-}
-
 // The backward (target == NULL: gy given) or the fused L2 training step
 // (target != NULL: gy = gscale (Y - target) formed per pixel from
 // `tables_in`, which must be the forward's packed tables; loss[b] += sum
@@ -931,6 +907,7 @@ static cudaError_t bwd_impl(const float* rgb, const float* gy, int batch, int h,
                             const float* tables_in, const float* gmax_in, const double* gss_in,
                             const float* target, float gscale, double* loss) {
   const bool l2 = target != nullptr;
+  const bool dyn = l2 || !gmax_in;  // no precomputed statistics: per-CTA probe bound
   if (l2 && (!tables_in || !loss)) return cudaErrorInvalidValue;
   const TableLayout L = TableLayout::make(dt, ds);
   const AccLayout A = AccLayout::make(dt, ds);
@@ -945,27 +922,13 @@ static cudaError_t bwd_impl(const float* rgb, const float* gy, int batch, int h,
   wp += rup((size_t)batch * A.total * 4);
   float* zb = (float*)wp;  // zero biases (biases do not enter any derivative)
   wp += rup((size_t)batch * (3 + k) * 4);
-  float* gmax = (float*)wp;
-  wp += rup((size_t)batch * 4);
-  double* gss = (double*)wp;
+  // caller-provided max |gY| and sum gY^2 per image (gss may be NULL: bound
+  // = max); without them (and in the L2 step) the kernel's per-CTA probe
+  const float* gmax = dyn ? nullptr : gmax_in;
+  const double* gss = dyn ? nullptr : gss_in;
   cudaError_t e;
   if ((e = cudaMemsetAsync(zb, 0, (size_t)batch * (3 + k) * 4, st)) != cudaSuccess) return e;
-  if (l2) {
-    if ((e = cudaMemsetAsync(loss, 0, (size_t)batch * 8, st)) != cudaSuccess) return e;
-  } else if (gmax_in) {
-    gmax = const_cast<float*>(gmax_in);  // caller-provided max |gY| per image
-    gss = const_cast<double*>(gss_in);   // and sum gY^2 (may be NULL: bound = max)
-  } else {
-    if ((e = cudaMemsetAsync(gmax, 0, (size_t)batch * 4, st)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(gss, 0, (size_t)batch * 8, st)) != cudaSuccess) return e;
-    const long long per = 3LL * h * w;
-    long long blocks = (per / 4 + 255) / 256;
-    if (blocks > 512) blocks = 512;
-    if (blocks < 1) blocks = 1;
-    dim3 g((unsigned)blocks, batch);
-    gy_stats_kernel<<<g, 256, 0, st>>>(gy, per, gmax, gss);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
+  if (l2 && (e = cudaMemsetAsync(loss, 0, (size_t)batch * 8, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(E, 0, (size_t)batch * A.total * 4, st)) != cudaSuccess) return e;
   if (tables_in) {
     tables = const_cast<float*>(tables_in);  // forward tables: biases do not enter the backward
@@ -999,14 +962,15 @@ static cudaError_t bwd_impl(const float* rgb, const float* gy, int batch, int h,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     long long grid = sms < rows ? sms : rows;
     const bool spec = dt == 33 && ds == 17;
-    auto kern = l2 ? (spec ? fused_bwd_kernel<33, 17, true> : fused_bwd_kernel<0, 0, true>)
-                   : (spec ? fused_bwd_kernel<33, 17, false> : fused_bwd_kernel<0, 0, false>);
-    const int inst = (spec ? 1 : 0) + (l2 ? 2 : 0);
+    auto kern = l2    ? (spec ? fused_bwd_kernel<33, 17, true, true> : fused_bwd_kernel<0, 0, true, true>)
+                : dyn ? (spec ? fused_bwd_kernel<33, 17, false, true> : fused_bwd_kernel<0, 0, false, true>)
+                      : (spec ? fused_bwd_kernel<33, 17, false, false> : fused_bwd_kernel<0, 0, false, false>);
+    const int inst = (spec ? 1 : 0) + (l2 ? 4 : dyn ? 2 : 0);
     // Attributes set once per (instantiation, device) to the largest request
     // any launch may make, so concurrent launches never see the limit lowered
     // under them (as for the forward kernel).
     constexpr int kMaxDev = 64;
-    static std::atomic<int> configured[kMaxDev][4];
+    static std::atomic<int> configured[kMaxDev][6];
     if (dev >= kMaxDev || configured[dev][inst].load(std::memory_order_acquire) == 0) {
       if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     fwd_max_smem_bytes())) != cudaSuccess)
