@@ -228,10 +228,10 @@ __device__ __forceinline__ uint32_t bbracket(float q, float dm1, float dm2, floa
 constexpr int kMaxFlushPx = 32767;
 constexpr float kFixedOne = 65536.0f;
 constexpr float kOutlierSigmas = 6.0f;
-#ifndef BWD_L2_HEADROOM
-#define BWD_L2_HEADROOM 1.5f
+#ifndef BWD_PROBE_HEADROOM
+#define BWD_PROBE_HEADROOM 1.5f
 #endif
-constexpr float kL2Headroom = BWD_L2_HEADROOM;  // fused L2 step: bound = headroom x the row statistic
+constexpr float kProbeHeadroom = BWD_PROBE_HEADROOM;  // probe bound = headroom x the row statistic
 __device__ __forceinline__ int to_fixed(float v, float S) {
   return __float_as_int(__fmaf_rn(v, S, 12582912.0f)) - 0x4B400000;
 }
@@ -464,8 +464,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       F.s[1] = blds4(sa + chan_bytes + F.sg * 16u);
       F.s[2] = blds4(sa + 2u * chan_bytes + F.sb * 16u);
     };
-    // Fused L2 step: the fixed-point bound of this CTA's image segment comes
-    // from its first row (a forward-only probe pass), B = 1.5 min(max |gY|,
+    // Dynamic bound (DYN: the fused L2 step, or no caller statistics): the
+    // fixed-point bound of this CTA's image segment comes from its first row
+    // (a probe pass; in the L2 step forward-only), B = 1.5 min(max |gY|,
     // 6 rms gY) of that row; pixels above B take the f32 slow path.  When
     // more than 1/64 of a row's pixels did, B is raised to max(2 B, 1.5 x the
     // row's own min(max, 6 rms)) after the partials at the old scale are
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       }
     };
     auto row_bound = [&](int slot) {  // with headroom for the rows after it
-      return kL2Headroom * fminf(s_max[slot], kOutlierSigmas * sqrtf(s_ss[slot] / (3.f * (float)p.w)));
+      return kProbeHeadroom * fminf(s_max[slot], kOutlierSigmas * sqrtf(s_ss[slot] / (3.f * (float)p.w)));
     };
     if (DYN) {
       if (threadIdx.x == 0) {
