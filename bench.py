@@ -535,7 +535,11 @@ def main():
         try:
             k0 = next(iter(json.load(open(prof))["kernels"].values()))
             pct = float(k0["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"])
-            smem_pipe = {"bound": "shared-memory (LSU) pipe", "pct_of_peak_elapsed": round(pct, 1),
+            tex = float(k0["l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed"])
+            issue = float(k0["smsp__issue_active.avg.pct_of_peak_sustained_active"])
+            smem_pipe = {"bound": "the SM's gather pipes: shared memory (LSU) and texture, balanced",
+                         "pct_of_peak_elapsed": round(pct, 1), "tex_pct_of_peak_elapsed": round(tex, 1),
+                         "issue_active_pct": round(issue, 1),
                          "source": "profiles/ncu_fused_fwd.json (ncu --set full, one launch)"}
         except (KeyError, StopIteration, ValueError):
             smem_pipe = None
