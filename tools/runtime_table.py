@@ -1,5 +1,6 @@
 """Multi-stage vs fused runtime on B200 (the paper's tab:runtime comparison,
-SURVEY.md §8(f) row 3), device-resident inputs, CUDA-event timing:
+SURVEY.md §8(f) row 3), device-resident inputs, CUDA-event timing of 20
+calls replayed from one CUDA graph:
 
   fused fast      svdlut fused fp32 kernel (product path)
   fused exact     f64 op-for-op kernel (bitwise equal to the reference)
@@ -49,11 +50,18 @@ for h, w in ((480, 720), (1080, 1920), (2160, 3840)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        # 20 calls captured in one CUDA graph: device time per frame, without
+        # the ~20 us of Python per call that dominates small frames
         reps = 20
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+            for _ in range(reps):
+                fn()
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
-        for _ in range(reps):
-            fn()
+        graph.replay()
         e1.record()
         torch.cuda.synchronize()
         res[name] = e0.elapsed_time(e1) * 1e3 / reps
