@@ -247,7 +247,7 @@ def run_reference_arm(a):
     total = sum(times)
     value = H * W * len(times) / total / 1e6
     # the unmodified reference: parallel twin in its own fresh process first, then the serial one
-    numba_n = ref_numba("fused", threads, 3)
+    numba_n = ref_numba("fused", threads, 7)
     numba_1 = ref_numba("fused", 1, 2)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
