@@ -152,7 +152,7 @@ struct PixFront {
   int jx;
   float dr, dg, db, er, eg, eb, ex;
   float4 q[9];  // chunk planes: pair rg 0-2, rb 3-5, gb 6-8
-  float4 s[3];  // merged grid slots {M, M', N, N'} per channel
+  float4 s[3];  // merged grid slots per channel: L2 step {M, M', N, N'}; backward {M', N', -, -}
 };
 
 // Y of one pixel from its cells, the forward kernel's arithmetic
@@ -189,6 +189,9 @@ __device__ __forceinline__ uint32_t bsmem_addr(const void* p) {
 }
 __device__ __forceinline__ float4 blds4(uint32_t a) {
   return *reinterpret_cast<const float4*>(__cvta_shared_to_generic(a));
+}
+__device__ __forceinline__ float2 blds2(uint32_t a) {
+  return *reinterpret_cast<const float2*>(__cvta_shared_to_generic(a));
 }
 // Cyclic rotation of a channel triple by the lane's channel offset r (rot1:
 // r == 1, rot2: r == 2) with selects: (a, b, c) -> (b, c, a) / (c, a, b).
@@ -430,7 +433,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
         const int jx = e / (3 * (ds - 1)), rem = e - jx * 3 * (ds - 1);
         const int ch = rem / (ds - 1), jc = rem - ch * (ds - 1);
         SVDLUT_CHECK(jyp >= 0 && jyp <= ds - 2);
-        S[e] = bgrid_entry(gsm, L, ch, jx, jc, jyp, eyp);
+        const float4 v = bgrid_entry(gsm, L, ch, jx, jc, jyp, eyp);  // {M, M', N, N'}
+        // the backward alone needs only d/dec = M' + N' ex: stored first, one LDS.64
+        S[e] = L2 ? v : make_float4(v.y, v.w, v.x, v.z);
       }
     };
     produce_rows(y_first);
@@ -460,9 +465,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       F.q[7] = bfetch<7>(ad, F.bg, F.bb);
       F.q[8] = bfetch<8>(ad, F.bg, F.bb);
       const uint32_t sa = slotK + (uint32_t)F.jx * jx_bytes;
-      F.s[0] = blds4(sa + F.sr * 16u);
-      F.s[1] = blds4(sa + chan_bytes + F.sg * 16u);
-      F.s[2] = blds4(sa + 2u * chan_bytes + F.sb * 16u);
+      if (L2) {
+        F.s[0] = blds4(sa + F.sr * 16u);
+        F.s[1] = blds4(sa + chan_bytes + F.sg * 16u);
+        F.s[2] = blds4(sa + 2u * chan_bytes + F.sb * 16u);
+      } else {  // {M', N'} only
+        const float2 t0 = blds2(sa + F.sr * 16u), t1 = blds2(sa + chan_bytes + F.sg * 16u),
+                     t2 = blds2(sa + 2u * chan_bytes + F.sb * 16u);
+        F.s[0] = make_float4(t0.x, t0.y, 0.f, 0.f);
+        F.s[1] = make_float4(t1.x, t1.y, 0.f, 0.f);
+        F.s[2] = make_float4(t2.x, t2.y, 0.f, 0.f);
+      }
     };
     // Dynamic bound (DYN: the fused L2 step, or no caller statistics): the
     // fixed-point bound of this CTA's image segment comes from its first row
@@ -631,9 +644,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
             gag += g0 * __fmaf_rn(c1.z, db, c0.z) + g1 * __fmaf_rn(c1.w, db, c0.w) + g2 * __fmaf_rn(c2.w, db, c2.z);
             gab += g0 * __fmaf_rn(c1.z, dg, c1.x) + g1 * __fmaf_rn(c1.w, dg, c1.y) + g2 * __fmaf_rn(c2.w, dg, c2.y);
           }
-          const float gsr = g0 * __fmaf_rn(F.s[0].w, ex, F.s[0].y);  // slot {M, M', N, N'}
-          const float gsg = g1 * __fmaf_rn(F.s[1].w, ex, F.s[1].y);
-          const float gsb = g2 * __fmaf_rn(F.s[2].w, ex, F.s[2].y);
+          // d/dec = M' + N' ex
+          const float gsr = g0 * (L2 ? __fmaf_rn(F.s[0].w, ex, F.s[0].y) : __fmaf_rn(F.s[0].y, ex, F.s[0].x));
+          const float gsg = g1 * (L2 ? __fmaf_rn(F.s[1].w, ex, F.s[1].y) : __fmaf_rn(F.s[1].y, ex, F.s[1].x));
+          const float gsb = g2 * (L2 ? __fmaf_rn(F.s[2].w, ex, F.s[2].y) : __fmaf_rn(F.s[2].y, ex, F.s[2].x));
           oxr[u] = (Xr < 0.f || Xr > 1.f) ? 0.f : __fmaf_rn(gar, tdm1, gsr * sdm1);
           oxg[u] = (Xg < 0.f || Xg > 1.f) ? 0.f : __fmaf_rn(gag, tdm1, gsg * sdm1);
           oxb[u] = (Xb < 0.f || Xb > 1.f) ? 0.f : __fmaf_rn(gab, tdm1, gsb * sdm1);
