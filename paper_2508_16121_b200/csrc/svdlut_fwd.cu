@@ -9,7 +9,9 @@
 //     chunk planes are gathered through the texture path, a second pipe beside
 //     the shared-memory (LSU) pipe: an LDS.128 delivers 128 B of lane data
 //     per clock, a TLD.128 64 B (tools/microbench/{ldsclean,texphase}.cu), so
-//     the split balances the two.
+//     the split balances the two (default: pair rg and chunk 0 of rb staged;
+//     rb chunks 1-2 and pair gb, stored in 4x4-tiled cell order, gathered
+//     through the texture path one pixel ahead of their use).
 //   * A CTA owns a contiguous range of 128-pixel chunks over (image, row,
 //     chunk) — balanced to one chunk — and its warps take the range's chunks
 //     round robin (lane = 4 consecutive pixels, 128-bit streaming loads and
