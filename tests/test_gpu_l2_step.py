@@ -174,3 +174,41 @@ def test_fused_step_on_a_row_strip(dev):
     assert abs(float(loss1[0]) - float(loss2[0])) <= 1e-6 * float(loss2[0])
     for k in g1:
         close(g1[k].cpu().numpy(), g2[k].cpu().numpy(), k)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_probe_paths_match_statistics_paths_fuzz(dev, seed):
+    """Random batch / shape / strip / residual growth: the backward without
+    caller statistics (per-CTA probe bound) and the one-pass step agree with
+    the statistics-driven two-kernel step (image boundaries inside CTA row
+    ranges, rescales, partial chunks, strips)."""
+    import torch
+
+    from paper_2508_16121_b200 import device
+
+    rng = np.random.default_rng(100 + seed)
+    b = int(rng.integers(1, 4))
+    h = int(rng.integers(2, 260))
+    w = int(rng.integers(2, 700))
+    case = _case(200 + seed, b, h, w)
+    st = {k: T(getattr(case, k), dev) for k in ("rgb",) + KEYS}
+    y0 = int(rng.integers(0, 40)) if seed % 2 else 0
+    h_total = h + y0 + int(rng.integers(0, 40))
+    planes = device.reconstruct(st["u"], st["s"], st["vt"])
+    tables = device.pack_tables(planes, st["lw"], st["lb"], st["grid_planes"], st["gw"], st["gb"])
+    ramp = torch.from_numpy(np.logspace(-float(rng.integers(0, 4)), 0, h).astype(np.float32)).to(dev)
+    tgt = st["rgb"].clamp_min(0) ** 0.8 + ramp[None, None, :, None] * 0.3
+    gscale = 2.0 / st["rgb"].numel()
+    loss1, g1 = device.fused_l2_step(st["rgb"], tgt, tables, planes, st["lw"], st["grid_planes"], st["gw"],
+                                     gscale=gscale, y0=y0, h_total=h_total)
+    gy, loss2, gmax = device.apply_l2(st["rgb"], tgt, tables, gscale=gscale, y0=y0, h_total=h_total)
+    g2 = device.fused_backward(st["rgb"], gy, planes, st["lw"], st["grid_planes"], st["gw"], y0=y0,
+                               h_total=h_total, tables=tables, gmax=gmax, gsumsq=loss2 * gscale * gscale)
+    g3 = device.fused_backward(st["rgb"], gy, planes, st["lw"], st["grid_planes"], st["gw"], y0=y0,
+                               h_total=h_total)
+    torch.cuda.synchronize()
+    assert torch.allclose(loss1, loss2, rtol=1e-6, atol=0)
+    for k in g2:
+        want = g2[k].cpu().numpy()
+        close(g1[k].cpu().numpy(), want, f"one-pass {k} (b={b} h={h} w={w} y0={y0})")
+        close(g3[k].cpu().numpy(), want, f"probe backward {k} (b={b} h={h} w={w} y0={y0})")
