@@ -212,3 +212,21 @@ def test_probe_paths_match_statistics_paths_fuzz(dev, seed):
         want = g2[k].cpu().numpy()
         close(g1[k].cpu().numpy(), want, f"one-pass {k} (b={b} h={h} w={w} y0={y0})")
         close(g3[k].cpu().numpy(), want, f"probe backward {k} (b={b} h={h} w={w} y0={y0})")
+
+
+@pytest.mark.parametrize("d_t,d_s,k,n_s", [(17, 8, 6, 4), (9, 5, 9, 3), (65, 9, 3, 8)])
+def test_fused_step_other_dims(dev, oracle_mod, d_t, d_s, k, n_s):
+    """The generic (non-33/17) instantiation of the one-pass step against the
+    f64 oracle."""
+    from paper_2508_16121_b200 import device, synth
+
+    case = synth.make_batch([300, 301], h=70, w=150, d_t=d_t, d_s=d_s, k=k, n_s=n_s)
+    if not device.fast_supported(d_t, d_s):
+        pytest.skip("tables beyond shared memory: exact kernel only")
+    tgt = np.clip(case.rgb, 0, None) ** 0.8
+    loss_ref, refs = _oracle_step(oracle_mod, case, tgt)
+    g = _run(dev, case, tgt, fused=True)
+    assert abs(float(g["loss"]) - loss_ref) <= 1e-5 * loss_ref
+    for i in range(2):
+        for key, want in refs[i].items():
+            close(g[key][i].cpu().numpy(), want, f"{key}[{i}]")
