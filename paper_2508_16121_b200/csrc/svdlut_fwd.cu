@@ -15,7 +15,7 @@
 //   * A CTA owns a contiguous range of 128-pixel chunks over (image, row,
 //     chunk) — balanced to one chunk — and its warps take the range's chunks
 //     round robin (lane = 4 consecutive pixels, 128-bit streaming loads and
-//     stores).  One thread bulk-prefetches input rows two rows ahead into L2.
+//     stores).  One thread bulk-prefetches input rows one row ahead into L2.
 //   * Brackets are evaluated for two pixels at a time on the FP32x2 pipe
 //     (__fmul2_rz / __fadd2_rz / __ffma2_rn); the merged grid slots carry a
 //     padding guide cell so a guide of exactly 1.0 needs no min().
@@ -49,7 +49,7 @@ constexpr int kChunk = 32 * kPx;       // pixels per warp chunk
 constexpr int kRing = FWD_RING;        // per-row grid slot buffers
 constexpr int kAhead = kRing - 1;      // rows of slots produced ahead of the one consumed
 #ifndef FWD_L2ROWS
-#define FWD_L2ROWS 2
+#define FWD_L2ROWS 1
 #endif
 constexpr int kL2Rows = FWD_L2ROWS;    // rows of L2 prefetch distance for the input
 constexpr uint32_t kSmemPlanes = FWD_PLANES;
