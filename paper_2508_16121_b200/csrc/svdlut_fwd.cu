@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) fused_fwd_kernel(FwdParams 
   if (threadIdx.x == blockDim.x - 32 && g_begin < g_end) {
     const long long r0 = g_begin / cpr;
     const int b0 = (int)(r0 / p.h), y0r = (int)(r0 - (long long)b0 * p.h);
-    const int y_end = (int)min((long long)p.h, (long long)y0r + kL2Rows + 2);
+    const int y_end = (int)min((long long)p.h, (long long)y0r + kL2Rows + 1);
     for (int yy = y0r; yy < y_end; ++yy) {
       Src<IN>::prefetch_row(Src<IN>::image(p.in, b0, pl), pl, plane_len, yy, p.w);
       if (LOSS) Src<kF32>::prefetch_row(Src<kF32>::image(p.target, b0, pl), pl, plane_len, yy, p.w);
