@@ -40,6 +40,10 @@ namespace svdlut {
 constexpr int kBwdWarps = BWD_NW;
 constexpr int kBPx = 4;
 constexpr uint32_t kMagic = 0x4B000000u;
+#ifndef BWD_XR_COPIES
+#define BWD_XR_COPIES 4
+#endif
+constexpr int kXRCopies = BWD_XR_COPIES;  // lane-group copies of the row's xc sums
 constexpr int kBwdL2Rows = 2;  // rows of L2 prefetch distance (X and gY planes)
 
 // LUT chunk planes (bit 3*pair + chunk) staged in shared memory by TMA; the
@@ -344,12 +348,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const uint32_t slotK0 = bsmem_addr(slots) - kMagic * 16u;
   int* Ei = reinterpret_cast<int*>(Es);
   int* Rrow = Ei + A.total;         // 2 rows x [Rx 3*ds | Rc 3*ds]
-  // 2 rows x 3 lane-group copies (lanes 0-11, 12-23, 24-31: lanes with the
-  // same corner x channel rotation never share a copy) x the row's xc plane
-  // [c 3][vx ds][vc ds]
+  // 2 rows x kXRCopies lane-group copies (4: lanes 0-7, 8-15, ...; lanes
+  // with the same corner x channel rotation never share a copy) x the row's
+  // xc plane [c 3][vx ds][vc ds]
   int* XRrow = Rrow + 12 * ds;
   const int xr_size = 3 * ds * ds;
-  const uint32_t sXR = bsmem_addr(XRrow) + (uint32_t)((lane / 12) * xr_size) * 4u;
+  const uint32_t sXR = bsmem_addr(XRrow) + (uint32_t)((kXRCopies == 3 ? lane / 12 : lane / (32 / kXRCopies)) * xr_size) * 4u;
   // byte address of LUT pair pr's cell from 2^23-biased index bits:
   // lutE[pr] + bits_a * (dt+1)*12 + bits_b * 12
   const uint32_t rowB = (uint32_t)(dt + 1) * 12u;
@@ -398,7 +402,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
           dst += plane_bytes;
         }
     }
-    for (int i = threadIdx.x; i < A.total + 12 * ds + 6 * xr_size; i += blockDim.x) Ei[i] = 0;
+    for (int i = threadIdx.x; i < A.total + 12 * ds + 2 * kXRCopies * xr_size; i += blockDim.x) Ei[i] = 0;
     float gm = 0.f;
     if (!DYN) {
       gm = p.gmax[b];
@@ -578,8 +582,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // cycles per LDS.128, tools/microbench/bwd_lds.txt); the atomics of
       // lanes that share a cell are spread over twelve words by the lane's
       // corner x channel rotation (3.6 cycles per ATOMS instead of 10).
-      int* XR = XRrow + (y & 1) * 3 * xr_size;
-      const uint32_t sXRy = sXR + (uint32_t)((y & 1) * 3 * xr_size) * 4u;
+      int* XR = XRrow + (y & 1) * kXRCopies * xr_size;
+      const uint32_t sXRy = sXR + (uint32_t)((y & 1) * kXRCopies * xr_size) * 4u;
       float row_max = 0.f, row_ss = 0.f;  // fused L2 step: this thread's |gY| statistics of row y
       int row_big = 0;
       for (int x0 = warp * 128; x0 < p.w; x0 += kBwdWarps * 128) {
@@ -785,10 +789,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
       // this row's xc sums into E_xc and its x-vertex / guide-vertex sums;
       // the buffer is zeroed for row y + 2 (rows y + 1 use the other one)
       for (int i = threadIdx.x; i < xr_size; i += blockDim.x) {
-        const int v = XR[i] + XR[i + xr_size] + XR[i + 2 * xr_size];
-        XR[i] = 0;
-        XR[i + xr_size] = 0;
-        XR[i + 2 * xr_size] = 0;
+        int v = 0;
+#pragma unroll
+        for (int cp = 0; cp < kXRCopies; ++cp) {
+          v += XR[i + cp * xr_size];
+          XR[i + cp * xr_size] = 0;
+        }
         if (v != 0) {
           const int c = i / (ds * ds), r2 = i - c * ds * ds, vx = r2 / ds, vc = r2 - vx * ds;
           E_xc[i] += v;  // one writer per entry in this phase
@@ -928,7 +934,7 @@ static cudaError_t bwd_impl(const float* rgb, const float* gy, int batch, int h,
   const AccLayout A = AccLayout::make(dt, ds);
   const int nent = (ds - 1) * 3 * (ds - 1);
   const size_t staged = (size_t)kBwdStaged * L.plane_floats * 4;
-  const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds + 18 * ds * ds) * 4;
+  const size_t smem = staged + 2 * (size_t)nent * 16 + ((size_t)A.total + 12 * ds + 6 * kXRCopies * ds * ds) * 4;
   if (smem > (size_t)fwd_max_smem_bytes()) return cudaErrorInvalidValue;
   char* wp = (char*)ws;
   float* tables = (float*)wp;
