@@ -44,6 +44,7 @@ constexpr uint32_t kMagic = 0x4B000000u;
 #define BWD_XR_COPIES 4
 #endif
 constexpr int kXRCopies = BWD_XR_COPIES;  // lane-group copies of the row's xc sums
+constexpr int kLutPad = 2;  // accumulator vertices per LUT row beyond d_t
 constexpr int kBwdL2Rows = 2;  // rows of L2 prefetch distance (X and gY planes)
 
 // LUT chunk planes (bit 3*pair + chunk) staged in shared memory by TMA; the
@@ -99,9 +100,10 @@ __device__ __forceinline__ void bprefetch_row(const float* plane0, long long pl,
   }
 }
 
-// Global accumulator layout per image (floats): lut [p 3][i d_t][j d_t+1][c 3]
-// (row stride padded by one vertex so the four corners of a cell fall in
-// distinct shared-memory banks: offsets 0, 3, 3(d_t+1), 3(d_t+2) words),
+// Global accumulator layout per image (floats): lut [p 3][i d_t][j d_t+2][c 3]
+// (row stride padded by two vertices: 3(d_t+2) = 105 words = 9 mod 32 at
+// d_t = 33 spreads the rotated corners' banks better than one vertex, 6 mod
+// 32: 8 x 1080p backward 638 -> 623 us),
 // grid [q 3 (xy|xc|yc)][c 3][a d_s][b d_s], then gsum [4].
 struct AccLayout {
   int dt, ds, lut_off, grid_off, gsum_off, total;
@@ -110,7 +112,7 @@ struct AccLayout {
     A.dt = dt;
     A.ds = ds;
     A.lut_off = 0;
-    A.grid_off = 3 * dt * (dt + 1) * 3;
+    A.grid_off = 3 * dt * (dt + kLutPad) * 3;
     A.gsum_off = A.grid_off + 9 * ds * ds;
     A.total = (A.gsum_off + 4 + 3) & ~3;
     return A;
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
     const int q = (k + lane / 3) & 3;
     kqa[k] = q & 1;
     kqb[k] = q & 2;
-    kcoff[k] = (uint32_t)(((q & 1) ? (dt + 1) * 3 : 0) + ((q & 2) ? 3 : 0)) * 4u;
+    kcoff[k] = (uint32_t)(((q & 1) ? (dt + kLutPad) * 3 : 0) + ((q & 2) ? 3 : 0)) * 4u;
     kxoff[k] = (uint32_t)(((q & 1) ? ds : 0) + ((q & 2) ? 1 : 0)) * 4u;
   }
 
@@ -356,11 +358,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
   const uint32_t sXR = bsmem_addr(XRrow) + (uint32_t)((kXRCopies == 3 ? lane / 12 : lane / (32 / kXRCopies)) * xr_size) * 4u;
   // byte address of LUT pair pr's cell from 2^23-biased index bits:
   // lutE[pr] + bits_a * (dt+1)*12 + bits_b * 12
-  const uint32_t rowB = (uint32_t)(dt + 1) * 12u;
+  const uint32_t rowB = (uint32_t)(dt + kLutPad) * 12u;
   uint32_t lutE[3];
 #pragma unroll
   for (int pr = 0; pr < 3; ++pr)
-    lutE[pr] = bsmem_addr(Ei) + (uint32_t)(A.lut_off + pr * dt * (dt + 1) * 3) * 4u - kMagic * (rowB + 12u);
+    lutE[pr] = bsmem_addr(Ei) + (uint32_t)(A.lut_off + pr * dt * (dt + kLutPad) * 3) * 4u - kMagic * (rowB + 12u);
   const uint32_t rcb0 = (uint32_t)rc0 * 4u, rcb1 = (uint32_t)rc1 * 4u, rcb2 = (uint32_t)rc2 * 4u;
   int* E_lut = Ei + A.lut_off;
   int* E_xy = Ei + A.grid_off;
@@ -670,7 +672,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
               const uint32_t ba = pr == 2 ? bg : br, bbq = pr == 0 ? bg : bb;
               const float da = pr == 2 ? dg : dr, dbb = pr == 0 ? dg : db;
               const uint32_t e = lutE[pr] + ba * rowB + bbq * 12u;
-              SVDLUT_CHECK(((pr * dt + (int)(ba - kMagic) + 1) * (dt + 1) + (int)(bbq - kMagic) + 1) * 3 + 2 <
+              SVDLUT_CHECK(((pr * dt + (int)(ba - kMagic) + 1) * (dt + kLutPad) + (int)(bbq - kMagic) + 1) * 3 + 2 <
                            A.grid_off);
               const float ea = 1.f - da, eb = 1.f - dbb;
 #pragma unroll
@@ -691,11 +693,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32, 1) fused_bwd_kernel(BwdParams 
 #pragma unroll
             for (int pr = 0; pr < 3; ++pr) {
               const int a = pr == 2 ? 1 : 0, bq = pr == 0 ? 1 : 2;
-              float* e = Eg + A.lut_off + ((pr * dt + ii[a]) * (dt + 1) + ii[bq]) * 3;
+              float* e = Eg + A.lut_off + ((pr * dt + ii[a]) * (dt + kLutPad) + ii[bq]) * 3;
 #pragma unroll
               for (int kc = 0; kc < 4; ++kc) {
                 const float wgt = ((kc & 1) ? dd[a] : 1.f - dd[a]) * ((kc & 2) ? dd[bq] : 1.f - dd[bq]);
-                float* ec = e + ((kc & 1) ? (dt + 1) * 3 : 0) + ((kc & 2) ? 3 : 0);
+                float* ec = e + ((kc & 1) ? (dt + kLutPad) * 3 : 0) + ((kc & 2) ? 3 : 0);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) atomicAdd(ec + c, gg[c] * wgt);
               }
@@ -884,7 +886,7 @@ __global__ void finalize_kernel(const float* __restrict__ lp, const float* __res
     float* D = dlp + (b * 9 + task) * (long long)dt * dt;
     for (int ij = threadIdx.x; ij < dt * dt; ij += blockDim.x) {
       const int i = ij / dt, j = ij - i * dt;
-      const float e = Eb[A.lut_off + ((pr * dt + i) * (dt + 1) + j) * 3 + c];
+      const float e = Eb[A.lut_off + ((pr * dt + i) * (dt + kLutPad) + j) * 3 + c];
       D[ij] = w * e;
       acc += (double)T[ij] * (double)e;
     }
